@@ -1,0 +1,370 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 CAGNET full-batch GCN training step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config reddit]
+                    [--strategy 1d|1.5d|2d|3d] [--repl c] [--impl ours|reference]
+
+N > 1 is launched with torchrun (one process per GPU, NCCL over NVLink).
+A step is one full-batch training epoch (forward, loss, backward, SGD) of the
+GCN on the synthetic graph of BASELINE.json's config, inputs resident in HBM.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GCN epoch time (ms) at 1/2/4/8 B200 per 1D/1.5D/2D/3D; SpMM GB/s vs HBM"
+REDDIT_N, REDDIT_E = 232965, 114848857
+CONFIGS = {
+    # BASELINE.json configs[0]
+    "config1": dict(n=4096, degree=16.0, dims=[128, 16, 8], generator="reference",
+                    label="ER n=4096 d=16, 2-layer GCN {128,16,8}"),
+    # configs[1]/[2]: Reddit-shaped, the bit-exact reference ER generator on the GPU
+    "reddit": dict(n=REDDIT_N, degree=REDDIT_E / REDDIT_N, dims=[602, 16, 16, 41],
+                   generator="reference",
+                   label="Reddit-shaped ER n=232965 nnz=115M f=602, 3-layer GCN {602,16,16,41}"),
+    # configs[3]: Amazon-shaped, O(nnz) ER-shaped generator
+    "amazon": dict(n=14249639, degree=230788269 / 14249639, dims=[300, 16, 16, 24],
+                   generator="skip",
+                   label="Amazon-shaped ER n=14.2M nnz=245M f=300, 3-layer GCN {300,16,16,24}"),
+    # configs[4]: Protein-shaped (BASELINE's 1.3B edges)
+    "protein": dict(n=8745542, degree=1.3e9 / 8745542, dims=[128, 16, 16, 256], generator="skip",
+                    label="Protein-shaped ER n=8.7M nnz=1.3B f=128, 3-layer GCN {128,16,16,256}"),
+}
+SEEDS = dict(seed_graph=1, seed_features=2, seed_labels=3)
+SEED_W, LR = 4, 0.5
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="reddit", choices=sorted(CONFIGS))
+    p.add_argument("--strategy", default="1d", choices=["1d", "1.5d", "2d", "3d"])
+    p.add_argument("--repl", type=int, default=0, help="1.5D replication (default 2 when 1.5d)")
+    p.add_argument("--block", type=int, default=0)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--sample-div", type=int, default=16,
+                   help="CPU sample = the config's graph with n/div vertices, same degree")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref = the unmodified reference sources) on a sample
+# ---------------------------------------------------------------------------
+def reference_sample(cfg, div, ranks, epochs, warmup):
+    """Times the reference's run_distributed (1D, `ranks` threads) on the
+    config's graph scaled to n/div vertices at the same average degree and
+    feature widths; returns (per-epoch seconds list, sample dict)."""
+    import oracle
+    ref = oracle.Ref()
+    n_s = max(cfg["n"] // div, 64)
+    dims = cfg["dims"]
+    t0 = time.perf_counter()
+    data = ref.dataset(n_s, min(cfg["degree"], n_s - 1), dims[0], dims[-1], 1, 2, 3)
+    gen_s = time.perf_counter() - t0
+    model = ref.model(dims, SEED_W, LR)
+    times = []
+    for e in range(warmup + epochs):
+        res = ref.distributed(data, model, "1d", ranks, 1, 0, epochs=1)
+        if e >= warmup:
+            times.append(res.seconds)
+    sample = dict(n=n_s, nnz=int(data.nnz), dims=dims, ranks=ranks, gen_s=round(gen_s, 2))
+    return times, sample
+
+
+def full_nnz(cfg):
+    return cfg["n"] * cfg["degree"] + cfg["n"]  # E[raw nnz] + self loops
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    try:
+        import oracle
+        if not oracle.ref_available():
+            raise FileNotFoundError("oracle/_ref/libcagnet_ref.so missing")
+    except Exception as e:  # pragma: no cover
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}))
+        return
+    threads = max(1, min(os.cpu_count() or 1, 16))
+    times, sample = reference_sample(cfg, args.sample_div, threads, args.steps, args.warmup)
+    scale = full_nnz(cfg) / sample["nnz"]
+    ms = statistics.median(times) * 1e3 * scale
+    desc = (f"reference run_distributed 1D P={threads} threads on n={sample['n']} "
+            f"(nnz={sample['nnz']}, same degree and dims), epoch time x{scale:.1f} "
+            f"(linear in nnz) to the full graph")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["label"], "strategy": "1d", "ranks": threads},
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": threads,
+                         "kind": "reference", "sample": desc},
+        "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def load_traffic(kernel_name):
+    """dram bytes per launch of `kernel_name` from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(path)).get(kernel_name)
+    except Exception:
+        return None
+
+
+def run_ours(args, cfg):
+    import torch
+    import paper_2005_03300_b200 as cg
+
+    rank, world, local = dist_env()
+    N = args.gpus
+    if world != N:
+        raise SystemExit(f"--gpus {N} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    kind = args.strategy
+    repl = args.repl or (2 if kind == "1.5d" else 1)
+    strat = cg.Strategy(kind, N, repl, args.block)
+
+    # NCCL bootstrap for the library's own communicators.
+    nid = None
+    if world > 1:
+        buf = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(cg.comm_unique_id()), dtype=torch.uint8))
+        pg.broadcast(buf, 0)
+        nid = bytes(buf.cpu().numpy().tobytes())
+
+    t0 = time.perf_counter()
+    data = cg.generate_dataset(cfg["n"], cfg["degree"], cfg["dims"][0], cfg["dims"][-1],
+                               device=local, generator=cfg["generator"], **SEEDS)
+    gen_s = time.perf_counter() - t0
+    model = cg.init_glorot(cfg["dims"], SEED_W, LR)
+    trainer = cg.make_trainer(data, model, strat, rank, nid)
+    trainer.distribute()
+    stream = torch.cuda.ExternalStream(trainer.stream())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if pg:
+            pg.barrier()
+            torch.cuda.synchronize()
+
+    # warm-up (untimed)
+    trainer.run_epochs(max(args.warmup, 1))
+    barrier()
+
+    # ---- timed region: K epochs, device events on the trainer's stream -------
+    trainer.set_timing(True)
+    trainer.profile_reset()
+    launches0 = cg.kernel_launches()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        start.record(stream)
+        for _ in range(args.steps):
+            trainer.epoch_async()
+        end.record(stream)
+        barrier()
+    launches = cg.kernel_launches() - launches0
+    trainer.set_timing(False)
+    losses = trainer.losses()
+    ms_total = start.elapsed_time(end)
+    prof = trainer.profile()
+
+    ms_t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if pg:
+        pg.all_reduce(ms_t, op=pg.ReduceOp.MAX)
+    ms_step = float(ms_t.item()) / args.steps
+
+    # ---- end-to-end: the public host-buffer call, H2D + epoch + D2H ----------
+    r0, r1, c0, c1, _ = trainer.tile(rank, cfg["dims"][0])
+    feats = data.features()[r0:r1, c0:c1]
+    x_pin = torch.empty(feats.shape, dtype=torch.float32, pin_memory=True)
+    x_pin.numpy()[:] = feats
+    lab_pin = torch.empty(r1 - r0, dtype=torch.int32, pin_memory=True)
+    lab_pin.numpy()[:] = data.labels()[r0:r1]
+    trainer.step_host(x_pin.numpy(), lab_pin.numpy())  # warm
+    barrier()
+    t1 = time.perf_counter()
+    for _ in range(args.steps):
+        trainer.step_host(x_pin.numpy(), lab_pin.numpy())
+    barrier()
+    e2e_ms = (time.perf_counter() - t1) * 1e3 / args.steps
+    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if pg:
+        pg.all_reduce(e2e_t, op=pg.ReduceOp.MAX)
+    e2e_ms = float(e2e_t.item())
+    h2d = feats.size * 4 + (r1 - r0) * 4
+
+    # ---- roofline of the dominant kernel (per-launch CUDA events) ------------
+    dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"]) if prof else (None, None)
+    peaks = load_peaks()
+    peak = peaks.get("hbm_gbs", 6650.0)
+    roof = None
+    if dom:
+        per_launch_ms = dom["ms"] / dom["launches"]
+        bytes_per_launch = dom["bytes"] / dom["launches"]
+        achieved = bytes_per_launch / (per_launch_ms * 1e-3) / 1e9
+        roof = {"kernel": dom_name, "bound": "hbm", "achieved": round(achieved, 1),
+                "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": load_traffic(dom_name),
+                "bytes_per_launch": bytes_per_launch, "ms_per_launch": round(per_launch_ms, 4),
+                "share_of_step": round(dom["ms"] / max(ms_total, 1e-9), 4),
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return
+
+    cpu = None
+    if N == 1 and not args.no_cpu_baseline:
+        try:
+            times, sample = reference_sample(cfg, args.sample_div, 1, 1, 0)
+            scale = full_nnz(cfg) / sample["nnz"]
+            cpu = {"value": round(times[0] * 1e3 * scale, 1), "unit": "ms", "cores": 1,
+                   "kind": "reference",
+                   "sample": f"reference run_distributed 1D P=1 (serial) on n={sample['n']} "
+                             f"nnz={sample['nnz']} (same degree/dims), one epoch, x{scale:.1f} "
+                             f"linear-in-nnz extrapolation to the full graph"}
+        except Exception as e:
+            cpu = {"value": None, "unit": "ms", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    clk = clocks.summary()
+    line = {
+        "metric": METRIC, "value": round(ms_step, 4), "unit": "ms", "n_gpus": N,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": cfg["label"], "strategy": kind, "ranks": N, "repl": repl,
+                   "block": args.block, "generator": cfg["generator"],
+                   "l2": "inputs larger than L2 (CSR A+A^T and H0 > 126 MB)"},
+        "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": 8},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "kernels": {k: {"launches": v["launches"], "ms_per_launch": round(v["ms"] / v["launches"], 4),
+                        "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}
+                    for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
+        "loss_last": float(losses[-1]) if len(losses) else None,
+        "setup_s": {"dataset_gen": round(gen_s, 2)},
+    }
+    print(json.dumps(line))
+    if pg:
+        pg.destroy_process_group()
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

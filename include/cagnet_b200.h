@@ -1,0 +1,248 @@
+/*
+ * cagnet_b200 — C-ABI of the B200-native CAGNET full-batch GCN training step
+ * (arXiv 2005.03300).  Plain pointers and sizes only; no torch or C++ types.
+ *
+ * Two levels:
+ *   1. kernel seams  — the device equivalents of the free functions the
+ *      reference strategies call: spmm_add, gemm_add, the fused
+ *      log_softmax/NLL tile, relu/hadamard epilogues, sgd_step.  All device
+ *      pointers are caller-owned; `stream` is a cudaStream_t (NULL = legacy
+ *      default stream).
+ *   2. API level     — the reference's graph-loading / partitioning /
+ *      training-loop API (dataset.hpp, gnn.hpp, dist.hpp) with device-resident
+ *      state behind opaque handles owned by the library until *_free.
+ *
+ * Every function returns CAGNET_OK (0) or an error code; the message for the
+ * calling thread is available from cagnet_last_error().  Shape errors are
+ * validated on the host before any launch (mirroring the reference's
+ * std::invalid_argument "who: shape ..." messages).
+ */
+#ifndef CAGNET_B200_H
+#define CAGNET_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define CAGNET_API __attribute__((visibility("default")))
+#else
+#define CAGNET_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CAGNET_OK 0
+#define CAGNET_EINVAL 1    /* std::invalid_argument in the reference */
+#define CAGNET_ECUDA 2     /* CUDA runtime / launch failure */
+#define CAGNET_ENCCL 3     /* NCCL failure (collective misuse, peer loss) */
+#define CAGNET_ERUNTIME 4  /* std::runtime_error in the reference (I/O, divergence) */
+
+/* gemm epilogues (fused after the tcgen05 accumulation) */
+#define CAGNET_EPI_NONE 0        /* C (+)= op(A) op(B) */
+#define CAGNET_EPI_RELU 1        /* C = Z; aux_out = relu(Z)         dense.cpp:80-85 */
+#define CAGNET_EPI_RELU_PRIME 2  /* C = acc * (aux > 0)              dense.cpp:72-92 */
+
+/* strategies (dist.hpp:41) */
+#define CAGNET_1D 0
+#define CAGNET_15D 1
+#define CAGNET_2D 2
+#define CAGNET_3D 3
+
+/* dataset generators */
+#define CAGNET_GEN_REFERENCE 0  /* bit-exact reference ER (csr.cpp:195-218), O(n^2) draws on GPU */
+#define CAGNET_GEN_SKIP 1       /* O(nnz) geometric-skip ER-shaped graph (Amazon/Protein scale) */
+
+CAGNET_API const char* cagnet_last_error(void);
+CAGNET_API int cagnet_version(void);
+CAGNET_API int cagnet_device_count(int* out);
+
+/* ------------------------------------------------------------------------ */
+/* 0. host-only partition geometry (no GPU needed)                           */
+/* ------------------------------------------------------------------------ */
+
+/* block_range (dist_common.cpp:29-36): out2 = {begin, end} of part idx. */
+CAGNET_API int cagnet_block_range(int64_t n, int parts, int idx, int64_t* out2);
+/* make_grid (dist_common.cpp:55-65): out4 = {grid kind, rows, cols, layers};
+ * CAGNET_EINVAL for impossible shapes (non-square 2D, non-cube 3D, c ∤ P). */
+CAGNET_API int cagnet_grid_shape(int kind, int ranks, int repl, int* out4);
+/* ProcessGrid groups (grid.cpp:142-189): which 0 world, 1 row, 2 column,
+ * 3 fiber; members ascending (capacity `ranks`). */
+CAGNET_API int cagnet_grid_group(int kind, int ranks, int repl, int rank, int which, int* members,
+                      int* count);
+/* Trainer::tile_rows / tile_cols / tile_owner without a trainer:
+ * out5 = {r0, r1, c0, c1, owner}. */
+CAGNET_API int cagnet_tile_geometry(int kind, int ranks, int repl, int64_t n, int rank, int64_t width,
+                         int64_t* out5);
+
+/* ------------------------------------------------------------------------ */
+/* 1. kernel seams                                                           */
+/* ------------------------------------------------------------------------ */
+
+/* spmm_add (csr.cpp:164-179; csr.hpp:71-75): T[i,:] (+)= sum_k vals[k] * H[col[k],:]
+ * in ascending-nonzero order per row.  row_ptr int64[n_rows+1], col_idx int32[nnz],
+ * vals fp32[nnz].  H is n_cols x f (leading dim ldh), T is n_rows x f (ldt).
+ * accumulate=0 overwrites T (spmm, csr.cpp:181-185). */
+CAGNET_API int cagnet_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                        const int32_t* col_idx, const float* vals, const float* H, int64_t ldh,
+                        int32_t f, float* T, int64_t ldt, int accumulate, void* stream);
+
+/* gemm_add / gemm (dense.cpp:37-70; dense.hpp:63-71): C (+)= op(A) op(B) on
+ * tcgen05 tensor cores, split-TF32 (3 MMAs: hi*hi + hi*lo + lo*hi), fp32
+ * accumulation in TMEM.  op(A) is m x k, op(B) is k x n; A is stored
+ * (ta ? k x m : m x k) with leading dim lda, B (tb ? n x k : k x n) with ldb.
+ * Epilogue per CAGNET_EPI_*: RELU writes Z to C and relu(Z) to aux_out (ldao);
+ * RELU_PRIME multiplies by 1[aux > 0] (ldaux).  Large k is split across CTAs
+ * and reduced deterministically. */
+CAGNET_API int cagnet_gemm_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A,
+                    int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                    int accumulate, int epilogue, const float* aux, int64_t ldaux,
+                    float* aux_out, int64_t ldao, void* stream);
+
+/* log_softmax_rows + nll_tile fused (dense.cpp:94-136).  Z holds full rows
+ * (rows x cols, ldz).  Writes the column tile [c0, c1) of log-probabilities to
+ * logp (ldl) and of the gradient (softmax - onehot)/train_total on masked rows
+ * to G (ldg); *loss_partial (device fp64) receives the undivided
+ * -sum logp[y] over masked rows whose label lies in [c0, c1).
+ * labels int32[rows] (may be NULL when G is NULL), mask uint8[rows] (NULL = all). */
+CAGNET_API int cagnet_logsoftmax_nll_f32(const float* Z, int64_t rows, int32_t cols, int64_t ldz,
+                              int32_t c0, int32_t c1, float* logp, int64_t ldl, float* G,
+                              int64_t ldg, const int32_t* labels, const uint8_t* mask,
+                              int64_t train_total, double* loss_partial, void* stream);
+
+/* relu (dense.cpp:80-85), out-of-place, rows x cols with leading dims. */
+CAGNET_API int cagnet_relu_f32(const float* Z, int64_t rows, int32_t cols, int64_t ldz, float* H,
+                    int64_t ldh, void* stream);
+
+/* sgd_step (gnn.cpp:106-120): W -= lr * Y elementwise over `count` floats. */
+CAGNET_API int cagnet_sgd_f32(float* W, const float* Y, int64_t count, float lr, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* 2. API level                                                              */
+/* ------------------------------------------------------------------------ */
+
+typedef struct cagnet_csr_s* cagnet_csr_t;         /* device CSR (int64 row_ptr, int32 col, fp32 vals) */
+typedef struct cagnet_dataset_s* cagnet_dataset_t; /* device GraphDataset (dataset.hpp:31-45) */
+typedef struct cagnet_trainer_s* cagnet_trainer_t; /* one rank of a Trainer (dist.hpp:83-131) */
+
+/* --- device CSR ------------------------------------------------------------ */
+CAGNET_API int cagnet_csr_upload(int device, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                      const int64_t* col_idx, const double* vals, cagnet_csr_t* out);
+/* shape = {n_rows, n_cols, nnz} */
+CAGNET_API int cagnet_csr_shape(cagnet_csr_t a, int64_t* shape);
+/* Any output may be NULL.  vals are the fp32 device values. */
+CAGNET_API int cagnet_csr_download(cagnet_csr_t a, int64_t* row_ptr, int64_t* col_idx, float* vals);
+/* Raw device pointers (for the kernel seams). */
+CAGNET_API int cagnet_csr_device_ptrs(cagnet_csr_t a, const int64_t** row_ptr, const int32_t** col_idx,
+                           const float** vals);
+CAGNET_API int cagnet_csr_free(cagnet_csr_t a);
+
+/* generate_erdos_renyi (csr.cpp:195-218) on the GPU, bit-exact: every ordered
+ * pair draws once from the same xoshiro256** stream (rows start at a GF(2)
+ * jump of u*(n-1) draws). */
+CAGNET_API int cagnet_er_generate(int device, int64_t n, double degree, uint64_t seed, cagnet_csr_t* out);
+/* add_self_loops_and_normalize (csr.cpp:94-116) on the GPU: fp64 1/sqrt(d_i d_j) rounded to fp32. */
+CAGNET_API int cagnet_csr_normalize(cagnet_csr_t raw, cagnet_csr_t* out);
+/* transpose (csr.cpp:118-138) on the GPU (stable radix sort by column). */
+CAGNET_API int cagnet_csr_transpose(cagnet_csr_t a, cagnet_csr_t* out);
+/* extract_block (csr.cpp:140-162) on the GPU. */
+CAGNET_API int cagnet_csr_extract_block(cagnet_csr_t a, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                             cagnet_csr_t* out);
+
+/* --- datasets (dataset.hpp:46-93) ------------------------------------------- */
+/* generate_dataset(n, d, f, C, sg, sf, sl) built on `device`: ER (generator per
+ * CAGNET_GEN_*), normalization, transpose, U[0,1) features, uniform labels,
+ * all-ones mask. */
+CAGNET_API int cagnet_dataset_generate(int device, int64_t n, double degree, int64_t num_features,
+                            int64_t num_classes, uint64_t seed_graph, uint64_t seed_features,
+                            uint64_t seed_labels, int generator, cagnet_dataset_t* out);
+/* make_dataset (dataset.cpp:76-90) from a raw host CSR (unit values implied),
+ * fp64 features (n x f), labels int64[n], mask uint8[n] (NULL = all ones). */
+CAGNET_API int cagnet_dataset_make(int device, int64_t n, const int64_t* raw_row_ptr,
+                        const int64_t* raw_col_idx, const double* features, int64_t f,
+                        const int64_t* labels, const uint8_t* mask, int64_t num_classes,
+                        cagnet_dataset_t* out);
+/* info = {n, nnz, num_features, num_classes, train_count} */
+CAGNET_API int cagnet_dataset_info(cagnet_dataset_t d, int64_t* info);
+/* which: 0 = adj, 1 = adj_t.  Borrowed handle, owned by the dataset. */
+CAGNET_API int cagnet_dataset_csr(cagnet_dataset_t d, int which, cagnet_csr_t* out);
+CAGNET_API int cagnet_dataset_features(cagnet_dataset_t d, float* out /* n x f, host */);
+CAGNET_API int cagnet_dataset_labels(cagnet_dataset_t d, int64_t* out);
+CAGNET_API int cagnet_dataset_free(cagnet_dataset_t d);
+
+/* --- model (gnn.hpp:29-42) --------------------------------------------------- */
+/* init_glorot (gnn.cpp:24-44): fp64 weights for every layer, concatenated
+ * (layer l is dims[l] x dims[l+1], row major), from one seeded generator. */
+CAGNET_API int cagnet_init_glorot(const int64_t* dims, int ndims, uint64_t seed, double* weights);
+
+/* --- training (dist.hpp:43-150) --------------------------------------------- */
+/* NCCL bootstrap: rank 0 creates the id, the launcher broadcasts its 128 bytes. */
+CAGNET_API int cagnet_comm_unique_id(uint8_t* out128);
+
+/* Creates rank `rank` of Strategy{kind, ranks, repl, block} on the dataset's
+ * device.  dims[ndims] are the layer widths; weights are the fp64 Glorot
+ * weights concatenated layer by layer (gnn.hpp:29-35), rounded to fp32 on
+ * device.  nccl_id may be NULL when ranks == 1. */
+CAGNET_API int cagnet_trainer_create(cagnet_dataset_t data, const int64_t* dims, int ndims,
+                          const double* weights, double learning_rate, int kind, int ranks,
+                          int repl, int block, int rank, const uint8_t* nccl_id,
+                          cagnet_trainer_t* out);
+/* Trainer::distribute (dist.hpp:87): per-rank CSR blocks and H0 tiles, on device. */
+CAGNET_API int cagnet_trainer_distribute(cagnet_trainer_t t);
+/* Trainer::forward_layer (1-based l) and Trainer::epoch (dist_common.cpp:97-100). */
+CAGNET_API int cagnet_trainer_forward_layer(cagnet_trainer_t t, int l);
+CAGNET_API int cagnet_trainer_epoch(cagnet_trainer_t t, double* loss);
+CAGNET_API int cagnet_trainer_run_epochs(cagnet_trainer_t t, int epochs, double* losses);
+/* Queues one epoch without waiting (losses stay on the device until read). */
+CAGNET_API int cagnet_trainer_epoch_async(cagnet_trainer_t t);
+/* Every epoch loss so far (waits for queued epochs); count = total epochs. */
+CAGNET_API int cagnet_trainer_losses(cagnet_trainer_t t, double* out, int cap, int* count);
+/* Blocks until all work queued by this rank has finished. */
+CAGNET_API int cagnet_trainer_sync(cagnet_trainer_t t);
+/* tile_rows / tile_cols / tile_owner (dist.hpp:96-101): out = {r0, r1, c0, c1, owner} */
+CAGNET_API int cagnet_trainer_tile(cagnet_trainer_t t, int rank, int64_t width, int64_t* out);
+/* Local tiles of h[layer] (0 = features .. L-1 = log-probabilities) and g[idx]
+ * (idx 0..L-2), downloaded as fp32 rows x cols (dense, ld = cols). */
+CAGNET_API int cagnet_trainer_h_tile(cagnet_trainer_t t, int layer, float* out);
+CAGNET_API int cagnet_trainer_g_tile(cagnet_trainer_t t, int idx, float* out);
+/* Replicated weights / weight gradients of layer l (dims[l] x dims[l+1]). */
+CAGNET_API int cagnet_trainer_weight(cagnet_trainer_t t, int l, float* out);
+CAGNET_API int cagnet_trainer_y(cagnet_trainer_t t, int l, float* out);
+/* Local partition structure: part index within this rank's a_parts/at_parts
+ * (which 0 = A, 1 = A^T).  shape = {n_rows, n_cols, nnz}. */
+CAGNET_API int cagnet_trainer_num_parts(cagnet_trainer_t t, int* out);
+CAGNET_API int cagnet_trainer_part(cagnet_trainer_t t, int which, int part, cagnet_csr_t* out);
+/* Per-category device time of the last epoch in ms: [spmm, gemm, elementwise,
+ * dbcast, sbcast, reduce, allgather, epoch_total] and per-category NCCL bytes
+ * received by this rank per the reference ledger conventions
+ * (runtime.cpp:142-184) accumulated since creation: [dbcast, sbcast, reduce, allgather]. */
+CAGNET_API int cagnet_trainer_stats(cagnet_trainer_t t, double* ms8, uint64_t* words_received4);
+/* Reference-ledger counters of this rank (ledger.hpp:41-47), 4 categories
+ * [dbcast, sbcast, reduce, allgather] x {messages, words_sent, words_received,
+ * payload_words, calls}. */
+CAGNET_API int cagnet_trainer_ledger(cagnet_trainer_t t, uint64_t* out20);
+/* Enable/disable per-category CUDA-event timing (adds event records; default off). */
+CAGNET_API int cagnet_trainer_set_timing(cagnet_trainer_t t, int on);
+/* Per-launch CUDA-event profile, aggregated by kernel name (e.g. "spmm_f602"):
+ * out4 = {launches, total_ms, algorithmic_bytes, flops} (SURVEY §8(d) byte model). */
+CAGNET_API int cagnet_trainer_profile_count(cagnet_trainer_t t, int* n);
+CAGNET_API int cagnet_trainer_profile_entry(cagnet_trainer_t t, int i, char* name, int cap,
+                                            double* out4);
+CAGNET_API int cagnet_trainer_profile_reset(cagnet_trainer_t t);
+/* One epoch from HOST buffers (the end-to-end call): H2D of this rank's
+ * feature tile (dense rows x cols fp32, pinned for full speed) and label rows,
+ * the epoch, D2H of the loss (blocking). */
+CAGNET_API int cagnet_trainer_step_host(cagnet_trainer_t t, const float* x_tile,
+                                        const int32_t* labels_tile, double* loss);
+/* Total hot-path kernel launches issued by this library so far. */
+CAGNET_API int cagnet_kernel_launches(uint64_t* out);
+/* The compute stream the trainer launches on (a cudaStream_t). */
+CAGNET_API int cagnet_trainer_stream(cagnet_trainer_t t, void** out);
+CAGNET_API int cagnet_trainer_free(cagnet_trainer_t t);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CAGNET_B200_H */

@@ -1,0 +1,286 @@
+// TEST INFRASTRUCTURE — NOT PRODUCT CODE.
+//
+// A thin extern "C" shim over the UNMODIFIED reference sources
+// (/root/reference/proj/src/*.cpp, compiled in place by oracle/Makefile into
+// oracle/_ref/libcagnet_ref.so).  It lets the Python tests and bench.py's
+// `--impl reference` / `cpu_baseline` legs drive the reference's own public
+// C++ API:
+//   generate_dataset        dataset.hpp:54-57   (dataset.cpp:110-118)
+//   init_glorot             gnn.hpp:41-42       (gnn.cpp:24-44)
+//   forward/backward/sgd    gnn.hpp:51-67       (gnn.cpp:68-120)
+//   make_trainer/distribute dist.hpp:133-134    (dist_common.cpp:194-203)
+//   run_distributed         dist.hpp:149-150    (dist_common.cpp:205-222)
+// Only tests/, __graft_entry__.smoke() and bench.py's reference/cpu_baseline
+// legs may load this library.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "cagnet/dataset.hpp"
+#include "cagnet/dist.hpp"
+#include "cagnet/gnn.hpp"
+
+using namespace cagnet;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+struct RefResult {
+  std::vector<double> losses;
+  DenseMatrix h_final;
+  std::vector<DenseMatrix> y, g, w;
+  CommLedger ledger;
+  bool has_ledger = false;
+  double seconds = 0.0;
+};
+
+void copy_csr(const CsrMatrix& a, int64_t* row_ptr, int64_t* col_idx, double* vals) {
+  if (row_ptr)
+    for (std::size_t i = 0; i <= a.n_rows; ++i) row_ptr[i] = static_cast<int64_t>(a.row_ptr[i]);
+  if (col_idx)
+    for (std::size_t k = 0; k < a.nnz(); ++k) col_idx[k] = static_cast<int64_t>(a.col_idx[k]);
+  if (vals) std::memcpy(vals, a.values.data(), a.nnz() * sizeof(double));
+}
+
+void copy_dense(const DenseMatrix& m, double* out) {
+  if (out && m.words()) std::memcpy(out, m.data(), m.words() * sizeof(double));
+}
+
+Strategy make_strategy(int kind, int ranks, int repl, int block) {
+  Strategy s;
+  s.kind = static_cast<StrategyKind>(kind);
+  s.ranks = ranks;
+  s.repl = repl;
+  s.block = block;
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// --- datasets ------------------------------------------------------------
+void* ref_dataset_generate(uint64_t n, double degree, uint64_t f, uint64_t classes,
+                           uint64_t sg, uint64_t sf, uint64_t sl) {
+  GraphDataset* d = nullptr;
+  if (guarded([&] { d = new GraphDataset(generate_dataset(n, degree, f, classes, sg, sf, sl)); }))
+    return nullptr;
+  return d;
+}
+
+// Dataset from a raw (unnormalized) CSR plus features/labels, through make_dataset.
+void* ref_dataset_make(uint64_t n, const int64_t* row_ptr, const int64_t* col_idx,
+                       const double* features, uint64_t f, const int64_t* labels,
+                       uint64_t classes) {
+  GraphDataset* d = nullptr;
+  if (guarded([&] {
+        CsrMatrix raw;
+        raw.n_rows = raw.n_cols = n;
+        raw.row_ptr.assign(row_ptr, row_ptr + n + 1);
+        raw.col_idx.assign(col_idx, col_idx + row_ptr[n]);
+        raw.values.assign(static_cast<std::size_t>(row_ptr[n]), 1.0);
+        DenseMatrix x(n, f);
+        std::memcpy(x.data(), features, n * f * sizeof(double));
+        d = new GraphDataset(make_dataset(raw, std::move(x),
+                                          std::vector<int64_t>(labels, labels + n),
+                                          std::vector<uint8_t>(n, 1), classes));
+      }))
+    return nullptr;
+  return d;
+}
+
+void* ref_dataset_permute(void* data, uint64_t seed, int64_t* perm_out) {
+  GraphDataset* d = nullptr;
+  if (guarded([&] {
+        PermutedDataset p = permute_random(*static_cast<GraphDataset*>(data), seed);
+        if (perm_out)
+          for (std::size_t i = 0; i < p.perm.size(); ++i) perm_out[i] = static_cast<int64_t>(p.perm[i]);
+        d = new GraphDataset(std::move(p.dataset));
+      }))
+    return nullptr;
+  return d;
+}
+
+void ref_dataset_free(void* d) { delete static_cast<GraphDataset*>(d); }
+uint64_t ref_dataset_n(void* d) { return static_cast<GraphDataset*>(d)->n; }
+uint64_t ref_dataset_nnz(void* d) { return static_cast<GraphDataset*>(d)->adj.nnz(); }
+uint64_t ref_dataset_features_cols(void* d) { return static_cast<GraphDataset*>(d)->features.cols(); }
+uint64_t ref_dataset_classes(void* d) { return static_cast<GraphDataset*>(d)->num_classes; }
+
+void ref_dataset_csr(void* d, int which, int64_t* row_ptr, int64_t* col_idx, double* vals) {
+  const GraphDataset& g = *static_cast<GraphDataset*>(d);
+  copy_csr(which == 0 ? g.adj : g.adj_t, row_ptr, col_idx, vals);
+}
+void ref_dataset_features(void* d, double* out) { copy_dense(static_cast<GraphDataset*>(d)->features, out); }
+void ref_dataset_labels(void* d, int64_t* out) {
+  const auto& l = static_cast<GraphDataset*>(d)->labels;
+  std::memcpy(out, l.data(), l.size() * sizeof(int64_t));
+}
+
+// Raw ER generator (csr.cpp:195-218).
+int64_t ref_er_nnz(uint64_t n, double degree, uint64_t seed) {
+  int64_t nnz = -1;
+  guarded([&] { nnz = static_cast<int64_t>(generate_erdos_renyi(n, degree, seed).nnz()); });
+  return nnz;
+}
+int ref_er_generate(uint64_t n, double degree, uint64_t seed, int64_t* row_ptr, int64_t* col_idx) {
+  return guarded([&] { copy_csr(generate_erdos_renyi(n, degree, seed), row_ptr, col_idx, nullptr); });
+}
+
+// --- model ---------------------------------------------------------------
+void* ref_model_glorot(const uint64_t* dims, int ndims, uint64_t seed, double lr) {
+  GnnModel* m = nullptr;
+  if (guarded([&] {
+        std::vector<std::size_t> d(dims, dims + ndims);
+        m = new GnnModel(init_glorot(d, seed, lr));
+      }))
+    return nullptr;
+  return m;
+}
+void ref_model_free(void* m) { delete static_cast<GnnModel*>(m); }
+void ref_model_weight(void* m, int l, double* out) {
+  copy_dense(static_cast<GnnModel*>(m)->weights.at(static_cast<std::size_t>(l)), out);
+}
+
+// --- training --------------------------------------------------------------
+// Serial reference: epochs of forward_serial/backward_serial/sgd_step, keeping
+// the last epoch's tape and gradients (harness.cpp:118-133 pattern).
+void* ref_serial_run(void* data, void* model, int epochs) {
+  RefResult* r = nullptr;
+  if (guarded([&] {
+        const GraphDataset& d = *static_cast<GraphDataset*>(data);
+        GnnModel m = *static_cast<GnnModel*>(model);
+        auto res = std::make_unique<RefResult>();
+        ForwardTape tape;
+        BackwardResult back;
+        auto t0 = std::chrono::steady_clock::now();
+        for (int e = 0; e < epochs; ++e) {
+          tape = forward_serial(d, m);
+          back = backward_serial(d, m, tape);
+          sgd_step(m, back.y);
+          res->losses.push_back(back.loss);
+        }
+        res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        res->h_final = tape.h.back();
+        res->y = back.y;
+        res->g = back.g;
+        res->w = m.weights;
+        r = res.release();
+      }))
+    return nullptr;
+  return r;
+}
+
+// run_distributed (dist_common.cpp:205-222) with the given scheduler; the
+// timing brackets run_epochs only (generation and distribute() excluded).
+void* ref_dist_run(void* data, void* model, int kind, int ranks, int repl, int block,
+                   int epochs, int sched) {
+  RefResult* r = nullptr;
+  if (guarded([&] {
+        const GraphDataset& d = *static_cast<GraphDataset*>(data);
+        const GnnModel& m = *static_cast<GnnModel*>(model);
+        const Strategy s = make_strategy(kind, ranks, repl, block);
+        std::unique_ptr<Trainer> t = make_trainer(d, m, s);
+        t->distribute();
+        SimRuntime rt(t->grid(), static_cast<Scheduler>(sched));
+        auto t0 = std::chrono::steady_clock::now();
+        t->run_epochs(rt, epochs);
+        auto res = std::make_unique<RefResult>();
+        res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        res->losses = t->verified_losses();
+        res->h_final = t->assemble_h_final();
+        for (std::size_t i = 0; i + 1 < m.num_layers(); ++i) res->g.push_back(t->assemble_g(i));
+        res->y = t->verified_y();
+        res->w = t->verified_model().weights;
+        res->ledger = rt.ledger();
+        res->has_ledger = true;
+        r = res.release();
+      }))
+    return nullptr;
+  return r;
+}
+
+void ref_result_free(void* r) { delete static_cast<RefResult*>(r); }
+double ref_result_seconds(void* r) { return static_cast<RefResult*>(r)->seconds; }
+void ref_result_losses(void* r, double* out) {
+  const auto& l = static_cast<RefResult*>(r)->losses;
+  std::memcpy(out, l.data(), l.size() * sizeof(double));
+}
+void ref_result_h_final(void* r, double* out) { copy_dense(static_cast<RefResult*>(r)->h_final, out); }
+void ref_result_y(void* r, int l, double* out) { copy_dense(static_cast<RefResult*>(r)->y.at(l), out); }
+void ref_result_g(void* r, int l, double* out) { copy_dense(static_cast<RefResult*>(r)->g.at(l), out); }
+void ref_result_w(void* r, int l, double* out) { copy_dense(static_cast<RefResult*>(r)->w.at(l), out); }
+// counters = {messages, words_sent, words_received, payload_words, calls}
+int ref_result_ledger(void* r, int cat, int rank, uint64_t* counters) {
+  const RefResult& res = *static_cast<RefResult*>(r);
+  if (!res.has_ledger) return -1;
+  const CommCounter& c = res.ledger.at(static_cast<Category>(cat), rank);
+  counters[0] = c.messages;
+  counters[1] = c.words_sent;
+  counters[2] = c.words_received;
+  counters[3] = c.payload_words;
+  counters[4] = c.calls;
+  return 0;
+}
+
+// --- partition structure -----------------------------------------------------
+// Trainer::distribute() then read back every rank's a_parts/at_parts
+// (dist.hpp:65-76, exposed through Trainer::slots()).
+void* ref_trainer_distribute(void* data, void* model, int kind, int ranks, int repl, int block) {
+  Trainer* t = nullptr;
+  if (guarded([&] {
+        auto up = make_trainer(*static_cast<GraphDataset*>(data), *static_cast<GnnModel*>(model),
+                               make_strategy(kind, ranks, repl, block));
+        up->distribute();
+        t = up.release();
+      }))
+    return nullptr;
+  return t;
+}
+void ref_trainer_free(void* t) { delete static_cast<Trainer*>(t); }
+int ref_trainer_num_parts(void* t, int rank) {
+  return static_cast<int>(static_cast<Trainer*>(t)->slots().at(rank).a_parts.size());
+}
+// shape = {n_rows, n_cols, nnz}
+void ref_trainer_part_shape(void* t, int rank, int which, int part, uint64_t* shape) {
+  const RankSlot& s = static_cast<Trainer*>(t)->slots().at(rank);
+  const CsrMatrix& a = (which == 0 ? s.a_parts : s.at_parts).at(part);
+  shape[0] = a.n_rows;
+  shape[1] = a.n_cols;
+  shape[2] = a.nnz();
+}
+void ref_trainer_part(void* t, int rank, int which, int part, int64_t* row_ptr, int64_t* col_idx,
+                      double* vals) {
+  const RankSlot& s = static_cast<Trainer*>(t)->slots().at(rank);
+  copy_csr((which == 0 ? s.a_parts : s.at_parts).at(part), row_ptr, col_idx, vals);
+}
+// tile geometry: {row_begin, row_end, col_begin, col_end, owner}
+void ref_trainer_tile(void* t, int rank, uint64_t width, int64_t* out) {
+  const Trainer& tr = *static_cast<Trainer*>(t);
+  BlockRange r = tr.tile_rows(rank), c = tr.tile_cols(rank, width);
+  out[0] = r.begin;
+  out[1] = r.end;
+  out[2] = c.begin;
+  out[3] = c.end;
+  out[4] = tr.tile_owner(rank);
+}
+
+}  // extern "C"

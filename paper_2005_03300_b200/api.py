@@ -1,0 +1,552 @@
+"""Python mirror of the reference's graph-loading, partitioning and
+training-loop API (proj/include/cagnet/{dataset,gnn,dist}.hpp) over the
+B200 C-ABI.  Names, argument meaning and error behaviour follow the
+reference; state lives on the GPU behind the library's handles.
+
+    data  = generate_dataset(n, degree, f, classes, sg, sf, sl)      # dataset.hpp:54-57
+    model = init_glorot(dims, seed, lr)                              # gnn.hpp:41-42
+    t     = make_trainer(data, model, Strategy("1d", ranks=1))       # dist.hpp:133-134
+    t.distribute(); losses = t.run_epochs(5)                          # dist.hpp:87-109
+    out   = run_distributed(factory, model, strat, epochs)            # dist.hpp:149-150
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import InvalidArgument, check, lib
+
+KINDS = {"1d": 0, "1.5d": 1, "2d": 2, "3d": 3}
+KIND_NAMES = {v: k for k, v in KINDS.items()}
+GENERATORS = {"reference": 0, "skip": 1}
+CATEGORIES = ("dbcast", "sbcast", "reduce", "allgather")
+COUNTER_FIELDS = ("messages", "words_sent", "words_received", "payload_words", "calls")
+
+
+# ---------------------------------------------------------------------------
+# partitioning (dist.hpp:25-58, grid.hpp)
+# ---------------------------------------------------------------------------
+def ceil_div(a: int, b: int) -> int:
+    if b == 0:
+        raise InvalidArgument(1, "ceil_div: zero divisor")
+    return (a + b - 1) // b
+
+
+def block_range(n: int, parts: int, idx: int) -> tuple[int, int]:
+    """dist_common.cpp:29-36 (through the C-ABI)."""
+    out = np.zeros(2, np.int64)
+    check(lib.cagnet_block_range(n, parts, idx, out))
+    return int(out[0]), int(out[1])
+
+
+def block_sizes(n: int, parts: int) -> list[int]:
+    return [e - b for b, e in (block_range(n, parts, i) for i in range(parts))]
+
+
+@dataclass
+class Strategy:
+    """dist.hpp:51-56: kind in {"1d", "1.5d", "2d", "3d"}, ranks P, 1.5D
+    replication c, 2D panel block width (0 = whole panel)."""
+    kind: str = "1d"
+    ranks: int = 1
+    repl: int = 1
+    block: int = 0
+
+    @property
+    def kind_id(self) -> int:
+        if self.kind not in KINDS:
+            raise InvalidArgument(1, f"strategy: unknown kind {self.kind!r}")
+        return KINDS[self.kind]
+
+
+class ProcessGrid:
+    """make_grid (dist_common.cpp:55-65) + ProcessGrid groups (grid.cpp)."""
+
+    def __init__(self, strat: Strategy):
+        if strat.block < 0:
+            raise InvalidArgument(1, "strategy: panel block width must be non-negative")
+        self.strat = strat
+        out = np.zeros(4, np.int32)
+        check(lib.cagnet_grid_shape(strat.kind_id, strat.ranks, strat.repl, out))
+        self.kind, self.rows, self.cols, self.layers = (int(x) for x in out)
+        self.ranks = strat.ranks
+
+    def _group(self, rank: int, which: int) -> list[int]:
+        buf = np.zeros(self.ranks, np.int32)
+        cnt = C.c_int()
+        check(lib.cagnet_grid_group(self.strat.kind_id, self.ranks, self.strat.repl, rank, which,
+                                    buf, C.byref(cnt)))
+        return [int(x) for x in buf[:cnt.value]]
+
+    def world(self):
+        return self._group(0, 0)
+
+    def row_group(self, rank):
+        return self._group(rank, 1)
+
+    def col_group(self, rank):
+        return self._group(rank, 2)
+
+    def fiber_group(self, rank):
+        return self._group(rank, 3)
+
+    def tile(self, n: int, rank: int, width: int) -> tuple[int, int, int, int, int]:
+        """(row_begin, row_end, col_begin, col_end, owner) of rank's H tile."""
+        out = np.zeros(5, np.int64)
+        check(lib.cagnet_tile_geometry(self.strat.kind_id, self.ranks, self.strat.repl, n, rank,
+                                       width, out))
+        return tuple(int(x) for x in out)
+
+
+def make_grid(strat: Strategy) -> ProcessGrid:
+    return ProcessGrid(strat)
+
+
+# ---------------------------------------------------------------------------
+# device CSR / datasets (dataset.hpp:31-93)
+# ---------------------------------------------------------------------------
+class DeviceCSR:
+    """A library-owned device CSR (int64 row_ptr, int32 col_idx, fp32 values)."""
+
+    def __init__(self, handle, owned=True):
+        self.h = handle
+        self.owned = owned
+        shape = np.zeros(3, np.int64)
+        check(lib.cagnet_csr_shape(self.h, shape))
+        self.n_rows, self.n_cols, self.nnz = (int(x) for x in shape)
+
+    def download(self):
+        """(row_ptr int64, col_idx int64, values fp32) on the host."""
+        rp = np.zeros(self.n_rows + 1, np.int64)
+        ci = np.zeros(max(self.nnz, 1), np.int64)
+        v = np.zeros(max(self.nnz, 1), np.float32)
+        check(lib.cagnet_csr_download(self.h, rp.ctypes.data, ci.ctypes.data, v.ctypes.data))
+        return rp, ci[:self.nnz], v[:self.nnz]
+
+    def device_ptrs(self):
+        rp, ci, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(lib.cagnet_csr_device_ptrs(self.h, C.byref(rp), C.byref(ci), C.byref(v)))
+        return rp.value, ci.value, v.value
+
+    def free(self):
+        if self.h and self.owned:
+            lib.cagnet_csr_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _new_csr(fn, *args) -> DeviceCSR:
+    out = C.c_void_p()
+    check(fn(*args, C.byref(out)))
+    return DeviceCSR(out)
+
+
+def csr_upload(row_ptr, col_idx, n_cols, vals=None, device=0) -> DeviceCSR:
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx, np.int64)
+    v = None if vals is None else np.ascontiguousarray(vals, np.float64)
+    return _new_csr(lib.cagnet_csr_upload, device, len(rp) - 1, n_cols, rp, ci,
+                    None if v is None else v.ctypes.data)
+
+
+def generate_erdos_renyi(n, degree, seed, device=0) -> DeviceCSR:
+    """csr.cpp:195-218 on the GPU, bit-exact."""
+    return _new_csr(lib.cagnet_er_generate, device, n, float(degree), seed)
+
+
+def add_self_loops_and_normalize(a: DeviceCSR) -> DeviceCSR:
+    return _new_csr(lib.cagnet_csr_normalize, a.h)
+
+
+def transpose(a: DeviceCSR) -> DeviceCSR:
+    return _new_csr(lib.cagnet_csr_transpose, a.h)
+
+
+def extract_block(a: DeviceCSR, r0, r1, c0, c1) -> DeviceCSR:
+    return _new_csr(lib.cagnet_csr_extract_block, a.h, r0, r1, c0, c1)
+
+
+class GraphDataset:
+    """dataset.hpp:31-45, device resident on `device`."""
+
+    def __init__(self, handle, device):
+        self.h = handle
+        self.device = device
+        info = np.zeros(5, np.int64)
+        check(lib.cagnet_dataset_info(self.h, info))
+        self.n, self.nnz, self.num_features, self.num_classes, self._train = (int(x) for x in info)
+
+    def train_count(self) -> int:
+        return self._train
+
+    def csr(self, which: int = 0) -> DeviceCSR:
+        out = C.c_void_p()
+        check(lib.cagnet_dataset_csr(self.h, which, C.byref(out)))
+        return DeviceCSR(out, owned=False)
+
+    @property
+    def adj(self) -> DeviceCSR:
+        return self.csr(0)
+
+    @property
+    def adj_t(self) -> DeviceCSR:
+        return self.csr(1)
+
+    def features(self) -> np.ndarray:
+        out = np.zeros((self.n, self.num_features), np.float32)
+        check(lib.cagnet_dataset_features(self.h, out))
+        return out
+
+    def labels(self) -> np.ndarray:
+        out = np.zeros(self.n, np.int64)
+        check(lib.cagnet_dataset_labels(self.h, out))
+        return out
+
+    def free(self):
+        if self.h:
+            lib.cagnet_dataset_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def generate_dataset(n, degree, num_features, num_classes, seed_graph=1, seed_features=2,
+                     seed_labels=3, device=0, generator="reference") -> GraphDataset:
+    """generate_dataset (dataset.cpp:110-118) built on the GPU.  generator
+    "reference" reproduces the reference graph bit for bit; "skip" is the
+    O(nnz) ER-shaped generator for graphs too large for O(n^2) draws."""
+    out = C.c_void_p()
+    check(lib.cagnet_dataset_generate(device, n, float(degree), num_features, num_classes,
+                                      seed_graph, seed_features, seed_labels,
+                                      GENERATORS[generator], C.byref(out)))
+    return GraphDataset(out, device)
+
+
+def make_dataset(raw_row_ptr, raw_col_idx, features, labels, num_classes, train_mask=None,
+                 device=0) -> GraphDataset:
+    """make_dataset (dataset.cpp:76-90) from a raw host CSR (canonical: sorted,
+    unique columns), fp64 features, labels and optional training mask."""
+    rp = np.ascontiguousarray(raw_row_ptr, np.int64)
+    ci = np.ascontiguousarray(raw_col_idx, np.int64)
+    x = np.ascontiguousarray(features, np.float64)
+    y = np.ascontiguousarray(labels, np.int64)
+    n = len(rp) - 1
+    if x.shape[0] != n or y.shape[0] != n:
+        raise InvalidArgument(1, f"GraphDataset: {x.shape[0]} feature rows / {y.shape[0]} labels "
+                                 f"for {n} vertices")
+    m = None if train_mask is None else np.ascontiguousarray(train_mask, np.uint8)
+    out = C.c_void_p()
+    check(lib.cagnet_dataset_make(device, n, rp, ci, x, x.shape[1], y,
+                                  None if m is None else m.ctypes.data, num_classes, C.byref(out)))
+    return GraphDataset(out, device)
+
+
+# ---------------------------------------------------------------------------
+# model (gnn.hpp:29-42)
+# ---------------------------------------------------------------------------
+@dataclass
+class GnnModel:
+    layer_dims: list
+    weights: list = field(default_factory=list)
+    learning_rate: float = 1.0
+
+    def num_layers(self) -> int:
+        return len(self.layer_dims)
+
+    def flat_weights(self) -> np.ndarray:
+        return np.concatenate([np.ascontiguousarray(w, np.float64).ravel() for w in self.weights])
+
+
+def init_glorot(layer_dims, seed, learning_rate=1.0) -> GnnModel:
+    dims = np.asarray(layer_dims, np.int64)
+    if len(dims) < 2:
+        raise InvalidArgument(1, f"init_glorot: need at least two layer dims, got {len(dims)}")
+    total = int(sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))) if len(dims) > 1 else 0
+    flat = np.zeros(max(total, 1))
+    check(lib.cagnet_init_glorot(dims, len(dims), seed, flat))
+    ws, off = [], 0
+    for l in range(len(dims) - 1):
+        k = int(dims[l] * dims[l + 1])
+        ws.append(flat[off:off + k].reshape(int(dims[l]), int(dims[l + 1])).copy())
+        off += k
+    return GnnModel([int(d) for d in dims], ws, float(learning_rate))
+
+
+# ---------------------------------------------------------------------------
+# training (dist.hpp:83-150)
+# ---------------------------------------------------------------------------
+def kernel_launches() -> int:
+    v = C.c_uint64()
+    check(lib.cagnet_kernel_launches(C.byref(v)))
+    return int(v.value)
+
+
+def device_count() -> int:
+    n = C.c_int()
+    check(lib.cagnet_device_count(C.byref(n)))
+    return n.value
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib.cagnet_comm_unique_id(buf))
+    return buf.raw
+
+
+class Trainer:
+    """One rank of a partitioned trainer (dist.hpp:83-131) on the dataset's GPU."""
+
+    def __init__(self, data: GraphDataset, model: GnnModel, strat: Strategy, rank: int = 0,
+                 nccl_id: bytes | None = None):
+        self.data, self.model, self.strat, self.rank = data, model, strat, rank
+        dims = np.asarray(model.layer_dims, np.int64)
+        w = model.flat_weights()
+        out = C.c_void_p()
+        nid = None if nccl_id is None else C.create_string_buffer(bytes(nccl_id), 128)
+        check(lib.cagnet_trainer_create(data.h, dims, len(dims), w, model.learning_rate,
+                                        strat.kind_id, strat.ranks, strat.repl, strat.block, rank,
+                                        None if nid is None else C.cast(nid, C.c_void_p),
+                                        C.byref(out)))
+        self.h = out
+        self.dims = [int(d) for d in dims]
+
+    # lifecycle -------------------------------------------------------------
+    def distribute(self):
+        check(lib.cagnet_trainer_distribute(self.h))
+
+    def forward_layer(self, l: int):
+        check(lib.cagnet_trainer_forward_layer(self.h, l))
+
+    def epoch(self) -> float:
+        loss = C.c_double()
+        check(lib.cagnet_trainer_epoch(self.h, C.byref(loss)))
+        return loss.value
+
+    def run_epochs(self, epochs: int) -> np.ndarray:
+        out = np.zeros(max(epochs, 1))
+        check(lib.cagnet_trainer_run_epochs(self.h, epochs, out))
+        return out[:epochs]
+
+    def epoch_async(self):
+        """Queues one epoch on the trainer's streams without waiting."""
+        check(lib.cagnet_trainer_epoch_async(self.h))
+
+    def losses(self) -> np.ndarray:
+        """Every epoch loss so far (waits for queued epochs)."""
+        cnt = C.c_int()
+        check(lib.cagnet_trainer_losses(self.h, np.zeros(1), 0, C.byref(cnt)))
+        out = np.zeros(max(cnt.value, 1))
+        check(lib.cagnet_trainer_losses(self.h, out, cnt.value, C.byref(cnt)))
+        return out[:cnt.value]
+
+    def sync(self):
+        check(lib.cagnet_trainer_sync(self.h))
+
+    # geometry ----------------------------------------------------------------
+    def tile(self, rank: int, width: int):
+        out = np.zeros(5, np.int64)
+        check(lib.cagnet_trainer_tile(self.h, rank, width, out))
+        return tuple(int(x) for x in out)
+
+    def tile_rows(self, rank):
+        return self.tile(rank, 1)[:2]
+
+    def tile_cols(self, rank, width):
+        return self.tile(rank, width)[2:4]
+
+    def tile_owner(self, rank):
+        return self.tile(rank, 1)[4]
+
+    def _tile_shape(self, width):
+        r0, r1, c0, c1, _ = self.tile(self.rank, width)
+        return r1 - r0, c1 - c0
+
+    # readback ----------------------------------------------------------------
+    def h_tile(self, layer: int) -> np.ndarray:
+        out = np.zeros(self._tile_shape(self.dims[layer]), np.float32)
+        check(lib.cagnet_trainer_h_tile(self.h, layer, out))
+        return out
+
+    def g_tile(self, idx: int) -> np.ndarray:
+        out = np.zeros(self._tile_shape(self.dims[idx + 1]), np.float32)
+        check(lib.cagnet_trainer_g_tile(self.h, idx, out))
+        return out
+
+    def weight(self, l: int) -> np.ndarray:
+        out = np.zeros((self.dims[l], self.dims[l + 1]), np.float32)
+        check(lib.cagnet_trainer_weight(self.h, l, out))
+        return out
+
+    def y(self, l: int) -> np.ndarray:
+        out = np.zeros((self.dims[l], self.dims[l + 1]), np.float32)
+        check(lib.cagnet_trainer_y(self.h, l, out))
+        return out
+
+    def num_parts(self) -> int:
+        n = C.c_int()
+        check(lib.cagnet_trainer_num_parts(self.h, C.byref(n)))
+        return n.value
+
+    def part(self, which: int, idx: int) -> DeviceCSR:
+        return _new_csr(lib.cagnet_trainer_part, self.h, which, idx)
+
+    def ledger(self) -> dict:
+        buf = np.zeros(20, np.uint64)
+        check(lib.cagnet_trainer_ledger(self.h, buf))
+        return {c: dict(zip(COUNTER_FIELDS, (int(x) for x in buf[5 * i:5 * i + 5])))
+                for i, c in enumerate(CATEGORIES)}
+
+    def last_epoch_ms(self) -> float:
+        ms = np.zeros(8)
+        check(lib.cagnet_trainer_stats(self.h, ms, None))
+        return float(ms[7])
+
+    def set_timing(self, on: bool = True):
+        check(lib.cagnet_trainer_set_timing(self.h, int(on)))
+
+    def profile(self) -> dict:
+        """{kernel name: dict(launches, ms, bytes, flops)} since the last reset."""
+        n = C.c_int()
+        check(lib.cagnet_trainer_profile_count(self.h, C.byref(n)))
+        out = {}
+        for i in range(n.value):
+            name = C.create_string_buffer(64)
+            v = np.zeros(4)
+            check(lib.cagnet_trainer_profile_entry(self.h, i, name, 64, v))
+            out[name.value.decode()] = dict(launches=int(v[0]), ms=float(v[1]), bytes=float(v[2]),
+                                            flops=float(v[3]))
+        return out
+
+    def profile_reset(self):
+        check(lib.cagnet_trainer_profile_reset(self.h))
+
+    def step_host(self, x_tile: np.ndarray, labels_tile: np.ndarray) -> float:
+        """One epoch from host buffers (H2D features/labels, epoch, D2H loss)."""
+        loss = C.c_double()
+        check(lib.cagnet_trainer_step_host(self.h, x_tile.ctypes.data, labels_tile.ctypes.data,
+                                           C.byref(loss)))
+        return loss.value
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(lib.cagnet_trainer_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def free(self):
+        if self.h:
+            lib.cagnet_trainer_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def make_trainer(data, model, strat, rank=0, nccl_id=None) -> Trainer:
+    return Trainer(data, model, strat, rank, nccl_id)
+
+
+@dataclass
+class DistOutcome:
+    """dist.hpp:138-147 (fp32 device results widened to fp64 on the host)."""
+    losses: np.ndarray
+    h_final: np.ndarray
+    y_final: list
+    g_final: list
+    model: GnnModel
+    ledger: list  # per rank
+
+
+def assemble_tiles(trainers, n, width, pick) -> np.ndarray:
+    """Trainer::assemble_tiles (dist_common.cpp:117-145) with the bitwise
+    replica check against each tile's owner."""
+    out = np.zeros((n, width), np.float64)
+    tiles = {t.rank: pick(t) for t in trainers}
+    for t in trainers:
+        r0, r1, c0, c1, owner = t.tile(t.rank, width)
+        tile = tiles[t.rank]
+        if tile.shape != (r1 - r0, c1 - c0):
+            raise RuntimeError(f"assemble: rank {t.rank} tile is {tile.shape}")
+        if owner != t.rank:
+            if not np.array_equal(tile.view(np.uint32), tiles[owner].view(np.uint32)):
+                raise RuntimeError(f"replica divergence: rank {t.rank} disagrees with rank {owner}")
+            continue
+        out[r0:r1, c0:c1] = tile
+    return out
+
+
+def _verified(trainers, get, what):
+    ref = get(trainers[0])
+    for t in trainers[1:]:
+        x = get(t)
+        if not np.array_equal(np.asarray(x).view(np.uint8), np.asarray(ref).view(np.uint8)):
+            raise RuntimeError(f"{what} replica divergence at rank {t.rank}")
+    return ref
+
+
+def run_distributed(data_factory, model: GnnModel, strat: Strategy, epochs: int,
+                    devices=None) -> DistOutcome:
+    """run_distributed (dist_common.cpp:205-222) in one process: one host
+    thread and one GPU per rank (the reference's thread-per-rank model,
+    runtime.cpp:270-285), NCCL over NVLink between them.  data_factory(device)
+    must build the same dataset on each device."""
+    if epochs <= 0:
+        raise InvalidArgument(1, "run_epochs: epoch count must be positive")
+    P = strat.ranks
+    ProcessGrid(strat)  # validates the geometry before any GPU work
+    if devices is None:
+        n_dev = C.c_int()
+        check(lib.cagnet_device_count(C.byref(n_dev)))
+        if n_dev.value < P:
+            raise InvalidArgument(1, f"run_distributed: {P} ranks need {P} GPUs, "
+                                     f"found {n_dev.value}")
+        devices = list(range(P))
+    nid = comm_unique_id() if P > 1 else None
+    datas = [None] * P
+    trainers = [None] * P
+    losses = [None] * P
+    errors = []
+
+    def body(r):
+        try:
+            datas[r] = data_factory(devices[r])
+            trainers[r] = Trainer(datas[r], model, strat, r, nid)
+            trainers[r].distribute()
+            losses[r] = trainers[r].run_epochs(epochs)
+        except Exception as e:  # the lowest-rank exception wins (runtime.cpp:281-284)
+            errors.append((r, e))
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        raise sorted(errors, key=lambda x: x[0])[0][1]
+    n = datas[0].n
+    L = len(model.layer_dims)
+    out_losses = _verified(trainers, lambda t: losses[t.rank], "loss")
+    h_final = assemble_tiles(trainers, n, model.layer_dims[-1], lambda t: t.h_tile(L - 1))
+    g_final = [assemble_tiles(trainers, n, model.layer_dims[i + 1], lambda t, i=i: t.g_tile(i))
+               for i in range(L - 1)]
+    y_final = [_verified(trainers, lambda t, i=i: t.y(i), "gradient").astype(np.float64)
+               for i in range(L - 1)]
+    w_final = [_verified(trainers, lambda t, i=i: t.weight(i), "weight").astype(np.float64)
+               for i in range(L - 1)]
+    ledgers = [t.ledger() for t in trainers]
+    return DistOutcome(np.asarray(out_losses), h_final, y_final, g_final,
+                       GnnModel(list(model.layer_dims), w_final, model.learning_rate), ledgers)

@@ -1,0 +1,625 @@
+// extern "C" boundary of libcagnet_b200.so (include/cagnet_b200.h).  Every
+// entry point validates shapes on the host, maps C++ exceptions to status
+// codes and records the message per thread.
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "../../include/cagnet_b200.h"
+#include <cmath>
+
+#include "kernels.cuh"
+#include "rng.hpp"
+#include "trainer.hpp"
+
+struct cagnet_csr_s {
+  cagnet::DeviceCsr csr;
+  bool borrowed = false;
+};
+struct cagnet_dataset_s {
+  std::unique_ptr<cagnet::DeviceDataset> data;
+  cagnet_csr_s adj, adj_t;
+};
+struct cagnet_trainer_s {
+  std::unique_ptr<cagnet::Trainer> t;
+  bool timing = false;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return CAGNET_OK;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return CAGNET_EINVAL;
+  } catch (const cagnet::CudaError& e) {
+    g_error = e.what();
+    return CAGNET_ECUDA;
+  } catch (const cagnet::NcclError& e) {
+    g_error = e.what();
+    return CAGNET_ENCCL;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return CAGNET_ERUNTIME;
+  }
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+void set_device(int device) { CG_CUDA(cudaSetDevice(device)); }
+
+cagnet::Strategy make_strategy(int kind, int ranks, int repl, int block) {
+  if (kind < 0 || kind > 3) throw std::invalid_argument("strategy: unknown kind");
+  cagnet::Strategy s;
+  s.kind = static_cast<cagnet::StrategyKind>(kind);
+  s.ranks = ranks;
+  s.repl = repl;
+  s.block = block;
+  return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cagnet_last_error(void) { return g_error.c_str(); }
+int cagnet_version(void) { return 1; }
+
+int cagnet_device_count(int* out) {
+  return guarded([&] {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *out = n;
+  });
+}
+
+// ---- host-only partition geometry -----------------------------------------------
+int cagnet_block_range(int64_t n, int parts, int idx, int64_t* out2) {
+  return guarded([&] {
+    const cagnet::BlockRange r = cagnet::block_range(n, parts, idx);
+    out2[0] = r.begin;
+    out2[1] = r.end;
+  });
+}
+
+int cagnet_grid_shape(int kind, int ranks, int repl, int* out4) {
+  return guarded([&] {
+    const cagnet::ProcessGrid g = cagnet::ProcessGrid::make(make_strategy(kind, ranks, repl, 0));
+    out4[0] = static_cast<int>(g.kind());
+    out4[1] = g.rows();
+    out4[2] = g.cols();
+    out4[3] = g.layers();
+  });
+}
+
+int cagnet_grid_group(int kind, int ranks, int repl, int rank, int which, int* members, int* count) {
+  return guarded([&] {
+    const cagnet::ProcessGrid g = cagnet::ProcessGrid::make(make_strategy(kind, ranks, repl, 0));
+    cagnet::require(rank >= 0 && rank < g.ranks(), "grid_group: rank outside the grid");
+    const cagnet::Group* grp = nullptr;
+    switch (which) {
+      case 0: grp = &g.world(); break;
+      case 1: grp = &g.row_group(rank); break;
+      case 2: grp = &g.col_group(rank); break;
+      case 3: grp = &g.fiber_group(rank); break;
+      default: throw std::invalid_argument("grid_group: which must be 0..3");
+    }
+    *count = static_cast<int>(grp->size());
+    for (size_t i = 0; i < grp->size(); ++i) members[i] = grp->members[i];
+  });
+}
+
+int cagnet_tile_geometry(int kind, int ranks, int repl, int64_t n, int rank, int64_t width,
+                         int64_t* out5) {
+  return guarded([&] {
+    const cagnet::ProcessGrid g = cagnet::ProcessGrid::make(make_strategy(kind, ranks, repl, 0));
+    cagnet::require(rank >= 0 && rank < g.ranks(), "tile_geometry: rank outside the grid");
+    const cagnet::BlockRange r = cagnet::tile_rows_of(g, n, rank), c = cagnet::tile_cols_of(g, rank, width);
+    out5[0] = r.begin;
+    out5[1] = r.end;
+    out5[2] = c.begin;
+    out5[3] = c.end;
+    out5[4] = cagnet::tile_owner_of(g, rank);
+  });
+}
+
+// ---- kernel seams --------------------------------------------------------------
+int cagnet_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                        const int32_t* col_idx, const float* vals, const float* H, int64_t ldh,
+                        int32_t f, float* T, int64_t ldt, int accumulate, void* stream) {
+  return guarded([&] {
+    cagnet::require(n_rows >= 0 && n_cols >= 0 && nnz >= 0 && f >= 0, "spmm: negative shape");
+    cagnet::require(ldh >= f && ldt >= f, "spmm: leading dimension smaller than f");
+    cagnet::require(n_rows == 0 || (row_ptr && T), "spmm: null row_ptr or output");
+    cagnet::require(nnz == 0 || (col_idx && vals && H), "spmm: null input arrays");
+    cagnet::kern::spmm_csr(n_rows, row_ptr, col_idx, vals, H, ldh, f, T, ldt, accumulate != 0,
+                           as_stream(stream));
+  });
+}
+
+int cagnet_gemm_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
+                    const float* B, int64_t ldb, float* C, int64_t ldc, int accumulate, int epilogue,
+                    const float* aux, int64_t ldaux, float* aux_out, int64_t ldao, void* stream) {
+  return guarded([&] {
+    cagnet::require(m >= 0 && n >= 0 && k >= 0, "gemm: negative shape");
+    cagnet::require(ldc >= n, "gemm: accumulator leading dimension smaller than n");
+    cagnet::require(lda >= (ta ? m : k) && ldb >= (tb ? k : n), "gemm: operand leading dimension too small");
+    cagnet::require(epilogue >= 0 && epilogue <= 2, "gemm: unknown epilogue");
+    cagnet::require(epilogue != CAGNET_EPI_RELU_PRIME || (aux && ldaux >= n), "gemm: relu' epilogue needs aux");
+    cagnet::kern::GemmDesc d;
+    d.m = m;
+    d.n = n;
+    d.k = k;
+    d.A = A;
+    d.a_sm = ta ? 1 : lda;
+    d.a_sk = ta ? lda : 1;
+    d.B = B;
+    d.b_sk = tb ? 1 : ldb;
+    d.b_sn = tb ? ldb : 1;
+    d.C = C;
+    d.ldc = ldc;
+    d.accumulate = accumulate != 0;
+    d.epilogue = epilogue;
+    d.aux = aux;
+    d.ldaux = ldaux;
+    d.aux_out = aux_out;
+    d.ldao = ldao;
+    cagnet::kern::gemm_tf32x3(d, as_stream(stream));
+  });
+}
+
+int cagnet_logsoftmax_nll_f32(const float* Z, int64_t rows, int32_t cols, int64_t ldz, int32_t c0,
+                              int32_t c1, float* logp, int64_t ldl, float* G, int64_t ldg,
+                              const int32_t* labels, const uint8_t* mask, int64_t train_total,
+                              double* loss_partial, void* stream) {
+  return guarded([&] {
+    if (cols == 0) throw std::invalid_argument("log_softmax_rows: zero columns");
+    cagnet::require(0 <= c0 && c0 <= c1 && c1 <= cols, "nll_tile: column tile outside the row");
+    cagnet::require(!G || labels, "nll_tile: labels required for the gradient");
+    if (G && train_total == 0) throw std::invalid_argument("nll_tile: empty training set");
+    cagnet::kern::logsoftmax_nll(Z, rows, cols, ldz, c0, c1, logp, ldl, G, ldg, labels, mask,
+                                 train_total, loss_partial, as_stream(stream));
+  });
+}
+
+int cagnet_relu_f32(const float* Z, int64_t rows, int32_t cols, int64_t ldz, float* H, int64_t ldh,
+                    void* stream) {
+  return guarded([&] { cagnet::kern::relu(Z, rows, cols, ldz, H, ldh, as_stream(stream)); });
+}
+
+int cagnet_sgd_f32(float* W, const float* Y, int64_t count, float lr, void* stream) {
+  return guarded([&] { cagnet::kern::sgd(W, Y, count, lr, as_stream(stream)); });
+}
+
+// ---- device CSR -------------------------------------------------------------------
+int cagnet_csr_upload(int device, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                      const int64_t* col_idx, const double* vals, cagnet_csr_t* out) {
+  return guarded([&] {
+    set_device(device);
+    auto h = std::make_unique<cagnet_csr_s>();
+    h->csr = cagnet::upload_csr(n_rows, n_cols, row_ptr, col_idx, vals, nullptr);
+    *out = h.release();
+  });
+}
+
+int cagnet_csr_shape(cagnet_csr_t a, int64_t* shape) {
+  return guarded([&] {
+    shape[0] = a->csr.n_rows;
+    shape[1] = a->csr.n_cols;
+    shape[2] = a->csr.nnz;
+  });
+}
+
+int cagnet_csr_download(cagnet_csr_t a, int64_t* row_ptr, int64_t* col_idx, float* vals) {
+  return guarded([&] {
+    const cagnet::DeviceCsr& c = a->csr;
+    set_device(c.device);
+    if (row_ptr)
+      CG_CUDA(cudaMemcpy(row_ptr, c.row_ptr.get(), (c.n_rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (col_idx && c.nnz) {
+      std::vector<int32_t> tmp(static_cast<size_t>(c.nnz));
+      CG_CUDA(cudaMemcpy(tmp.data(), c.col_idx.get(), c.nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+      for (int64_t k = 0; k < c.nnz; ++k) col_idx[k] = tmp[static_cast<size_t>(k)];
+    }
+    if (vals && c.nnz)
+      CG_CUDA(cudaMemcpy(vals, c.vals.get(), c.nnz * sizeof(float), cudaMemcpyDeviceToHost));
+  });
+}
+
+int cagnet_csr_device_ptrs(cagnet_csr_t a, const int64_t** row_ptr, const int32_t** col_idx,
+                           const float** vals) {
+  return guarded([&] {
+    if (row_ptr) *row_ptr = a->csr.row_ptr.get();
+    if (col_idx) *col_idx = a->csr.col_idx.get();
+    if (vals) *vals = a->csr.vals.get();
+  });
+}
+
+int cagnet_csr_free(cagnet_csr_t a) {
+  return guarded([&] {
+    if (a && !a->borrowed) {
+      set_device(a->csr.device);
+      delete a;
+    }
+  });
+}
+
+int cagnet_er_generate(int device, int64_t n, double degree, uint64_t seed, cagnet_csr_t* out) {
+  return guarded([&] {
+    set_device(device);
+    auto h = std::make_unique<cagnet_csr_s>();
+    h->csr = cagnet::er_generate_device(n, degree, seed, nullptr);
+    *out = h.release();
+  });
+}
+
+int cagnet_csr_normalize(cagnet_csr_t raw, cagnet_csr_t* out) {
+  return guarded([&] {
+    set_device(raw->csr.device);
+    auto h = std::make_unique<cagnet_csr_s>();
+    h->csr = cagnet::normalize_device(raw->csr, nullptr, nullptr);
+    *out = h.release();
+  });
+}
+
+int cagnet_csr_transpose(cagnet_csr_t a, cagnet_csr_t* out) {
+  return guarded([&] {
+    set_device(a->csr.device);
+    auto h = std::make_unique<cagnet_csr_s>();
+    h->csr = cagnet::transpose_device(a->csr, nullptr);
+    *out = h.release();
+  });
+}
+
+int cagnet_csr_extract_block(cagnet_csr_t a, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                             cagnet_csr_t* out) {
+  return guarded([&] {
+    set_device(a->csr.device);
+    auto h = std::make_unique<cagnet_csr_s>();
+    h->csr = cagnet::extract_block_device(a->csr, r0, r1, c0, c1, nullptr);
+    *out = h.release();
+  });
+}
+
+// ---- datasets -------------------------------------------------------------------------
+static void wrap_dataset(cagnet_dataset_s* d) {
+  // Borrowed CSR views share the dataset's device buffers without copying.
+  d->adj.borrowed = d->adj_t.borrowed = true;
+}
+
+int cagnet_dataset_generate(int device, int64_t n, double degree, int64_t num_features,
+                            int64_t num_classes, uint64_t seed_graph, uint64_t seed_features,
+                            uint64_t seed_labels, int generator, cagnet_dataset_t* out) {
+  return guarded([&] {
+    cagnet::require(generator == CAGNET_GEN_REFERENCE || generator == CAGNET_GEN_SKIP,
+                    "dataset: unknown generator");
+    set_device(device);
+    auto d = std::make_unique<cagnet_dataset_s>();
+    d->data = cagnet::dataset_generate(n, degree, num_features, num_classes, seed_graph,
+                                       seed_features, seed_labels, generator);
+    wrap_dataset(d.get());
+    *out = d.release();
+  });
+}
+
+int cagnet_dataset_make(int device, int64_t n, const int64_t* raw_row_ptr, const int64_t* raw_col_idx,
+                        const double* features, int64_t f, const int64_t* labels, const uint8_t* mask,
+                        int64_t num_classes, cagnet_dataset_t* out) {
+  return guarded([&] {
+    set_device(device);
+    auto d = std::make_unique<cagnet_dataset_s>();
+    d->data = cagnet::dataset_make(n, raw_row_ptr, raw_col_idx, features, f, labels, mask, num_classes);
+    wrap_dataset(d.get());
+    *out = d.release();
+  });
+}
+
+int cagnet_dataset_info(cagnet_dataset_t d, int64_t* info) {
+  return guarded([&] {
+    info[0] = d->data->n;
+    info[1] = d->data->adj.nnz;
+    info[2] = d->data->f;
+    info[3] = d->data->num_classes;
+    info[4] = d->data->train_count;
+  });
+}
+
+int cagnet_dataset_csr(cagnet_dataset_t d, int which, cagnet_csr_t* out) {
+  return guarded([&] {
+    cagnet::require(which == 0 || which == 1, "dataset_csr: which must be 0 (adj) or 1 (adj_t)");
+    cagnet_csr_s* h = which == 0 ? &d->adj : &d->adj_t;
+    // Shallow view: copy the metadata, alias the buffers (never freed through the view).
+    const cagnet::DeviceCsr& src = which == 0 ? d->data->adj : d->data->adj_t;
+    h->csr.device = src.device;
+    h->csr.n_rows = src.n_rows;
+    h->csr.n_cols = src.n_cols;
+    h->csr.nnz = src.nnz;
+    h->csr.row_ptr.ptr = src.row_ptr.ptr;
+    h->csr.row_ptr.count = 0;
+    h->csr.col_idx.ptr = src.col_idx.ptr;
+    h->csr.col_idx.count = 0;
+    h->csr.vals.ptr = src.vals.ptr;
+    h->csr.vals.count = 0;
+    *out = h;
+  });
+}
+
+int cagnet_dataset_features(cagnet_dataset_t d, float* out) {
+  return guarded([&] {
+    const cagnet::DeviceDataset& ds = *d->data;
+    set_device(ds.device);
+    if (ds.n && ds.f)
+      CG_CUDA(cudaMemcpy2D(out, ds.f * sizeof(float), ds.features.get(), ds.ldf * sizeof(float),
+                           ds.f * sizeof(float), ds.n, cudaMemcpyDeviceToHost));
+  });
+}
+
+int cagnet_dataset_labels(cagnet_dataset_t d, int64_t* out) {
+  return guarded([&] {
+    const cagnet::DeviceDataset& ds = *d->data;
+    set_device(ds.device);
+    std::vector<int32_t> tmp(static_cast<size_t>(ds.n));
+    if (ds.n) CG_CUDA(cudaMemcpy(tmp.data(), ds.labels.get(), ds.n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < ds.n; ++i) out[i] = tmp[static_cast<size_t>(i)];
+  });
+}
+
+int cagnet_dataset_free(cagnet_dataset_t d) {
+  return guarded([&] {
+    if (!d) return;
+    set_device(d->data->device);
+    // Detach the borrowed views before the owning buffers go away.
+    for (cagnet_csr_s* v : {&d->adj, &d->adj_t}) {
+      v->csr.row_ptr.ptr = nullptr;
+      v->csr.col_idx.ptr = nullptr;
+      v->csr.vals.ptr = nullptr;
+    }
+    delete d;
+  });
+}
+
+// ---- training ---------------------------------------------------------------------------
+int cagnet_init_glorot(const int64_t* dims, int ndims, uint64_t seed, double* weights) {
+  return guarded([&] {
+    if (ndims < 2)
+      throw std::invalid_argument("init_glorot: need at least two layer dims, got " + std::to_string(ndims));
+    for (int l = 0; l < ndims; ++l)
+      if (dims[l] <= 0) throw std::invalid_argument("init_glorot: zero-width layer");
+    // gnn.cpp:24-44: one generator, layers in order, row-major fill,
+    // U(-b, b) with b = sqrt(6 / (f_in + f_out)).
+    cagnet::Xoshiro rng(seed);
+    int64_t off = 0;
+    for (int l = 0; l + 1 < ndims; ++l) {
+      const double bound = std::sqrt(6.0 / static_cast<double>(dims[l] + dims[l + 1]));
+      for (int64_t e = 0; e < dims[l] * dims[l + 1]; ++e) weights[off + e] = rng.uniform(-bound, bound);
+      off += dims[l] * dims[l + 1];
+    }
+  });
+}
+
+int cagnet_comm_unique_id(uint8_t* out128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    CG_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int cagnet_trainer_create(cagnet_dataset_t data, const int64_t* dims, int ndims, const double* weights,
+                          double learning_rate, int kind, int ranks, int repl, int block, int rank,
+                          const uint8_t* nccl_id, cagnet_trainer_t* out) {
+  return guarded([&] {
+    set_device(data->data->device);
+    cagnet::require(ndims >= 2, "init_glorot: need at least two layer dims, got " + std::to_string(ndims));
+    ncclUniqueId id;
+    if (nccl_id) std::memcpy(&id, nccl_id, sizeof(id));
+    auto t = std::make_unique<cagnet_trainer_s>();
+    t->t = cagnet::make_trainer(*data->data, std::vector<int64_t>(dims, dims + ndims), weights,
+                                learning_rate, make_strategy(kind, ranks, repl, block), rank,
+                                nccl_id ? &id : nullptr);
+    *out = t.release();
+  });
+}
+
+int cagnet_trainer_distribute(cagnet_trainer_t t) {
+  return guarded([&] {
+    set_device(t->t->device());
+    t->t->distribute();
+  });
+}
+
+int cagnet_trainer_forward_layer(cagnet_trainer_t t, int l) {
+  return guarded([&] {
+    set_device(t->t->device());
+    t->t->forward_layer(l);
+  });
+}
+
+int cagnet_trainer_epoch(cagnet_trainer_t t, double* loss) {
+  return guarded([&] {
+    set_device(t->t->device());
+    std::vector<double> l = t->t->run_epochs(1);
+    if (loss) *loss = l.empty() ? 0.0 : l.back();
+  });
+}
+
+int cagnet_trainer_run_epochs(cagnet_trainer_t t, int epochs, double* losses) {
+  return guarded([&] {
+    set_device(t->t->device());
+    if (epochs <= 0) throw std::invalid_argument("run_epochs: epoch count must be positive");
+    std::vector<double> l = t->t->run_epochs(epochs);
+    if (losses) std::memcpy(losses, l.data(), l.size() * sizeof(double));
+  });
+}
+
+int cagnet_trainer_epoch_async(cagnet_trainer_t t) {
+  return guarded([&] {
+    set_device(t->t->device());
+    t->t->epoch();
+  });
+}
+
+int cagnet_trainer_losses(cagnet_trainer_t t, double* out, int cap, int* count) {
+  return guarded([&] {
+    const std::vector<double>& l = t->t->all_losses();
+    *count = static_cast<int>(l.size());
+    for (int i = 0; i < cap && i < static_cast<int>(l.size()); ++i) out[i] = l[static_cast<size_t>(i)];
+  });
+}
+
+int cagnet_trainer_sync(cagnet_trainer_t t) {
+  return guarded([&] { t->t->sync(); });
+}
+
+int cagnet_trainer_tile(cagnet_trainer_t t, int rank, int64_t width, int64_t* out) {
+  return guarded([&] {
+    const cagnet::BlockRange r = t->t->tile_rows(rank), c = t->t->tile_cols(rank, width);
+    out[0] = r.begin;
+    out[1] = r.end;
+    out[2] = c.begin;
+    out[3] = c.end;
+    out[4] = t->t->tile_owner(rank);
+  });
+}
+
+int cagnet_trainer_h_tile(cagnet_trainer_t t, int layer, float* out) {
+  return guarded([&] {
+    t->t->sync();
+    t->t->h_tile(layer, out);
+  });
+}
+int cagnet_trainer_g_tile(cagnet_trainer_t t, int idx, float* out) {
+  return guarded([&] {
+    t->t->sync();
+    t->t->g_tile(idx, out);
+  });
+}
+int cagnet_trainer_weight(cagnet_trainer_t t, int l, float* out) {
+  return guarded([&] {
+    t->t->sync();
+    t->t->weight(l, out);
+  });
+}
+int cagnet_trainer_y(cagnet_trainer_t t, int l, float* out) {
+  return guarded([&] {
+    t->t->sync();
+    t->t->ygrad(l, out);
+  });
+}
+
+int cagnet_trainer_num_parts(cagnet_trainer_t t, int* out) {
+  return guarded([&] { *out = t->t->num_parts(); });
+}
+
+int cagnet_trainer_part(cagnet_trainer_t t, int which, int part, cagnet_csr_t* out) {
+  return guarded([&] {
+    const cagnet::DeviceCsr& src = t->t->part(which, part);
+    auto h = std::make_unique<cagnet_csr_s>();
+    h->borrowed = false;
+    // Deep copy so the handle can outlive the trainer.
+    h->csr.device = src.device;
+    h->csr.n_rows = src.n_rows;
+    h->csr.n_cols = src.n_cols;
+    h->csr.nnz = src.nnz;
+    h->csr.row_ptr.resize(static_cast<size_t>(src.n_rows + 1));
+    h->csr.col_idx.resize(static_cast<size_t>(src.nnz));
+    h->csr.vals.resize(static_cast<size_t>(src.nnz));
+    CG_CUDA(cudaMemcpy(h->csr.row_ptr.get(), src.row_ptr.get(), (src.n_rows + 1) * sizeof(int64_t),
+                       cudaMemcpyDeviceToDevice));
+    if (src.nnz) {
+      CG_CUDA(cudaMemcpy(h->csr.col_idx.get(), src.col_idx.get(), src.nnz * sizeof(int32_t),
+                         cudaMemcpyDeviceToDevice));
+      CG_CUDA(cudaMemcpy(h->csr.vals.get(), src.vals.get(), src.nnz * sizeof(float), cudaMemcpyDeviceToDevice));
+    }
+    *out = h.release();
+  });
+}
+
+int cagnet_trainer_stats(cagnet_trainer_t t, double* ms8, uint64_t* words_received4) {
+  return guarded([&] {
+    if (ms8) {
+      for (int i = 0; i < 8; ++i) ms8[i] = 0.0;
+      ms8[7] = t->t->last_epoch_ms();
+    }
+    if (words_received4)
+      for (int c = 0; c < 4; ++c)
+        words_received4[c] = t->t->comm().counter(static_cast<cagnet::Category>(c)).words_received;
+  });
+}
+
+int cagnet_trainer_ledger(cagnet_trainer_t t, uint64_t* out20) {
+  return guarded([&] {
+    for (int c = 0; c < 4; ++c) {
+      const cagnet::CommCounter& k = t->t->comm().counter(static_cast<cagnet::Category>(c));
+      out20[5 * c + 0] = k.messages;
+      out20[5 * c + 1] = k.words_sent;
+      out20[5 * c + 2] = k.words_received;
+      out20[5 * c + 3] = k.payload_words;
+      out20[5 * c + 4] = k.calls;
+    }
+  });
+}
+
+int cagnet_trainer_set_timing(cagnet_trainer_t t, int on) {
+  return guarded([&] {
+    t->timing = on != 0;
+    t->t->set_timing(on != 0);
+  });
+}
+
+int cagnet_trainer_profile_count(cagnet_trainer_t t, int* n) {
+  return guarded([&] { *n = static_cast<int>(t->t->profile().size()); });
+}
+
+int cagnet_trainer_profile_entry(cagnet_trainer_t t, int i, char* name, int cap, double* out4) {
+  return guarded([&] {
+    const auto& p = t->t->profile();
+    cagnet::require(i >= 0 && i < static_cast<int>(p.size()), "profile_entry: index out of range");
+    const auto& e = p[static_cast<size_t>(i)];
+    if (name && cap > 0) {
+      std::strncpy(name, e.name.c_str(), static_cast<size_t>(cap - 1));
+      name[cap - 1] = 0;
+    }
+    out4[0] = static_cast<double>(e.launches);
+    out4[1] = e.ms;
+    out4[2] = e.bytes;
+    out4[3] = e.flops;
+  });
+}
+
+int cagnet_trainer_profile_reset(cagnet_trainer_t t) {
+  return guarded([&] { t->t->reset_profile(); });
+}
+
+int cagnet_trainer_step_host(cagnet_trainer_t t, const float* x_tile, const int32_t* labels_tile,
+                             double* loss) {
+  return guarded([&] {
+    const double l = t->t->step_host(x_tile, labels_tile);
+    if (loss) *loss = l;
+  });
+}
+
+int cagnet_kernel_launches(uint64_t* out) {
+  return guarded([&] { *out = cagnet::launch_counter().load(); });
+}
+
+int cagnet_trainer_stream(cagnet_trainer_t t, void** out) {
+  return guarded([&] { *out = reinterpret_cast<void*>(t->t->stream()); });
+}
+
+int cagnet_trainer_free(cagnet_trainer_t t) {
+  return guarded([&] { delete t; });
+}
+
+}  // extern "C"

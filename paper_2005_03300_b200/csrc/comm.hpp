@@ -1,0 +1,88 @@
+// Rank-boundary collectives on NCCL over NVLink / NVSwitch, one communicator
+// per grid group (ncclCommSplit of the world communicator by group id).  This
+// replaces the reference's SimRuntime rendezvous (runtime.cpp:186-228) and
+// RankContext collectives (runtime.hpp:55-96).  Every call meters the same
+// per-category counters as the reference ledger (runtime.cpp:142-184), so the
+// traffic of a GPU run can be reconciled with the simulator's ledger word for
+// word.  Singleton groups short-circuit and meter nothing, exactly like the
+// reference.
+#pragma once
+
+#include <nccl.h>
+
+#include <cstdint>
+#include <map>
+#include <vector>
+
+#include "common.cuh"
+#include "grid.hpp"
+
+namespace cagnet {
+
+enum class Category : int { DBcast = 0, SBcast = 1, Reduce = 2, AllGather = 3 };
+constexpr int kNumCategories = 4;
+
+struct CommCounter {
+  uint64_t messages = 0;
+  uint64_t words_sent = 0;
+  uint64_t words_received = 0;
+  uint64_t payload_words = 0;
+  uint64_t calls = 0;
+};
+
+#define CG_NCCL(expr)                                                                     \
+  do {                                                                                    \
+    ncclResult_t _r = (expr);                                                             \
+    if (_r != ncclSuccess)                                                                \
+      throw ::cagnet::NcclError(std::string(#expr) + ": " + ncclGetErrorString(_r) + " (" + \
+                                __FILE__ + ":" + std::to_string(__LINE__) + ")");        \
+  } while (0)
+
+class Comm {
+ public:
+  // id may be null only when the grid has a single rank.
+  Comm(const ProcessGrid& grid, int rank, const ncclUniqueId* id);
+  ~Comm();
+  Comm(const Comm&) = delete;
+  Comm& operator=(const Comm&) = delete;
+
+  int rank() const { return rank_; }
+
+  // One-to-all broadcast of `count` elements in place at `buf` (root sends
+  // from it, others receive into it).  `words` is the ledger payload.
+  void bcast(const Group& g, int root_rank, void* buf, size_t count, ncclDataType_t t,
+             Category cat, uint64_t words, cudaStream_t s);
+  // Three-array sparse panel broadcast; ledger payload = nnz (CsrMatrix::words).
+  void bcast_csr(const Group& g, int root_rank, int64_t* row_ptr, int64_t n_rows, int32_t* col,
+                 float* vals, int64_t nnz, Category cat, cudaStream_t s);
+  // In-place elementwise sum, every member gets the result.
+  void all_reduce(const Group& g, void* buf, size_t count, ncclDataType_t t, Category cat,
+                  uint64_t words, cudaStream_t s);
+  // Sum then scatter equal padded slices of `slice_count` elements; slot_words
+  // are the logical (unpadded) words per member for the ledger.
+  void reduce_scatter(const Group& g, const void* send, void* recv, size_t slice_count,
+                      ncclDataType_t t, Category cat, const std::vector<uint64_t>& slot_words,
+                      cudaStream_t s);
+  // Concatenate equal padded slices in ascending member order.
+  void all_gather(const Group& g, const void* send, void* recv, size_t slice_count,
+                  ncclDataType_t t, Category cat, const std::vector<uint64_t>& slot_words,
+                  cudaStream_t s);
+
+  // Unmetered world all-gather for setup metadata (tile shapes).
+  void setup_all_gather(const void* send, void* recv, size_t count, ncclDataType_t t,
+                        cudaStream_t s);
+
+  const CommCounter& counter(Category c) const { return counters_[static_cast<int>(c)]; }
+
+ private:
+  ncclComm_t comm_for(const Group& g) const;
+  CommCounter& ctr(Category c) { return counters_[static_cast<int>(c)]; }
+
+  int rank_ = 0;
+  int ranks_ = 1;
+  ncclComm_t world_ = nullptr;
+  std::map<int, ncclComm_t> comms_;  // group id -> communicator
+  CommCounter counters_[kNumCategories];
+};
+
+}  // namespace cagnet

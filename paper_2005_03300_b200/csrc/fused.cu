@@ -1,0 +1,266 @@
+// K3 — fused elementwise kernels: log_softmax + NLL + gradient, ReLU, SGD and
+// the small layout helpers the partition layer needs (strided copies,
+// transposes).  All are HBM-streaming kernels.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cagnet {
+namespace kern {
+namespace {
+
+constexpr int kMaxParts = 8;
+constexpr int kLossBlocks = 1024;
+
+struct RowBlocks {
+  const float* base;
+  int64_t block_stride;  // elements between column blocks
+  int64_t ld;
+  int parts;
+  int widths[kMaxParts];
+  int offs[kMaxParts + 1];
+};
+
+__device__ __forceinline__ float load_col(const RowBlocks& b, int64_t r, int j) {
+  int q = 0;
+#pragma unroll
+  for (int t = 1; t < kMaxParts; ++t)
+    if (t < b.parts && j >= b.offs[t]) q = t;
+  return b.base[q * b.block_stride + r * b.ld + (j - b.offs[q])];
+}
+
+// One warp per row.  Reference order: mx = max_j z; s = sum_j exp(z - mx);
+// lse = log(s); logp = z - mx - lse (dense.cpp:94-107); grad on training rows
+// = exp(logp) / |T| minus 1/|T| at the label; loss partial += -logp[y]
+// (dense.cpp:109-136), accumulated in fp64.
+__global__ void __launch_bounds__(256)
+    logsoftmax_nll_kernel(const RowBlocks zb, int64_t rows, int c0, int c1, float* logp,
+                          int64_t ldl, float* G, int64_t ldg, const int32_t* __restrict__ labels,
+                          const uint8_t* __restrict__ mask, double inv_total,
+                          double* __restrict__ partials) {
+  const int lane = threadIdx.x & 31;
+  const int warps_per_block = blockDim.x >> 5;
+  const int cols = zb.offs[zb.parts];
+  double loss = 0.0;
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * warps_per_block + (threadIdx.x >> 5);
+       r < rows; r += static_cast<int64_t>(gridDim.x) * warps_per_block) {
+    float mx = -INFINITY;
+    for (int j = lane; j < cols; j += 32) mx = fmaxf(mx, load_col(zb, r, j));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float s = 0.f;
+    for (int j = lane; j < cols; j += 32) s += expf(load_col(zb, r, j) - mx);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float lse = logf(s);
+    const bool train = mask == nullptr || mask[r] != 0;
+    const int y = labels ? labels[r] : -1;
+    const float inv = static_cast<float>(inv_total);
+    for (int j = c0 + lane; j < c1; j += 32) {
+      const float lp = (load_col(zb, r, j) - mx) - lse;
+      if (logp) logp[r * ldl + (j - c0)] = lp;
+      if (G) {
+        float g = 0.f;
+        if (train) {
+          g = expf(lp) * inv;
+          if (j == y) g -= inv;
+        }
+        G[r * ldg + (j - c0)] = g;
+      }
+      if (train && j == y) loss += -static_cast<double>(lp);
+    }
+  }
+  // Deterministic block reduction in fp64.
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, o);
+  if (lane == 0) red[threadIdx.x >> 5] = loss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < warps_per_block; ++w) t += red[w];
+    partials[blockIdx.x] = t;
+  }
+}
+
+__global__ void sum_partials_kernel(const double* __restrict__ partials, int count,
+                                    double* out) {
+  __shared__ double red[256];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) t += partials[i];
+  red[threadIdx.x] = t;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+void launch_lsm(const RowBlocks& zb, int64_t rows, int c0, int c1, float* logp, int64_t ldl,
+                float* G, int64_t ldg, const int32_t* labels, const uint8_t* mask,
+                int64_t train_total, double* loss_out, cudaStream_t s) {
+  const int sms = num_sms(current_device());
+  int64_t blocks = ceil_div64(rows > 0 ? rows : 1, 8);
+  if (blocks > 4 * sms) blocks = 4 * sms;
+  if (blocks > kLossBlocks) blocks = kLossBlocks;
+  double* partials = nullptr;
+  CG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&partials), kLossBlocks * sizeof(double), s));
+  const double inv = train_total > 0 ? 1.0 / static_cast<double>(train_total) : 0.0;
+  logsoftmax_nll_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+      zb, rows, c0, c1, logp, ldl, G, ldg, labels, mask, inv, partials);
+  CG_LAUNCH_CHECK();
+  if (loss_out) {
+    sum_partials_kernel<<<1, 256, 0, s>>>(partials, static_cast<int>(blocks), loss_out);
+    CG_LAUNCH_CHECK();
+  }
+  CG_CUDA(cudaFreeAsync(partials, s));
+}
+
+__global__ void relu_kernel(const float* __restrict__ Z, int64_t rows, int cols, int64_t ldz,
+                            float* __restrict__ H, int64_t ldh) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / cols, c = e % cols;
+    const float z = Z[r * ldz + c];
+    H[r * ldh + c] = z > 0.f ? z : 0.f;
+  }
+}
+
+__global__ void sgd_kernel(float* __restrict__ W, const float* __restrict__ Y, int64_t count,
+                           float lr) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    W[e] -= lr * Y[e];
+}
+
+__global__ void copy2d_kernel(float* __restrict__ dst, int64_t ldd, const float* __restrict__ src,
+                              int64_t lds, int64_t rows, int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / cols, c = e % cols;
+    dst[r * ldd + c] = src[r * lds + c];
+  }
+}
+
+__global__ void transpose2d_kernel(float* __restrict__ dst, int64_t ldd,
+                                   const float* __restrict__ src, int64_t lds, int64_t rows,
+                                   int64_t cols) {
+  __shared__ float tile[32][33];
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = src[r * lds + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[c * ldd + r] = tile[threadIdx.x][i];
+  }
+}
+
+__global__ void fill_kernel(float* p, int64_t count, float v) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    p[e] = v;
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ s, float* __restrict__ d,
+                                  int64_t count) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d[e] = static_cast<float>(s[e]);
+}
+
+unsigned grid_for(int64_t total) {
+  const int sms = num_sms(current_device());
+  int64_t b = ceil_div64(total > 0 ? total : 1, 256);
+  if (b > 8 * sms) b = 8 * sms;
+  return static_cast<unsigned>(b);
+}
+
+}  // namespace
+
+void logsoftmax_nll(const float* Z, int64_t rows, int cols, int64_t ldz, int c0, int c1,
+                    float* logp, int64_t ldl, float* G, int64_t ldg, const int32_t* labels,
+                    const uint8_t* mask, int64_t train_total, double* loss_out,
+                    cudaStream_t stream) {
+  RowBlocks zb{};
+  zb.base = Z;
+  zb.block_stride = 0;
+  zb.ld = ldz;
+  zb.parts = 1;
+  zb.widths[0] = cols;
+  zb.offs[0] = 0;
+  zb.offs[1] = cols;
+  launch_lsm(zb, rows, c0, c1, logp, ldl, G, ldg, labels, mask, train_total, loss_out, stream);
+}
+
+void logsoftmax_nll_blocks(const float* base, int parts, const int* widths, int64_t block_stride,
+                           int64_t rows, int64_t ldz, int own_part, float* logp, int64_t ldl,
+                           float* G, int64_t ldg, const int32_t* labels, const uint8_t* mask,
+                           int64_t train_total, double* loss_out, cudaStream_t stream) {
+  require(parts >= 1 && parts <= kMaxParts, "logsoftmax_nll_blocks: 1..8 column blocks");
+  RowBlocks zb{};
+  zb.base = base;
+  zb.block_stride = block_stride;
+  zb.ld = ldz;
+  zb.parts = parts;
+  zb.offs[0] = 0;
+  for (int q = 0; q < parts; ++q) {
+    zb.widths[q] = widths[q];
+    zb.offs[q + 1] = zb.offs[q] + widths[q];
+  }
+  for (int q = parts; q < kMaxParts; ++q) zb.offs[q + 1] = zb.offs[parts];
+  launch_lsm(zb, rows, zb.offs[own_part], zb.offs[own_part + 1], logp, ldl, G, ldg, labels, mask,
+             train_total, loss_out, stream);
+}
+
+void relu(const float* Z, int64_t rows, int cols, int64_t ldz, float* H, int64_t ldh,
+          cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return;
+  relu_kernel<<<grid_for(rows * cols), 256, 0, stream>>>(Z, rows, cols, ldz, H, ldh);
+  CG_LAUNCH_CHECK();
+}
+
+void sgd(float* W, const float* Y, int64_t count, float lr, cudaStream_t stream) {
+  if (count <= 0) return;
+  sgd_kernel<<<grid_for(count), 256, 0, stream>>>(W, Y, count, lr);
+  CG_LAUNCH_CHECK();
+}
+
+void copy2d(float* dst, int64_t ldd, const float* src, int64_t lds, int64_t rows, int64_t cols,
+            cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return;
+  if (ldd == cols && lds == cols) {
+    CG_CUDA(cudaMemcpyAsync(dst, src, rows * cols * sizeof(float), cudaMemcpyDeviceToDevice,
+                            stream));
+    return;
+  }
+  copy2d_kernel<<<grid_for(rows * cols), 256, 0, stream>>>(dst, ldd, src, lds, rows, cols);
+  CG_LAUNCH_CHECK();
+}
+
+void transpose2d(float* dst, int64_t ldd, const float* src, int64_t lds, int64_t rows,
+                 int64_t cols, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return;
+  dim3 grid(static_cast<unsigned>(ceil_div64(cols, 32)), static_cast<unsigned>(ceil_div64(rows, 32)));
+  transpose2d_kernel<<<grid, dim3(32, 8), 0, stream>>>(dst, ldd, src, lds, rows, cols);
+  CG_LAUNCH_CHECK();
+}
+
+void fill(float* p, int64_t count, float v, cudaStream_t stream) {
+  if (count <= 0) return;
+  fill_kernel<<<grid_for(count), 256, 0, stream>>>(p, count, v);
+  CG_LAUNCH_CHECK();
+}
+
+void f64_to_f32(const double* src, float* dst, int64_t count, cudaStream_t stream) {
+  if (count <= 0) return;
+  f64_to_f32_kernel<<<grid_for(count), 256, 0, stream>>>(src, dst, count);
+  CG_LAUNCH_CHECK();
+}
+
+}  // namespace kern
+}  // namespace cagnet

@@ -1,0 +1,72 @@
+// Internal launchers for the hot-path kernels (sm_100a).  The C-ABI in
+// capi.cu and the C++ trainers call these; nothing here allocates except the
+// split-K workspace, which is stream-ordered.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace cagnet {
+namespace kern {
+
+// ---- K1: CSR SpMM (csr.cpp:164-179) ---------------------------------------
+// T[i, 0:f] = (accumulate ? T[i, 0:f] : 0) + sum_k vals[k] * H[col[k], 0:f]
+// with the nonzeros of each row folded in ascending order (the reference's
+// accumulation order), one fp32 FMA per term.
+void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
+              const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
+              cudaStream_t stream);
+
+// ---- K2: tcgen05 split-TF32 GEMM (dense.cpp:37-70) ---------------------------
+// op(A) m x k: element (i, p) at A[i * a_sm + p * a_sk]
+// op(B) k x n: element (p, j) at B[p * b_sk + j * b_sn]
+enum Epilogue { EPI_NONE = 0, EPI_RELU = 1, EPI_RELU_PRIME = 2 };
+struct GemmDesc {
+  int64_t m = 0, n = 0, k = 0;
+  const float* A = nullptr;
+  int64_t a_sm = 0, a_sk = 0;
+  const float* B = nullptr;
+  int64_t b_sk = 0, b_sn = 0;
+  float* C = nullptr;
+  int64_t ldc = 0;
+  bool accumulate = false;
+  int epilogue = EPI_NONE;
+  const float* aux = nullptr;  // RELU_PRIME: pre-activation Z (ldaux)
+  int64_t ldaux = 0;
+  float* aux_out = nullptr;    // RELU: receives relu(Z) (ldao)
+  int64_t ldao = 0;
+};
+void gemm_tf32x3(const GemmDesc& d, cudaStream_t stream);
+
+// ---- K3: fused elementwise ----------------------------------------------------
+// log_softmax_rows + nll_tile (dense.cpp:94-136) over full rows of Z; writes
+// the column tile [c0, c1) of logp and G; loss partial (fp64, undivided) is
+// written to *loss_out (device) deterministically.
+void logsoftmax_nll(const float* Z, int64_t rows, int cols, int64_t ldz, int c0, int c1,
+                    float* logp, int64_t ldl, float* G, int64_t ldg, const int32_t* labels,
+                    const uint8_t* mask, int64_t train_total, double* loss_out,
+                    cudaStream_t stream);
+// Variant for tiles whose full rows are spread over `parts` column blocks laid
+// out back to back (the 2D/3D all-gather result): block q holds rows x
+// width_q columns at base + q * block_stride with leading dim ldz.
+void logsoftmax_nll_blocks(const float* base, int parts, const int* widths, int64_t block_stride,
+                           int64_t rows, int64_t ldz, int own_part, float* logp, int64_t ldl,
+                           float* G, int64_t ldg, const int32_t* labels, const uint8_t* mask,
+                           int64_t train_total, double* loss_out, cudaStream_t stream);
+void relu(const float* Z, int64_t rows, int cols, int64_t ldz, float* H, int64_t ldh,
+          cudaStream_t stream);
+void sgd(float* W, const float* Y, int64_t count, float lr, cudaStream_t stream);
+// dst[r, 0:cols] = src[r, 0:cols] for strided row-major blocks.
+void copy2d(float* dst, int64_t ldd, const float* src, int64_t lds, int64_t rows, int64_t cols,
+            cudaStream_t stream);
+// dst (cols x rows, ldd) = src^T (rows x cols, lds)
+void transpose2d(float* dst, int64_t ldd, const float* src, int64_t lds, int64_t rows,
+                 int64_t cols, cudaStream_t stream);
+void fill(float* p, int64_t count, float v, cudaStream_t stream);
+// fp64 host-converted values → fp32 device values happen on the host; this
+// converts device fp64 → fp32.
+void f64_to_f32(const double* src, float* dst, int64_t count, cudaStream_t stream);
+
+}  // namespace kern
+}  // namespace cagnet

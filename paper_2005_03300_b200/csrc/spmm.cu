@@ -1,0 +1,246 @@
+// K1 — CSR SpMM for the GCN propagation Aᵀ·H (forward) and A·G (backward).
+//
+// Reference: spmm_add, csr.cpp:164-179 — acc(i,:) += v_k * H(c_k,:) for the
+// nonzeros of row i in ascending order.  This kernel keeps that order per
+// output element (one fp32 FMA per nonzero, sequential per lane), so the only
+// difference to the fp64 reference is fp32 rounding.
+//
+// Mapping: a row group of LPR lanes owns one output row; each lane holds VPL
+// 128-bit column vectors of the row in registers.  Column indices and values
+// are loaded once, coalesced, by the LPR lanes of the group and broadcast to
+// the group with warp shuffles; every gathered H row is read as LPR*16 B
+// contiguous segments.  Rows of an Erdős–Rényi graph have near-uniform length
+// (binomial degree), so row-group mapping balances without merge-path.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace cagnet {
+namespace kern {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<4> {
+  using T = float4;
+};
+template <>
+struct VecT<1> {
+  using T = float;
+};
+
+__device__ __forceinline__ void fma_vec(float4& acc, float v, const float4& h) {
+  acc.x = fmaf(v, h.x, acc.x);
+  acc.y = fmaf(v, h.y, acc.y);
+  acc.z = fmaf(v, h.z, acc.z);
+  acc.w = fmaf(v, h.w, acc.w);
+}
+__device__ __forceinline__ void fma_vec(float& acc, float v, const float& h) {
+  acc = fmaf(v, h, acc);
+}
+__device__ __forceinline__ void zero_vec(float4& a) { a = make_float4(0.f, 0.f, 0.f, 0.f); }
+__device__ __forceinline__ void zero_vec(float& a) { a = 0.f; }
+
+// Loads vector `vec` of a row (f valid floats) with a scalar tail.
+__device__ __forceinline__ float4 load_vec(const float* __restrict__ row, int vec, int f) {
+  const int c = vec * 4;
+  if (c + 4 <= f) return __ldg(reinterpret_cast<const float4*>(row + c));
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c + 0 < f) r.x = __ldg(row + c + 0);
+  if (c + 1 < f) r.y = __ldg(row + c + 1);
+  if (c + 2 < f) r.z = __ldg(row + c + 2);
+  return r;
+}
+__device__ __forceinline__ float load_vec1(const float* __restrict__ row, int vec) {
+  return __ldg(row + vec);
+}
+
+__device__ __forceinline__ void store_vec(float* row, int vec, int f, const float4& v) {
+  const int c = vec * 4;
+  if (c + 4 <= f) {
+    *reinterpret_cast<float4*>(row + c) = v;
+    return;
+  }
+  if (c + 0 < f) row[c + 0] = v.x;
+  if (c + 1 < f) row[c + 1] = v.y;
+  if (c + 2 < f) row[c + 2] = v.z;
+}
+
+// VEC = 4: 16-byte vectors (requires 16 B aligned rows); VEC = 1: scalars.
+template <int VEC, int LPR, int VPL, bool ACC>
+__global__ void __launch_bounds__(kThreads)
+    spmm_rows_kernel(int64_t n_rows, const int64_t* __restrict__ row_ptr,
+                     const int32_t* __restrict__ col_idx, const float* __restrict__ vals,
+                     const float* __restrict__ H, int64_t ldh, int f, float* __restrict__ T,
+                     int64_t ldt) {
+  using V = typename VecT<VEC>::T;
+  constexpr int RPW = 32 / LPR;  // rows per warp
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % LPR;
+  const int grp = lane / LPR;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
+  const int64_t row = warp * RPW + grp;
+  const int nvec = (f + VEC - 1) / VEC;
+
+  int64_t beg = 0, len = 0;
+  if (row < n_rows) {
+    beg = row_ptr[row];
+    len = row_ptr[row + 1] - beg;
+  }
+  // Uniform trip count across the warp so every lane joins the shuffles.
+  int64_t maxlen = len;
+#pragma unroll
+  for (int o = 16; o >= LPR; o >>= 1) {
+    const int64_t other = __shfl_xor_sync(0xffffffffu, maxlen, o);
+    maxlen = other > maxlen ? other : maxlen;
+  }
+
+  V acc[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    zero_vec(acc[i]);
+    const int vec = sub + i * LPR;
+    if (ACC && row < n_rows && vec < nvec) {
+      if constexpr (VEC == 4)
+        acc[i] = load_vec(T + row * ldt, vec, f);
+      else
+        acc[i] = T[row * ldt + vec];
+    }
+  }
+
+  const int src0 = grp * LPR;
+  for (int64_t base = 0; base < maxlen; base += LPR) {
+    int c = 0;
+    float v = 0.f;
+    if (base + sub < len) {
+      c = __ldg(col_idx + beg + base + sub);
+      v = __ldg(vals + beg + base + sub);
+    }
+    const int64_t remain = len - base;  // nonzeros of this group left in the chunk
+#pragma unroll 4
+    for (int t = 0; t < LPR; ++t) {
+      const int cc = __shfl_sync(0xffffffffu, c, src0 + t);
+      const float vv = __shfl_sync(0xffffffffu, v, src0 + t);
+      if (t < remain) {
+        const float* hrow = H + static_cast<int64_t>(cc) * ldh;
+        V hv[VPL];
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) {
+          const int vec = sub + i * LPR;
+          zero_vec(hv[i]);
+          if (vec < nvec) {
+            if constexpr (VEC == 4)
+              hv[i] = load_vec(hrow, vec, f);
+            else
+              hv[i] = load_vec1(hrow, vec);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) fma_vec(acc[i], vv, hv[i]);
+      }
+    }
+  }
+
+  if (row < n_rows) {
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) {
+      const int vec = sub + i * LPR;
+      if (vec < nvec) {
+        if constexpr (VEC == 4)
+          store_vec(T + row * ldt, vec, f, acc[i]);
+        else
+          T[row * ldt + vec] = acc[i];
+      }
+    }
+  }
+}
+
+template <int VEC, int LPR, int VPL>
+void launch_one(int64_t n_rows, const int64_t* rp, const int32_t* ci, const float* v,
+                const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool acc,
+                cudaStream_t s) {
+  constexpr int rows_per_block = (kThreads / 32) * (32 / LPR);
+  const int64_t blocks = ceil_div64(n_rows, rows_per_block);
+  if (acc)
+    spmm_rows_kernel<VEC, LPR, VPL, true>
+        <<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(n_rows, rp, ci, v, H, ldh, f, T, ldt);
+  else
+    spmm_rows_kernel<VEC, LPR, VPL, false>
+        <<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(n_rows, rp, ci, v, H, ldh, f, T, ldt);
+  CG_LAUNCH_CHECK();
+}
+
+template <int VEC, int LPR>
+void launch_vpl(int vpl, int64_t n_rows, const int64_t* rp, const int32_t* ci, const float* v,
+                const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool acc,
+                cudaStream_t s) {
+  switch (vpl) {
+    case 1: return launch_one<VEC, LPR, 1>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    case 2: return launch_one<VEC, LPR, 2>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    case 3: return launch_one<VEC, LPR, 3>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    case 4: return launch_one<VEC, LPR, 4>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    case 5: return launch_one<VEC, LPR, 5>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    case 6: return launch_one<VEC, LPR, 6>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    case 7: return launch_one<VEC, LPR, 7>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    default: return launch_one<VEC, LPR, 8>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+  }
+}
+
+// Picks lanes-per-row (4..32) and vectors-per-lane (<= 8) maximising the share
+// of active vector slots; ties go to wider groups (longer coalesced segments).
+void pick_shape(int nvec, int* lpr, int* vpl) {
+  int best_l = 32, best_v = (nvec + 31) / 32;
+  double best_u = -1.0;
+  for (int l = 4; l <= 32; l *= 2) {
+    const int v = (nvec + l - 1) / l;
+    if (v > 8) continue;
+    const double u = static_cast<double>(nvec) / (l * v);
+    if (u >= best_u) {
+      best_u = u;
+      best_l = l;
+      best_v = v;
+    }
+  }
+  *lpr = best_l;
+  *vpl = best_v < 1 ? 1 : best_v;
+}
+
+template <int VEC>
+void dispatch(int64_t n_rows, const int64_t* rp, const int32_t* ci, const float* v,
+              const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool acc,
+              cudaStream_t s) {
+  const int nvec = (f + VEC - 1) / VEC;
+  int lpr, vpl;
+  pick_shape(nvec, &lpr, &vpl);
+  switch (lpr) {
+    case 4: return launch_vpl<VEC, 4>(vpl, n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    case 8: return launch_vpl<VEC, 8>(vpl, n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    case 16: return launch_vpl<VEC, 16>(vpl, n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    default: return launch_vpl<VEC, 32>(vpl, n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+  }
+}
+
+}  // namespace
+
+void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
+              const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
+              cudaStream_t stream) {
+  if (n_rows <= 0 || f <= 0) return;
+  const bool aligned = (ldh % 4 == 0) && (ldt % 4 == 0) &&
+                       (reinterpret_cast<uintptr_t>(H) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(T) % 16 == 0);
+  // Column chunks of at most 32 lanes * 8 vectors keep accumulators in registers.
+  const int chunk = aligned ? 32 * 8 * 4 : 32 * 8;
+  for (int c0 = 0; c0 < f; c0 += chunk) {
+    const int fc = f - c0 < chunk ? f - c0 : chunk;
+    if (aligned)
+      dispatch<4>(n_rows, row_ptr, col_idx, vals, H + c0, ldh, fc, T + c0, ldt, accumulate, stream);
+    else
+      dispatch<1>(n_rows, row_ptr, col_idx, vals, H + c0, ldh, fc, T + c0, ldt, accumulate, stream);
+  }
+}
+
+}  // namespace kern
+}  // namespace cagnet

@@ -1,0 +1,145 @@
+// Block-row strategies: 1D (dist_1d.cpp:20-89) and 1.5D with replication
+// factor c (dist_15d.cpp:20-104).  1D is the c = 1 case of the same code:
+// rank (i, j) of the (P/c) x c grid owns block row i, walks the propagation
+// stages [chunk_begin(j), chunk_end(j)) (dist_impl.hpp:50-53) broadcasting
+// embedding panels down its column group, and the per-column partials meet in
+// a row all-reduce.  Broadcast panels are double-buffered on the comm stream
+// so stage q+1's NCCL broadcast overlaps stage q's SpMM.
+#include "kernels.cuh"
+#include "trainer.hpp"
+
+namespace cagnet {
+namespace {
+
+class TrainerRows final : public Trainer {
+ public:
+  using Trainer::Trainer;
+
+  BlockRange tile_rows(int r) const override { return tile_rows_of(grid_, data_.n, r); }
+  BlockRange tile_cols(int r, int64_t width) const override { return tile_cols_of(grid_, r, width); }
+  int tile_owner(int r) const override { return tile_owner_of(grid_, r); }
+
+  void distribute() override {
+    init_tiles();
+    const BlockRange rows = tile_rows(rank_);
+    a_parts_.clear();
+    at_parts_.clear();
+    for (int q = 0; q < blocks(); ++q) {
+      const BlockRange cols = block_range(data_.n, blocks(), q);
+      a_parts_.push_back(extract_block_device(data_.adj, rows.begin, rows.end, cols.begin, cols.end, cs_));
+      at_parts_.push_back(extract_block_device(data_.adj_t, rows.begin, rows.end, cols.begin, cols.end, cs_));
+    }
+    int64_t maxf = 0;
+    for (int64_t d : dims_) maxf = d > maxf ? d : maxf;
+    const int64_t step = ceil_div64(data_.n, blocks());
+    acc_.alloc(rows.size(), maxf);
+    for (int i = 0; i < 2; ++i) panel_[i].alloc(step, maxf);
+    CG_CUDA(cudaDeviceSynchronize());
+  }
+
+  void forward_layer(int l) override {
+    if (l < 1 || l >= num_layers())
+      throw std::invalid_argument("run_forward_layer: layer " + std::to_string(l) + " outside [1, " +
+                                  std::to_string(num_layers()) + ")");
+    const int64_t fin = dims_[static_cast<size_t>(l - 1)];
+    const Mat& h = h_[static_cast<size_t>(l - 1)].m;
+    Mat t = view(acc_, h.rows, fin);
+    stages(at_parts_, h, t);
+    if (!one_d()) row_reduce(t);
+    Mat z = z_[static_cast<size_t>(l - 1)].m;
+    if (l + 1 == num_layers()) {
+      gemm_aw(t, l - 1, 0, 0, z, false, kern::EPI_NONE, Mat{});
+      // log_softmax (dense.cpp:94-107) fused with nll_tile (dense.cpp:109-136).
+      Mat hl = h_[static_cast<size_t>(l)].m;
+      Mat g = g_[static_cast<size_t>(l - 1)].m;
+      kern::logsoftmax_nll(z.p, z.rows, static_cast<int>(z.cols), z.ld, 0, static_cast<int>(z.cols), hl.p,
+                           hl.ld, g.p, g.ld, labels_.get(), mask_.get(), train_total_,
+                           loss_partial_.get(), cs_);
+    } else {
+      gemm_aw(t, l - 1, 0, 0, z, false, kern::EPI_RELU, h_[static_cast<size_t>(l)].m);
+    }
+  }
+
+  void backward_and_step() override {
+    const int L = num_layers();
+    // Only column 0 contributes the loss so replicated rows count once.
+    if (grid_.col_of(rank_) != 0) CG_CUDA(cudaMemsetAsync(loss_partial_.get(), 0, sizeof(double), cs_));
+    loss_all_reduce(loss_partial_.get());
+    for (int l = L - 1; l >= 1; --l) {
+      const Mat& g = g_[static_cast<size_t>(l - 1)].m;
+      Mat s = view(acc_, g.rows, dims_[static_cast<size_t>(l)]);
+      stages(a_parts_, g, s);
+      if (!one_d()) row_reduce(s);
+      Mat y = Y_[static_cast<size_t>(l - 1)].m;
+      if (grid_.col_of(rank_) == 0)
+        gemm_hts(h_[static_cast<size_t>(l - 1)].m, s, y, false);
+      else
+        CG_CUDA(cudaMemsetAsync(y.p, 0, y.rows * y.ld * sizeof(float), cs_));
+      ms_after_cs();
+      comm_->all_reduce(grid_.world(), y.p, static_cast<size_t>(y.rows * y.cols), ncclFloat32,
+                        Category::Reduce, words(y), ms_);
+      cs_after_ms();
+      if (l >= 2) {
+        const Mat& zp = z_[static_cast<size_t>(l - 2)].m;
+        gemm_swt(s, l - 1, 0, 0, g_[static_cast<size_t>(l - 2)].m, false, kern::EPI_RELU_PRIME, &zp);
+      }
+    }
+    sgd_all();
+  }
+
+ private:
+  bool one_d() const { return grid_.kind() == GridKind::Row1D; }
+  int blocks() const { return grid_.rows(); }
+  int repl() const { return grid_.cols(); }
+  int chunk_begin(int j) const { return j * (blocks() / repl()); }
+  int chunk_end(int j) const { return j + 1 == repl() ? blocks() : (j + 1) * (blocks() / repl()); }
+  const Group& stage_group() const { return one_d() ? grid_.world() : grid_.col_group(rank_); }
+
+  static Mat view(OwnedMat& buf, int64_t rows, int64_t cols) {
+    return Mat{buf.m.p, rows, cols, padded_ld(cols)};
+  }
+
+  // out = sum over this column's stages q of parts[q] * (tile of rank (q, j)).
+  void stages(const std::vector<DeviceCsr>& parts, const Mat& mine, Mat out) {
+    const int j = grid_.col_of(rank_);
+    const Group& grp = stage_group();
+    const bool comm = grp.size() > 1;
+    ms_after_cs();
+    int idx = 0;
+    for (int q = chunk_begin(j); q < chunk_end(j); ++q, ++idx) {
+      const int root = one_d() ? q : grid_.rank_at(q, j);
+      const int b = idx & 1;
+      Mat panel = root == rank_ ? mine
+                                : Mat{panel_[b].m.p, parts[static_cast<size_t>(q)].n_cols, mine.cols, mine.ld};
+      if (comm) {
+        if (idx >= 2) CG_CUDA(cudaStreamWaitEvent(ms_, ev_free_[b], 0));
+        bcast_mat(grp, root, panel, Category::DBcast);
+        CG_CUDA(cudaEventRecord(ev_ready_[b], ms_));
+        CG_CUDA(cudaStreamWaitEvent(cs_, ev_ready_[b], 0));
+      }
+      spmm(parts[static_cast<size_t>(q)], panel, out, idx > 0);
+      if (comm) CG_CUDA(cudaEventRecord(ev_free_[b], cs_));
+    }
+    if (idx == 0) CG_CUDA(cudaMemsetAsync(out.p, 0, out.rows * out.ld * sizeof(float), cs_));
+  }
+
+  void row_reduce(Mat m) {
+    ms_after_cs();
+    comm_->all_reduce(grid_.row_group(rank_), m.p, static_cast<size_t>(m.rows * m.ld), ncclFloat32,
+                      Category::Reduce, words(m), ms_);
+    cs_after_ms();
+  }
+
+  OwnedMat acc_;
+  OwnedMat panel_[2];
+};
+
+}  // namespace
+
+std::unique_ptr<Trainer> make_trainer_rows(const DeviceDataset& data, std::vector<int64_t> dims,
+                                           const double* weights, double lr, Strategy strat,
+                                           int rank, const ncclUniqueId* id) {
+  return std::make_unique<TrainerRows>(data, std::move(dims), weights, lr, strat, rank, id);
+}
+
+}  // namespace cagnet

@@ -1,0 +1,460 @@
+// Trainer base: tiles, weights, streams, shared GEMM/SpMM plumbing, and the
+// device GraphDataset constructors.
+#include <cstring>
+
+#include "kernels.cuh"
+#include "rng.hpp"
+#include "trainer.hpp"
+
+namespace cagnet {
+
+// ---- datasets ----------------------------------------------------------------
+namespace {
+
+void finish_dataset(DeviceDataset& d, const std::vector<int32_t>& labels,
+                    const std::vector<uint8_t>& mask, cudaStream_t s) {
+  d.labels.resize(static_cast<size_t>(d.n));
+  d.mask.resize(static_cast<size_t>(d.n));
+  if (d.n) {
+    CG_CUDA(cudaMemcpyAsync(d.labels.get(), labels.data(), d.n * sizeof(int32_t),
+                            cudaMemcpyHostToDevice, s));
+    CG_CUDA(cudaMemcpyAsync(d.mask.get(), mask.data(), d.n, cudaMemcpyHostToDevice, s));
+  }
+  int64_t cnt = 0;
+  for (int64_t i = 0; i < d.n; ++i) {
+    if (!mask[static_cast<size_t>(i)]) continue;
+    ++cnt;
+    if (labels[static_cast<size_t>(i)] < 0 || labels[static_cast<size_t>(i)] >= d.num_classes)
+      throw std::invalid_argument("GraphDataset: label " + std::to_string(labels[static_cast<size_t>(i)]) +
+                                  " of training vertex " + std::to_string(i) + " outside [0, " +
+                                  std::to_string(d.num_classes) + ")");
+  }
+  d.train_count = cnt;
+  CG_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+std::unique_ptr<DeviceDataset> dataset_generate(int64_t n, double degree, int64_t f,
+                                                int64_t classes, uint64_t sg, uint64_t sf,
+                                                uint64_t sl, int generator) {
+  require(classes > 0, "random_labels: need at least one class");
+  auto d = std::make_unique<DeviceDataset>();
+  d->device = current_device();
+  d->n = n;
+  d->f = f;
+  d->num_classes = classes;
+  cudaStream_t s;
+  CG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  try {
+    {
+      DeviceCsr raw = generator == 0 ? er_generate_device(n, degree, sg, s)
+                                     : er_skip_generate_device(n, degree, sg, s);
+      d->adj = normalize_device(raw, nullptr, s);
+    }
+    d->adj_t = transpose_device(d->adj, s);
+    d->ldf = padded_ld(f);
+    d->features.resize(static_cast<size_t>(n * d->ldf));
+    CG_CUDA(cudaMemsetAsync(d->features.get(), 0, n * d->ldf * sizeof(float), s));
+    random_features_device(n, f, sf, d->features.get(), d->ldf, s);
+    std::vector<int32_t> labels = random_labels_host(n, classes, sl);
+    std::vector<uint8_t> mask(static_cast<size_t>(n), 1);
+    finish_dataset(*d, labels, mask, s);
+  } catch (...) {
+    cudaStreamDestroy(s);
+    throw;
+  }
+  CG_CUDA(cudaStreamDestroy(s));
+  return d;
+}
+
+std::unique_ptr<DeviceDataset> dataset_make(int64_t n, const int64_t* raw_rp,
+                                            const int64_t* raw_ci, const double* features,
+                                            int64_t f, const int64_t* labels,
+                                            const uint8_t* mask, int64_t classes) {
+  auto d = std::make_unique<DeviceDataset>();
+  d->device = current_device();
+  d->n = n;
+  d->f = f;
+  d->num_classes = classes;
+  cudaStream_t s;
+  CG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  try {
+    // validate_csr-style checks on the raw structure (csr.cpp:25-48).
+    require(raw_rp[0] == 0, "make_dataset: row_ptr must start at 0");
+    for (int64_t i = 0; i < n; ++i) {
+      require(raw_rp[i] <= raw_rp[i + 1], "make_dataset: row_ptr decreases at row " + std::to_string(i));
+      for (int64_t k = raw_rp[i]; k < raw_rp[i + 1]; ++k) {
+        require(raw_ci[k] >= 0 && raw_ci[k] < n, "make_dataset: column index out of range in row " + std::to_string(i));
+        require(k == raw_rp[i] || raw_ci[k - 1] < raw_ci[k],
+                "make_dataset: columns not strictly increasing in row " + std::to_string(i));
+      }
+    }
+    {
+      DeviceCsr raw = upload_csr(n, n, raw_rp, raw_ci, nullptr, s);
+      d->adj = normalize_device(raw, nullptr, s);
+    }
+    d->adj_t = transpose_device(d->adj, s);
+    d->ldf = padded_ld(f);
+    d->features.resize(static_cast<size_t>(n * d->ldf));
+    std::vector<float> hf(static_cast<size_t>(n * d->ldf), 0.f);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < f; ++j) hf[static_cast<size_t>(i * d->ldf + j)] = static_cast<float>(features[i * f + j]);
+    CG_CUDA(cudaMemcpyAsync(d->features.get(), hf.data(), hf.size() * sizeof(float),
+                            cudaMemcpyHostToDevice, s));
+    std::vector<int32_t> lab(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) lab[static_cast<size_t>(i)] = static_cast<int32_t>(labels[i]);
+    std::vector<uint8_t> m(static_cast<size_t>(n), 1);
+    if (mask) std::memcpy(m.data(), mask, static_cast<size_t>(n));
+    finish_dataset(*d, lab, m, s);
+  } catch (...) {
+    cudaStreamDestroy(s);
+    throw;
+  }
+  CG_CUDA(cudaStreamDestroy(s));
+  return d;
+}
+
+// ---- OwnedMat ------------------------------------------------------------------
+void OwnedMat::alloc(int64_t rows, int64_t cols, int64_t ld, int64_t capacity_rows) {
+  if (ld < 0) ld = padded_ld(cols);
+  const int64_t cap = capacity_rows > rows ? capacity_rows : rows;
+  const size_t count = static_cast<size_t>((cap > 0 ? cap : 1) * (ld > 0 ? ld : 1));
+  buf.resize(count);
+  CG_CUDA(cudaMemset(buf.get(), 0, count * sizeof(float)));
+  m.p = buf.get();
+  m.rows = rows;
+  m.cols = cols;
+  m.ld = ld;
+}
+
+// ---- Trainer ---------------------------------------------------------------------
+Trainer::Trainer(const DeviceDataset& data, std::vector<int64_t> dims, const double* weights,
+                 double lr, Strategy strat, int rank, const ncclUniqueId* id)
+    : data_(data),
+      dims_(std::move(dims)),
+      lr_(lr),
+      strat_(strat),
+      grid_(ProcessGrid::make(strat)),
+      rank_(rank),
+      train_total_(data.train_count),
+      device_(data.device) {
+  require(dims_.size() >= 2, "model: need at least two layers");
+  for (int64_t d : dims_) require(d > 0, "init_glorot: zero-width layer");
+  require(dims_.front() == data.f, "model: input width " + std::to_string(dims_.front()) +
+                                       " but dataset has " + std::to_string(data.f) + " features");
+  require(dims_.back() == data.num_classes,
+          "model: output width " + std::to_string(dims_.back()) + " but dataset has " +
+              std::to_string(data.num_classes) + " classes");
+  require(train_total_ > 0, "distributed training: empty training set");
+  require(rank >= 0 && rank < grid_.ranks(), "trainer: rank outside the grid");
+  CG_CUDA(cudaSetDevice(device_));
+  CG_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+  CG_CUDA(cudaStreamCreateWithFlags(&ms_, cudaStreamNonBlocking));
+  CG_CUDA(cudaEventCreateWithFlags(&ev_cs_, cudaEventDisableTiming));
+  CG_CUDA(cudaEventCreateWithFlags(&ev_ms_, cudaEventDisableTiming));
+  for (int i = 0; i < 2; ++i) {
+    CG_CUDA(cudaEventCreateWithFlags(&ev_ready_[i], cudaEventDisableTiming));
+    CG_CUDA(cudaEventCreateWithFlags(&ev_free_[i], cudaEventDisableTiming));
+  }
+  CG_CUDA(cudaEventCreate(&ev_t0_));
+  CG_CUDA(cudaEventCreate(&ev_t1_));
+  comm_ = std::make_unique<Comm>(grid_, rank, id);
+
+  const int L = num_layers();
+  W_.resize(static_cast<size_t>(L - 1));
+  Y_.resize(static_cast<size_t>(L - 1));
+  int64_t off = 0;
+  const int side = grid_.kind() == GridKind::Grid2D || grid_.kind() == GridKind::Grid3D ? grid_.rows() : 1;
+  for (int l = 0; l + 1 < L; ++l) {
+    const int64_t r = dims_[static_cast<size_t>(l)], c = dims_[static_cast<size_t>(l + 1)];
+    W_[static_cast<size_t>(l)].alloc(r, c, c);
+    // Y gets the padded slot rows of the 2D/3D row all-gather.
+    Y_[static_cast<size_t>(l)].alloc(r, c, c, side * ceil_div64(r, side));
+    std::vector<float> wf(static_cast<size_t>(r * c));
+    for (int64_t e = 0; e < r * c; ++e) wf[static_cast<size_t>(e)] = static_cast<float>(weights[off + e]);
+    CG_CUDA(cudaMemcpy(W_[static_cast<size_t>(l)].m.p, wf.data(), wf.size() * sizeof(float),
+                       cudaMemcpyHostToDevice));
+    off += r * c;
+  }
+  loss_partial_.resize(1);
+  CG_CUDA(cudaMemset(loss_partial_.get(), 0, sizeof(double)));
+  losses_dev_.resize(4096);
+}
+
+Trainer::~Trainer() {
+  cudaSetDevice(device_);
+  if (cs_) cudaStreamSynchronize(cs_);
+  if (ms_) cudaStreamSynchronize(ms_);
+  comm_.reset();
+  for (cudaEvent_t e : {ev_cs_, ev_ms_, ev_t0_, ev_t1_, ev_ready_[0], ev_ready_[1], ev_free_[0], ev_free_[1]})
+    if (e) cudaEventDestroy(e);
+  if (cs_) cudaStreamDestroy(cs_);
+  if (ms_) cudaStreamDestroy(ms_);
+}
+
+void Trainer::init_tiles() {
+  const int L = num_layers();
+  const BlockRange rows = tile_rows(rank_);
+  h_.clear();
+  z_.clear();
+  g_.clear();
+  h_.resize(static_cast<size_t>(L));
+  z_.resize(static_cast<size_t>(L - 1));
+  g_.resize(static_cast<size_t>(L - 1));
+  for (int l = 0; l < L; ++l) {
+    const BlockRange cols = tile_cols(rank_, dims_[static_cast<size_t>(l)]);
+    h_[static_cast<size_t>(l)].alloc(rows.size(), cols.size());
+    if (l > 0) {
+      z_[static_cast<size_t>(l - 1)].alloc(rows.size(), cols.size());
+      g_[static_cast<size_t>(l - 1)].alloc(rows.size(), cols.size());
+    }
+  }
+  const BlockRange fc = tile_cols(rank_, data_.f);
+  kern::copy2d(h_[0].m.p, h_[0].m.ld, data_.features.get() + rows.begin * data_.ldf + fc.begin,
+               data_.ldf, rows.size(), fc.size(), cs_);
+  labels_.resize(static_cast<size_t>(rows.size()));
+  mask_.resize(static_cast<size_t>(rows.size()));
+  if (rows.size()) {
+    CG_CUDA(cudaMemcpyAsync(labels_.get(), data_.labels.get() + rows.begin,
+                            rows.size() * sizeof(int32_t), cudaMemcpyDeviceToDevice, cs_));
+    CG_CUDA(cudaMemcpyAsync(mask_.get(), data_.mask.get() + rows.begin, rows.size(),
+                            cudaMemcpyDeviceToDevice, cs_));
+  }
+}
+
+void Trainer::ms_after_cs() {
+  CG_CUDA(cudaEventRecord(ev_cs_, cs_));
+  CG_CUDA(cudaStreamWaitEvent(ms_, ev_cs_, 0));
+}
+void Trainer::cs_after_ms() {
+  CG_CUDA(cudaEventRecord(ev_ms_, ms_));
+  CG_CUDA(cudaStreamWaitEvent(cs_, ev_ms_, 0));
+}
+
+void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc) {
+  if (a.n_cols != h.rows)
+    throw std::invalid_argument("spmm: sparse is " + std::to_string(a.n_rows) + "x" +
+                                std::to_string(a.n_cols) + " but dense has " +
+                                std::to_string(h.rows) + " rows");
+  spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, acc);
+}
+
+void Trainer::spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32_t* ci,
+                       const float* v, const Mat& h, Mat out, bool acc) {
+  if (out.rows != rows || out.cols != h.cols)
+    throw std::invalid_argument("spmm: accumulator shape mismatch");
+  const int slot = prof_begin();
+  kern::spmm_csr(rows, rp, ci, v, h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld, acc, cs_);
+  if (slot >= 0) {
+    // B = 8(r+1) + 8 nnz + 4 f c + 4 f r (1 + acc); F = 2 nnz f.
+    const double f = static_cast<double>(h.cols), r = static_cast<double>(rows);
+    const double bytes = 8.0 * (r + 1) + 8.0 * nnz + 4.0 * f * h.rows + 4.0 * f * r * (acc ? 2 : 1);
+    prof_end(slot, "spmm", h.cols, bytes, 2.0 * nnz * f);
+  }
+}
+
+int Trainer::prof_begin() {
+  if (!timing_) return -1;
+  if (recs_used_ == recs_.size()) {
+    ProfRec r;
+    CG_CUDA(cudaEventCreate(&r.a));
+    CG_CUDA(cudaEventCreate(&r.b));
+    recs_.push_back(r);
+  }
+  const int slot = static_cast<int>(recs_used_++);
+  CG_CUDA(cudaEventRecord(recs_[static_cast<size_t>(slot)].a, cs_));
+  return slot;
+}
+
+void Trainer::prof_end(int slot, const char* kind, int64_t f, double bytes, double flops) {
+  ProfRec& r = recs_[static_cast<size_t>(slot)];
+  CG_CUDA(cudaEventRecord(r.b, cs_));
+  r.name = std::string(kind) + "_f" + std::to_string(f);
+  r.bytes = bytes;
+  r.flops = flops;
+}
+
+void Trainer::collect_profile() {
+  if (recs_used_ == 0) return;
+  CG_CUDA(cudaSetDevice(device_));
+  CG_CUDA(cudaStreamSynchronize(cs_));
+  for (size_t i = 0; i < recs_used_; ++i) {
+    float ms = 0.f;
+    CG_CUDA(cudaEventElapsedTime(&ms, recs_[i].a, recs_[i].b));
+    ProfEntry* e = nullptr;
+    for (auto& p : profile_)
+      if (p.name == recs_[i].name) e = &p;
+    if (!e) {
+      profile_.push_back(ProfEntry{recs_[i].name});
+      e = &profile_.back();
+    }
+    e->launches += 1;
+    e->ms += ms;
+    e->bytes += recs_[i].bytes;
+    e->flops += recs_[i].flops;
+  }
+  recs_used_ = 0;
+}
+
+double Trainer::step_host(const float* x_tile, const int32_t* labels_tile) {
+  CG_CUDA(cudaSetDevice(device_));
+  const Mat& h0 = h_.at(0).m;
+  if (h0.rows && h0.cols)
+    CG_CUDA(cudaMemcpy2DAsync(h0.p, h0.ld * sizeof(float), x_tile, h0.cols * sizeof(float),
+                              h0.cols * sizeof(float), h0.rows, cudaMemcpyHostToDevice, cs_));
+  if (h0.rows)
+    CG_CUDA(cudaMemcpyAsync(labels_.get(), labels_tile, h0.rows * sizeof(int32_t),
+                            cudaMemcpyHostToDevice, cs_));
+  epoch();
+  std::vector<double> l = run_epochs(0);
+  return losses_host_.empty() ? 0.0 : losses_host_.back();
+}
+
+void Trainer::gemm_aw(const Mat& a, int l, int64_t r0, int64_t c0, Mat c, bool acc, int epi,
+                      Mat aux_out) {
+  const Mat& w = W_[static_cast<size_t>(l)].m;
+  kern::GemmDesc d;
+  d.m = a.rows;
+  d.n = c.cols;
+  d.k = a.cols;
+  d.A = a.p;
+  d.a_sm = a.ld;
+  d.a_sk = 1;
+  d.B = w.p + r0 * w.ld + c0;
+  d.b_sk = w.ld;
+  d.b_sn = 1;
+  d.C = c.p;
+  d.ldc = c.ld;
+  d.accumulate = acc;
+  d.epilogue = epi;
+  d.aux_out = aux_out.p;
+  d.ldao = aux_out.ld;
+  run_gemm(d, "gemm_tw");
+}
+
+void Trainer::run_gemm(const kern::GemmDesc& d, const char* kind) {
+  const int slot = prof_begin();
+  kern::gemm_tf32x3(d, cs_);
+  if (slot >= 0) {
+    // 4 (m k + k n + m n) algorithmic bytes, 2 m n k flops.
+    const double m = static_cast<double>(d.m), n = static_cast<double>(d.n), k = static_cast<double>(d.k);
+    prof_end(slot, kind, d.k, 4.0 * (m * k + k * n + m * n * (d.accumulate ? 2 : 1)) +
+                                  (d.epilogue == kern::EPI_RELU ? 4.0 * m * n : 0.0) +
+                                  (d.epilogue == kern::EPI_RELU_PRIME ? 4.0 * m * n : 0.0),
+             2.0 * m * n * k);
+  }
+}
+
+void Trainer::gemm_hts(const Mat& h, const Mat& s, Mat c, bool acc) {
+  kern::GemmDesc d;
+  d.m = h.cols;
+  d.n = s.cols;
+  d.k = h.rows;
+  d.A = h.p;
+  d.a_sm = 1;
+  d.a_sk = h.ld;
+  d.B = s.p;
+  d.b_sk = s.ld;
+  d.b_sn = 1;
+  d.C = c.p;
+  d.ldc = c.ld;
+  d.accumulate = acc;
+  run_gemm(d, "gemm_hts");
+}
+
+void Trainer::gemm_swt(const Mat& s, int l, int64_t r0, int64_t c0, Mat c, bool acc, int epi,
+                       const Mat* aux) {
+  const Mat& w = W_[static_cast<size_t>(l)].m;
+  kern::GemmDesc d;
+  d.m = s.rows;
+  d.n = c.cols;
+  d.k = s.cols;
+  d.A = s.p;
+  d.a_sm = s.ld;
+  d.a_sk = 1;
+  d.B = w.p + r0 * w.ld + c0;
+  d.b_sk = 1;
+  d.b_sn = w.ld;
+  d.C = c.p;
+  d.ldc = c.ld;
+  d.accumulate = acc;
+  d.epilogue = epi;
+  if (aux) {
+    d.aux = aux->p;
+    d.ldaux = aux->ld;
+  }
+  run_gemm(d, "gemm_swt");
+}
+
+void Trainer::bcast_mat(const Group& g, int root, Mat m, Category cat) {
+  comm_->bcast(g, root, m.p, static_cast<size_t>(m.rows * m.ld), ncclFloat32, cat, words(m), ms_);
+}
+
+void Trainer::sgd_all() {
+  for (size_t l = 0; l < W_.size(); ++l)
+    kern::sgd(W_[l].m.p, Y_[l].m.p, W_[l].m.rows * W_[l].m.cols, static_cast<float>(lr_), cs_);
+}
+
+void Trainer::loss_all_reduce(double* partial_dev) {
+  ms_after_cs();
+  comm_->all_reduce(grid_.world(), partial_dev, 1, ncclFloat64, Category::Reduce, 1, ms_);
+  cs_after_ms();
+  if (epochs_done_ - epochs_read_ >= static_cast<int>(losses_dev_.count)) flush_losses();
+  CG_CUDA(cudaMemcpyAsync(losses_dev_.get() + (epochs_done_ - epochs_read_), partial_dev,
+                          sizeof(double), cudaMemcpyDeviceToDevice, cs_));
+  ++epochs_done_;
+}
+
+void Trainer::epoch() {
+  CG_CUDA(cudaSetDevice(device_));
+  CG_CUDA(cudaEventRecord(ev_t0_, cs_));
+  for (int l = 1; l < num_layers(); ++l) forward_layer(l);
+  backward_and_step();
+  CG_CUDA(cudaEventRecord(ev_t1_, cs_));
+}
+
+void Trainer::flush_losses() {
+  sync();
+  const int pending = epochs_done_ - epochs_read_;
+  std::vector<double> tot(static_cast<size_t>(pending));
+  if (pending)
+    CG_CUDA(cudaMemcpy(tot.data(), losses_dev_.get(), pending * sizeof(double), cudaMemcpyDeviceToHost));
+  for (double t : tot) losses_host_.push_back(t / static_cast<double>(train_total_));
+  epochs_read_ = epochs_done_;
+}
+
+std::vector<double> Trainer::run_epochs(int epochs) {
+  if (epochs < 0) throw std::invalid_argument("run_epochs: epoch count must be positive");
+  const size_t first = losses_host_.size() + static_cast<size_t>(epochs_done_ - epochs_read_);
+  for (int e = 0; e < epochs; ++e) epoch();
+  flush_losses();
+  if (epochs > 0) CG_CUDA(cudaEventElapsedTime(&last_epoch_ms_, ev_t0_, ev_t1_));
+  return std::vector<double>(losses_host_.begin() + static_cast<std::ptrdiff_t>(first), losses_host_.end());
+}
+
+double Trainer::last_loss() {
+  flush_losses();
+  return losses_host_.empty() ? 0.0 : losses_host_.back();
+}
+
+void Trainer::sync() {
+  CG_CUDA(cudaSetDevice(device_));
+  CG_CUDA(cudaStreamSynchronize(ms_));
+  CG_CUDA(cudaStreamSynchronize(cs_));
+}
+
+namespace {
+void download(const Mat& m, float* out) {
+  if (m.rows == 0 || m.cols == 0) return;
+  CG_CUDA(cudaMemcpy2D(out, m.cols * sizeof(float), m.p, m.ld * sizeof(float), m.cols * sizeof(float),
+                       m.rows, cudaMemcpyDeviceToHost));
+}
+}  // namespace
+
+void Trainer::h_tile(int layer, float* out) const { download(h_.at(static_cast<size_t>(layer)).m, out); }
+void Trainer::g_tile(int idx, float* out) const { download(g_.at(static_cast<size_t>(idx)).m, out); }
+void Trainer::weight(int l, float* out) const { download(W_.at(static_cast<size_t>(l)).m, out); }
+void Trainer::ygrad(int l, float* out) const { download(Y_.at(static_cast<size_t>(l)).m, out); }
+
+}  // namespace cagnet

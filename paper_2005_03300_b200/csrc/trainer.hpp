@@ -1,0 +1,187 @@
+// Device-resident GraphDataset and the per-rank Trainer of the four CAGNET
+// partitioning strategies (dist.hpp:59-131, dist_impl.hpp, dist_{1d,15d,2d,3d}.cpp).
+//
+// One Trainer object is one rank: it owns its GPU tiles, its NCCL
+// communicators and two streams (compute `cs`, communication `ms`).  Stage
+// loops double-buffer their broadcast panels so that the NCCL broadcast of
+// stage q+1 runs on `ms` while the SpMM of stage q runs on `cs`.
+#pragma once
+
+#include <nccl.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "comm.hpp"
+#include "graph.cuh"
+#include "grid.hpp"
+#include "kernels.cuh"
+
+namespace cagnet {
+
+// dataset.hpp:31-45 with device-resident arrays.
+struct DeviceDataset {
+  int device = 0;
+  int64_t n = 0, f = 0, num_classes = 0, train_count = 0;
+  DeviceCsr adj, adj_t;
+  DevBuf<float> features;  // n x f, ld = ldf
+  int64_t ldf = 0;
+  DevBuf<int32_t> labels;
+  DevBuf<uint8_t> mask;
+};
+
+// generate_dataset (dataset.cpp:110-118) on the current device.
+std::unique_ptr<DeviceDataset> dataset_generate(int64_t n, double degree, int64_t f,
+                                                int64_t classes, uint64_t sg, uint64_t sf,
+                                                uint64_t sl, int generator);
+// make_dataset (dataset.cpp:76-90) from host arrays.
+std::unique_ptr<DeviceDataset> dataset_make(int64_t n, const int64_t* raw_rp,
+                                            const int64_t* raw_ci, const double* features,
+                                            int64_t f, const int64_t* labels,
+                                            const uint8_t* mask, int64_t classes);
+
+struct Mat {
+  float* p = nullptr;
+  int64_t rows = 0, cols = 0, ld = 0;
+};
+
+struct OwnedMat {
+  DevBuf<float> buf;
+  Mat m;
+  // Zero-initialised rows x cols with ld = padded_ld(cols) unless given;
+  // extra_rows adds zeroed padding rows (for equal-count NCCL slices).
+  void alloc(int64_t rows, int64_t cols, int64_t ld = -1, int64_t capacity_rows = -1);
+};
+
+class Trainer {
+ public:
+  Trainer(const DeviceDataset& data, std::vector<int64_t> dims, const double* weights,
+          double lr, Strategy strat, int rank, const ncclUniqueId* id);
+  virtual ~Trainer();
+
+  const ProcessGrid& grid() const { return grid_; }
+  const Strategy& strategy() const { return strat_; }
+  int rank() const { return rank_; }
+  int device() const { return device_; }
+  int num_layers() const { return static_cast<int>(dims_.size()); }
+  const std::vector<int64_t>& dims() const { return dims_; }
+
+  virtual void distribute() = 0;
+  virtual void forward_layer(int l) = 0;  // 1-based, consumes h[l-1]
+  // Loss (into the device loss slot), gradients and the SGD update.
+  virtual void backward_and_step() = 0;
+  virtual BlockRange tile_rows(int rank) const = 0;
+  virtual BlockRange tile_cols(int rank, int64_t width) const = 0;
+  virtual int tile_owner(int rank) const { return rank; }
+
+  // dist_common.cpp:97-100.  Losses stay on the device until read.
+  void epoch();
+  std::vector<double> run_epochs(int epochs);
+  double last_loss();
+  void flush_losses();
+  const std::vector<double>& all_losses() {
+    flush_losses();
+    return losses_host_;
+  }
+  void sync();
+
+  // Readback helpers (host fp32, dense ld = cols).
+  void h_tile(int layer, float* out) const;
+  void g_tile(int idx, float* out) const;
+  void weight(int l, float* out) const;
+  void ygrad(int l, float* out) const;
+  int num_parts() const { return static_cast<int>(a_parts_.size()); }
+  const DeviceCsr& part(int which, int idx) const {
+    return which == 0 ? a_parts_.at(static_cast<size_t>(idx)) : at_parts_.at(static_cast<size_t>(idx));
+  }
+  const Comm& comm() const { return *comm_; }
+  cudaStream_t stream() const { return cs_; }
+  float last_epoch_ms() const { return last_epoch_ms_; }
+
+  // --- per-launch CUDA-event profile (bench roofline) ---
+  struct ProfEntry {
+    std::string name;
+    int64_t launches = 0;
+    double ms = 0, bytes = 0, flops = 0;
+  };
+  void set_timing(bool on) { timing_ = on; }
+  void reset_profile() {
+    collect_profile();
+    profile_.clear();
+  }
+  const std::vector<ProfEntry>& profile() {
+    collect_profile();
+    return profile_;
+  }
+  // One epoch from host buffers: H2D of this rank's feature tile (rows x
+  // cols, dense) and label rows, the epoch, D2H of the loss.
+  double step_host(const float* x_tile, const int32_t* labels_tile);
+
+ protected:
+  // --- helpers shared by the strategies ---
+  void init_tiles();  // h/z/g tile shapes from tile_rows/tile_cols, labels, H0
+  void ms_after_cs();
+  void cs_after_ms();
+  void spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc);
+  void spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32_t* ci, const float* v,
+                const Mat& h, Mat out, bool acc);
+  // C (+)= A · W[r0:r0+k, c0:c0+n]
+  void gemm_aw(const Mat& a, int l, int64_t r0, int64_t c0, Mat c, bool acc, int epi,
+               Mat aux_out);
+  // C (+)= H^T · S
+  void gemm_hts(const Mat& h, const Mat& s, Mat c, bool acc);
+  // C (+)= S · W[r0:r0+n, c0:c0+k]^T, optional relu' epilogue with aux
+  void gemm_swt(const Mat& s, int l, int64_t r0, int64_t c0, Mat c, bool acc, int epi,
+                const Mat* aux);
+  void run_gemm(const kern::GemmDesc& d, const char* kind);
+  void bcast_mat(const Group& g, int root, Mat m, Category cat);
+  void sgd_all();
+  void loss_all_reduce(double* partial_dev);
+  uint64_t words(const Mat& m) const { return static_cast<uint64_t>(m.rows * m.cols); }
+  // Brackets one kernel launch on cs_ with events when timing is on.
+  int prof_begin();
+  void prof_end(int slot, const char* kind, int64_t f, double bytes, double flops);
+  void collect_profile();
+
+  struct ProfRec {
+    cudaEvent_t a = nullptr, b = nullptr;
+    std::string name;
+    double bytes = 0, flops = 0;
+  };
+  bool timing_ = false;
+  std::vector<ProfRec> recs_;
+  size_t recs_used_ = 0;
+  std::vector<ProfEntry> profile_;
+
+  const DeviceDataset& data_;
+  std::vector<int64_t> dims_;
+  double lr_;
+  Strategy strat_;
+  ProcessGrid grid_;
+  int rank_;
+  int64_t train_total_;
+  int device_;
+  std::unique_ptr<Comm> comm_;
+  cudaStream_t cs_ = nullptr, ms_ = nullptr;
+  cudaEvent_t ev_cs_ = nullptr, ev_ms_ = nullptr, ev_t0_ = nullptr, ev_t1_ = nullptr;
+  cudaEvent_t ev_ready_[2] = {nullptr, nullptr}, ev_free_[2] = {nullptr, nullptr};
+
+  std::vector<OwnedMat> W_, Y_;  // replicated, dims[l] x dims[l+1], ld = cols
+  std::vector<OwnedMat> h_, z_, g_;
+  DevBuf<int32_t> labels_;
+  DevBuf<uint8_t> mask_;
+  std::vector<DeviceCsr> a_parts_, at_parts_;
+  DevBuf<double> loss_partial_;
+  DevBuf<double> losses_dev_;
+  int epochs_done_ = 0;
+  int epochs_read_ = 0;
+  std::vector<double> losses_host_;
+  float last_epoch_ms_ = 0.f;
+};
+
+std::unique_ptr<Trainer> make_trainer(const DeviceDataset& data, std::vector<int64_t> dims,
+                                      const double* weights, double lr, Strategy strat,
+                                      int rank, const ncclUniqueId* id);
+
+}  // namespace cagnet

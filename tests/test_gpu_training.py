@@ -1,0 +1,163 @@
+"""End-to-end GCN training on the GPU against the serial fp64 oracle — the
+verify_against_serial recipe (harness.cpp:118-166) at the north star's fp32
+tolerance: h_final, every y_l, g_l, w_l within 1e-4 relative Frobenius and
+the loss |Δ|/max(1,|loss|) <= 1e-4 per epoch (test_dist_strategies.cpp:63-66)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = 1e-4
+
+
+@pytest.fixture(autouse=True)
+def _gpu(need_gpus):
+    need_gpus(1)
+
+
+def max_rel_error(out, ref_losses, ref_h, ref_y, ref_g, ref_w):
+    import oracle
+    worst = oracle.rel_frobenius(out["h_final"], ref_h)
+    for l in range(len(ref_y)):
+        worst = max(worst, oracle.rel_frobenius(out["y"][l], ref_y[l]))
+        worst = max(worst, oracle.rel_frobenius(out["g"][l], ref_g[l]))
+        worst = max(worst, oracle.rel_frobenius(out["w"][l], ref_w[l]))
+    for a, b in zip(out["losses"], ref_losses):
+        worst = max(worst, abs(a - b) / max(1.0, abs(b)))
+    return worst
+
+
+def run_single(cg, data, model, strat, epochs):
+    t = cg.make_trainer(data, model, strat)
+    t.distribute()
+    losses = t.run_epochs(epochs)
+    L = len(model.layer_dims)
+    return dict(losses=losses, h_final=t.h_tile(L - 1).astype(np.float64),
+                y=[t.y(l).astype(np.float64) for l in range(L - 1)],
+                g=[t.g_tile(l).astype(np.float64) for l in range(L - 1)],
+                w=[t.weight(l).astype(np.float64) for l in range(L - 1)], trainer=t)
+
+
+@pytest.mark.parametrize("strat", [("1d", 1, 1, 0), ("1.5d", 1, 1, 0), ("2d", 1, 1, 0),
+                                   ("2d", 1, 1, 3), ("3d", 1, 1, 0)])
+def test_single_rank_matches_serial(cg, orc, strat):
+    dims = [12, 10, 7, 5]
+    data = cg.generate_dataset(64, 8.0, dims[0], dims[-1], 7, 8, 9)
+    model = cg.init_glorot(dims, 3, 0.25)
+    od = orc.generate_dataset(64, 8.0, dims[0], dims[-1], 7, 8, 9)
+    losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.25, 3)
+    out = run_single(cg, data, model, cg.Strategy(*strat), 3)
+    err = max_rel_error(out, losses, h, y, g, w)
+    assert err < TOL, err
+    led = out["trainer"].ledger()
+    assert all(v == 0 for c in led.values() for v in c.values())  # P = 1 meters nothing
+
+
+def test_pinned_loss_trace_fp32(cg):
+    expected = [1.4676915537761182, 1.3547714828994135, 1.3527671034478277,
+                1.3514914086563463, 1.3507757616337233]
+    data = cg.generate_dataset(32, 8.0, 16, 4, 1, 2, 3)
+    assert data.nnz == 281
+    model = cg.init_glorot([16, 16, 4], 4, 0.5)
+    t = cg.make_trainer(data, model, cg.Strategy("1d", 1))
+    t.distribute()
+    losses = t.run_epochs(5)
+    for a, b in zip(losses, expected):
+        assert abs(a - b) / max(1.0, abs(b)) < TOL
+    assert losses[-1] < losses[0]
+
+
+def test_config1_matches_serial(cg, orc):
+    """BASELINE configs[0]: ER n=4096 d=16, dims {128,16,8}, 1D P=1."""
+    dims = [128, 16, 8]
+    data = cg.generate_dataset(4096, 16.0, 128, 8, 1, 2, 3)
+    model = cg.init_glorot(dims, 4, 0.5)
+    od = orc.generate_dataset(4096, 16.0, 128, 8, 1, 2, 3)
+    losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.5, 3)
+    out = run_single(cg, data, model, cg.Strategy("1d", 1), 3)
+    assert max_rel_error(out, losses, h, y, g, w) < TOL
+    c = np.load(os.path.join(GOLD, "reference_config1.npz"))
+    assert np.allclose(out["losses"][:2], c["serial_losses"], rtol=TOL, atol=0)
+
+
+def test_forward_layer_alone(cg, orc):
+    dims = [9, 6, 4]
+    data = cg.generate_dataset(50, 5.0, 9, 4, 1, 2, 3)
+    model = cg.init_glorot(dims, 5, 0.5)
+    t = cg.make_trainer(data, model, cg.Strategy("1d", 1))
+    t.distribute()
+    t.forward_layer(1)
+    od = orc.generate_dataset(50, 5.0, 9, 4, 1, 2, 3)
+    z = orc.gemm(orc.spmm(od["adj_t"], od["features"]), model.weights[0])
+    import oracle
+    assert oracle.rel_frobenius(t.h_tile(1), np.maximum(z, 0)) < 1e-5
+    with pytest.raises(cg.InvalidArgument):
+        t.forward_layer(3)
+
+
+def test_trainer_rejects_bad_models(cg):
+    data = cg.generate_dataset(10, 3.0, 8, 4, 1, 2, 3)
+    with pytest.raises(cg.InvalidArgument):
+        cg.make_trainer(data, cg.init_glorot([7, 6, 4], 4), cg.Strategy("1d", 1))
+    with pytest.raises(cg.InvalidArgument):
+        cg.make_trainer(data, cg.init_glorot([8, 6, 5], 4), cg.Strategy("1d", 1))
+    with pytest.raises(cg.InvalidArgument):
+        cg.make_trainer(data, cg.init_glorot([8, 6, 4], 4), cg.Strategy("2d", 2))
+
+
+def test_make_dataset_from_host_arrays(cg, orc):
+    raw = orc.er_generate(80, 6.0, 2)
+    x = orc.random_features(80, 5, 3)
+    y = orc.random_labels(80, 3, 4)
+    mask = (np.arange(80) % 3 != 0).astype(np.uint8)
+    data = cg.make_dataset(raw.row_ptr, raw.col_idx, x, y, 3, train_mask=mask)
+    assert data.train_count() == int(mask.sum())
+    model = cg.init_glorot([5, 4, 3], 9, 0.5)
+    adj = orc.normalize(raw)
+    od = dict(n=80, adj=adj, adj_t=orc.transpose(adj), features=x, labels=y, mask=mask)
+    losses, h, yy, g, w = orc.train_serial(od, [5, 4, 3], model.weights, 0.5, 2)
+    out = run_single(cg, data, model, cg.Strategy("1d", 1), 2)
+    assert max_rel_error(out, losses, h, yy, g, w) < TOL
+
+
+# ---- multi-GPU: every strategy vs the reference's own distributed outcome -----
+DIST = {  # name -> (kind, P, repl, block, n, dims)   (tests/golden/make_golden.py)
+    "1d_p2": ("1d", 2, 1, 0, 20, [8, 6, 4]),
+    "1d_p3": ("1d", 3, 1, 0, 20, [8, 6, 4]),
+    "15d_p4_c2": ("1.5d", 4, 2, 0, 20, [8, 6, 4]),
+    "15d_p6_c2": ("1.5d", 6, 2, 0, 20, [8, 6, 4]),
+    "2d_p4": ("2d", 4, 1, 0, 18, [8, 6, 4]),
+    "2d_p4_b3": ("2d", 4, 1, 3, 18, [8, 6, 4]),
+    "1d_p8": ("1d", 8, 1, 0, 20, [8, 6, 4]),
+    "15d_p8_c2": ("1.5d", 8, 2, 0, 20, [8, 6, 4]),
+    "3d_p8": ("3d", 8, 1, 0, 9, [8, 8, 4]),
+}
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("name", list(DIST))
+def test_distributed_matches_reference(cg, need_gpus, name):
+    kind, P, repl, block, n, dims = DIST[name]
+    need_gpus(P)
+    gd = np.load(os.path.join(GOLD, "reference_dist.npz"))
+    model = cg.init_glorot(dims, 14, 0.5)
+    strat = cg.Strategy(kind, P, repl, block)
+    out = cg.run_distributed(lambda dev: cg.generate_dataset(n, 4.0, dims[0], dims[-1], 11, 12, 13,
+                                                             device=dev), model, strat, 3)
+    L = len(dims)
+    res = dict(losses=out.losses, h_final=out.h_final, y=out.y_final, g=out.g_final,
+               w=out.model.weights)
+    err = max_rel_error(res, gd[f"{name}_losses"], gd[f"{name}_h_final"],
+                        [gd[f"{name}_y_{l}"] for l in range(L - 1)],
+                        [gd[f"{name}_g_{l}"] for l in range(L - 1)],
+                        [gd[f"{name}_w_{l}"] for l in range(L - 1)])
+    assert err < TOL, err
+    # Ledger reconciliation: the NCCL path meters the reference's counters exactly.
+    want = gd[f"{name}_ledger"]  # [category, rank, field]
+    for r in range(P):
+        for ci, cat in enumerate(cg.CATEGORIES):
+            got = [out.ledger[r][cat][f] for f in ("messages", "words_sent", "words_received",
+                                                   "payload_words", "calls")]
+            assert got == [int(x) for x in want[ci, r]], (name, r, cat)
