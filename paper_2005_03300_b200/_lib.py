@@ -108,7 +108,23 @@ SIGNATURES = {
 _RESTYPES = {"cagnet_last_error": C.c_char_p, "cagnet_version": i32}
 
 
+def _preload_nccl() -> None:
+    """Bind libnccl.so.2 to the NCCL that PyTorch ships (2.28) before our
+    library pulls in the older system copy, so both share one NCCL."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for base in (spec.submodule_search_locations or []) if spec else []:
+            path = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(path):
+                C.CDLL(path, mode=C.RTLD_GLOBAL)
+                return
+    except Exception:
+        pass
+
+
 def _load() -> C.CDLL:
+    _preload_nccl()
     if not os.path.exists(LIB_PATH):
         raise ImportError(
             f"{LIB_PATH} is missing: build the CUDA extension first "

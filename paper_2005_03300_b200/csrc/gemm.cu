@@ -89,43 +89,54 @@ struct Stager {
     }
   }
 
-  // Byte offset of item i inside the R x BK stage buffer.
+  // Splits item i into hi/lo tf32 and stores it into the K-major
+  // SWIZZLE_NONE stage layout: element (row, k) of a 32-wide k-block lives at
+  // (row/8)*1024 + (k/4)*128 + (row%8)*16 + (k%4)*4 bytes (core matrices of
+  // 8 rows x 16 B; K-direction stride 128 B, 8-row-group stride 1 KB).
   template <int R>
-  __device__ static uint32_t offset(int i, int tid) {
+  __device__ static void store(char* hi, char* lo, int i, int tid, const float4& v) {
     const int c = i * kThreads + tid;
     if constexpr (MODE == 1) {
+      // v holds rows 4q..4q+3 of one k; scatter them as scalars.  The store
+      // order is rotated per lane so each warp-wide store hits 32 banks.
       const int k_lo = c & 7, q_lo = (c >> 3) & 3, k_hi = (c >> 5) & 3, q_hi = c >> 7;
-      return static_cast<uint32_t>((q_hi * 4 + q_lo) * 128 + k_hi * (R * 32) + k_lo * 16);
+      const int k = k_hi * 8 + k_lo;
+      const int q = q_hi * 4 + q_lo;
+      const int rot = ((k_lo >> 2) + 2 * (q_lo >> 1)) & 3;
+      const uint32_t kpart = static_cast<uint32_t>((k >> 2) * 128 + (k & 3) * 4);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int e = (j + rot) & 3;
+        const float x = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+        const int row = 4 * q + e;
+        const uint32_t off = static_cast<uint32_t>((row >> 3) * 1024 + (row & 7) * 16) + kpart;
+        const float h = tc::to_tf32(x);
+        *reinterpret_cast<float*>(hi + off) = h;
+        *reinterpret_cast<float*>(lo + off) = tc::to_tf32(x - h);
+      }
     } else {
       const int r_lo = c & 7, kq = (c >> 3) & 7, r_hi = c >> 6;
-      return static_cast<uint32_t>(r_hi * 1024 + kq * 128 + r_lo * 16);
+      const uint32_t off = static_cast<uint32_t>(r_hi * 1024 + kq * 128 + r_lo * 16);
+      float4 h, l;
+      h.x = tc::to_tf32(v.x);
+      h.y = tc::to_tf32(v.y);
+      h.z = tc::to_tf32(v.z);
+      h.w = tc::to_tf32(v.w);
+      l.x = tc::to_tf32(v.x - h.x);
+      l.y = tc::to_tf32(v.y - h.y);
+      l.z = tc::to_tf32(v.z - h.z);
+      l.w = tc::to_tf32(v.w - h.w);
+      *reinterpret_cast<float4*>(hi + off) = h;
+      *reinterpret_cast<float4*>(lo + off) = l;
     }
   }
 
-  // Descriptor for the k-step kk (8 tf32 elements) of an R-row stage buffer.
-  template <int R>
+  // Descriptor of k-step kk (8 tf32 = two 16 B core-matrix columns).
   __device__ static uint64_t desc(uint32_t base, int kk) {
-    if constexpr (MODE == 1)
-      return tc::smem_desc(base + kk * (R * 32), /*lbo=*/R * 32, /*sbo=*/128);
-    else
-      return tc::smem_desc(base + kk * 256, /*lbo=*/128, /*sbo=*/1024);
+    return tc::smem_desc(base + kk * 256, /*lbo=*/128, /*sbo=*/1024);
   }
 };
 
-__device__ __forceinline__ void split_store(char* hi_base, char* lo_base, uint32_t off,
-                                            const float4& v) {
-  float4 h, l;
-  h.x = tc::to_tf32(v.x);
-  h.y = tc::to_tf32(v.y);
-  h.z = tc::to_tf32(v.z);
-  h.w = tc::to_tf32(v.w);
-  l.x = tc::to_tf32(v.x - h.x);
-  l.y = tc::to_tf32(v.y - h.y);
-  l.z = tc::to_tf32(v.z - h.z);
-  l.w = tc::to_tf32(v.w - h.w);
-  *reinterpret_cast<float4*>(hi_base + off) = h;
-  *reinterpret_cast<float4*>(lo_base + off) = l;
-}
 
 __device__ __forceinline__ float apply_epilogue(const Params& p, int64_t r, int64_t c, float v) {
   if (p.accumulate) v += p.C[r * p.ldc + c];
@@ -145,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const Params p
   constexpr uint32_t B_BYTES = BN * BK * 4;
   constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
-  constexpr uint32_t IDESC = tc::idesc_tf32(BM, BN, AMODE == 1, BMODE == 1);
+  constexpr uint32_t IDESC = tc::idesc_tf32(BM, BN, 0, 0);  // both operands K-major in smem
 
   extern __shared__ __align__(1024) char smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 2 * STAGE_BYTES);
@@ -188,11 +199,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const Params p
     if (kb >= 2) tc::mbar_wait(&mbar[s], static_cast<uint32_t>(((kb >> 1) - 1) & 1));
 #pragma unroll
     for (int i = 0; i < A_ITEMS; ++i)
-      split_store(st, st + A_BYTES, Stager<AMODE>::template offset<BM>(i, tid), ra[i]);
+      Stager<AMODE>::template store<BM>(st, st + A_BYTES, i, tid, ra[i]);
 #pragma unroll
     for (int i = 0; i < B_ITEMS; ++i)
-      split_store(st + 2 * A_BYTES, st + 2 * A_BYTES + B_BYTES,
-                  Stager<BMODE>::template offset<BN>(i, tid), rb[i]);
+      Stager<BMODE>::template store<BN>(st + 2 * A_BYTES, st + 2 * A_BYTES + B_BYTES, i, tid, rb[i]);
     tc::fence_proxy_async_smem();
     __syncthreads();
     if (kb + 1 < nkb) load_stage(kb + 1);
@@ -202,10 +212,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const Params p
       const uint32_t b_hi = a_hi + 2 * A_BYTES, b_lo = b_hi + B_BYTES;
 #pragma unroll
       for (int kk = 0; kk < BK / 8; ++kk) {
-        const uint64_t ah = Stager<AMODE>::template desc<BM>(a_hi, kk);
-        const uint64_t al = Stager<AMODE>::template desc<BM>(a_lo, kk);
-        const uint64_t bh = Stager<BMODE>::template desc<BN>(b_hi, kk);
-        const uint64_t bl = Stager<BMODE>::template desc<BN>(b_lo, kk);
+        const uint64_t ah = Stager<AMODE>::desc(a_hi, kk);
+        const uint64_t al = Stager<AMODE>::desc(a_lo, kk);
+        const uint64_t bh = Stager<BMODE>::desc(b_hi, kk);
+        const uint64_t bl = Stager<BMODE>::desc(b_lo, kk);
         tc::mma_tf32(tmem, ah, bh, IDESC, (kb | kk) != 0);
         tc::mma_tf32(tmem, ah, bl, IDESC, 1);
         tc::mma_tf32(tmem, al, bh, IDESC, 1);
