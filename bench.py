@@ -56,6 +56,11 @@ def parse():
     p.add_argument("--strategy", default="1d", choices=["1d", "1.5d", "2d", "3d"])
     p.add_argument("--repl", type=int, default=0, help="1.5D replication (default 2 when 1.5d)")
     p.add_argument("--block", type=int, default=0)
+    p.add_argument("--reference-order", action="store_true",
+                   help="propagate as the reference does, (A^T H) W, instead of the default "
+                        "narrow-first A^T (H W) on 1D/1.5D (same product)")
+    p.add_argument("--no-alt", action="store_true",
+                   help="skip timing the other propagation order")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--sample-div", type=int, default=16,
@@ -223,7 +228,8 @@ def run_ours(args, cfg):
         pg = dist
     kind = args.strategy
     repl = args.repl or (2 if kind == "1.5d" else 1)
-    strat = cg.Strategy(kind, N, repl, args.block)
+    strat = cg.Strategy(kind, N, repl, args.block,
+                        reassociate=not args.reference_order and kind in ("1d", "1.5d"))
 
     # NCCL bootstrap for the library's own communicators.
     nid = None
@@ -275,6 +281,27 @@ def run_ours(args, cfg):
     if pg:
         pg.all_reduce(ms_t, op=pg.ReduceOp.MAX)
     ms_step = float(ms_t.item()) / args.steps
+
+    # ---- the other propagation order, same trainer, same timing rules --------
+    alt = None
+    if kind in ("1d", "1.5d") and not args.no_alt:
+        lib_set = cg.lib.cagnet_trainer_set_option
+        cg.check(lib_set(trainer.h, b"reassociate", int(not strat.reassociate)))
+        trainer.run_epochs(1)
+        barrier()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record(stream)
+        for _ in range(args.steps):
+            trainer.epoch_async()
+        e2.record(stream)
+        barrier()
+        alt_t = torch.tensor([s2.elapsed_time(e2)], dtype=torch.float64, device="cuda")
+        if pg:
+            pg.all_reduce(alt_t, op=pg.ReduceOp.MAX)
+        alt = {"propagation": "reference order (A^T H) W" if strat.reassociate
+               else "narrow-first A^T (H W)",
+               "ms_per_step": round(float(alt_t.item()) / args.steps, 4)}
+        cg.check(lib_set(trainer.h, b"reassociate", int(strat.reassociate)))
 
     # ---- end-to-end: the public host-buffer call, H2D + epoch + D2H ----------
     r0, r1, c0, c1, _ = trainer.tile(rank, cfg["dims"][0])
@@ -338,7 +365,10 @@ def run_ours(args, cfg):
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
         "config": {"workload": cfg["label"], "strategy": kind, "ranks": N, "repl": repl,
-                   "block": args.block, "generator": cfg["generator"],
+                   "block": args.block,
+                   "propagation": "narrow-first A^T (H W)" if strat.reassociate
+                   else "reference order (A^T H) W",
+                   "generator": cfg["generator"],
                    "l2": "inputs larger than L2 (CSR A+A^T and H0 > 126 MB)"},
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": 8},
@@ -349,6 +379,7 @@ def run_ours(args, cfg):
         "kernels": {k: {"launches": v["launches"], "ms_per_launch": round(v["ms"] / v["launches"], 4),
                         "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] else None}
                     for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
+        "other_propagation": alt,
         "loss_last": float(losses[-1]) if len(losses) else None,
         "setup_s": {"dataset_gen": round(gen_s, 2)},
     }

@@ -224,6 +224,10 @@ CAGNET_API int cagnet_trainer_stats(cagnet_trainer_t t, double* ms8, uint64_t* w
 CAGNET_API int cagnet_trainer_ledger(cagnet_trainer_t t, uint64_t* out20);
 /* Enable/disable per-category CUDA-event timing (adds event records; default off). */
 CAGNET_API int cagnet_trainer_set_timing(cagnet_trainer_t t, int on);
+/* Trainer options: "reassociate" (1 = narrow-first propagation Aᵀ(H W) when
+ * f_out < f_in, block-row strategies; same product, f_out-wide panels),
+ * "timing" (per-launch CUDA-event profile). */
+CAGNET_API int cagnet_trainer_set_option(cagnet_trainer_t t, const char* name, int64_t value);
 /* Per-launch CUDA-event profile, aggregated by kernel name (e.g. "spmm_f602"):
  * out4 = {launches, total_ms, algorithmic_bytes, flops} (SURVEY §8(d) byte model). */
 CAGNET_API int cagnet_trainer_profile_count(cagnet_trainer_t t, int* n);

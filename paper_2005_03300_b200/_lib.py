@@ -98,6 +98,7 @@ SIGNATURES = {
     "cagnet_trainer_ledger": [vp, _u64p],
     "cagnet_trainer_set_timing": [vp, i32],
     "cagnet_trainer_stream": [vp, C.POINTER(vp)],
+    "cagnet_trainer_set_option": [vp, C.c_char_p, i64],
     "cagnet_trainer_profile_count": [vp, C.POINTER(i32)],
     "cagnet_trainer_profile_entry": [vp, i32, C.c_char_p, i32, _f64p],
     "cagnet_trainer_profile_reset": [vp],

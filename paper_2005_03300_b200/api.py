@@ -54,6 +54,9 @@ class Strategy:
     ranks: int = 1
     repl: int = 1
     block: int = 0
+    # Extension (not in the reference): narrow-first propagation Aᵀ(H W) for
+    # layers with f_out < f_in on the block-row strategies (1D / 1.5D).
+    reassociate: bool = False
 
     @property
     def kind_id(self) -> int:
@@ -321,6 +324,8 @@ class Trainer:
                                         C.byref(out)))
         self.h = out
         self.dims = [int(d) for d in dims]
+        if strat.reassociate:
+            check(lib.cagnet_trainer_set_option(self.h, b"reassociate", 1))
 
     # lifecycle -------------------------------------------------------------
     def distribute(self):

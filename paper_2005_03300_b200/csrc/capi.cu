@@ -578,6 +578,18 @@ int cagnet_trainer_set_timing(cagnet_trainer_t t, int on) {
   });
 }
 
+int cagnet_trainer_set_option(cagnet_trainer_t t, const char* name, int64_t value) {
+  return guarded([&] {
+    const std::string n(name ? name : "");
+    if (n == "reassociate")
+      t->t->set_reassociate(value != 0);
+    else if (n == "timing")
+      t->t->set_timing(value != 0);
+    else
+      throw std::invalid_argument("trainer option: unknown option '" + n + "'");
+  });
+}
+
 int cagnet_trainer_profile_count(cagnet_trainer_t t, int* n) {
   return guarded([&] { *n = static_cast<int>(t->t->profile().size()); });
 }

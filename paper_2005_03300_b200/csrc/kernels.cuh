@@ -17,6 +17,14 @@ namespace kern {
 void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
               const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
               cudaStream_t stream);
+// Same, with row i's nonzeros given as [seg_begin[i], seg_end[i]).
+void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_end,
+                   const int32_t* col_idx, const float* vals, const float* H, int64_t ldh, int f,
+                   float* T, int64_t ldt, bool accumulate, cudaStream_t stream);
+// split[b * rows + r] (b = 0..nb) = first nonzero of row r in column block b
+// of the ceiling-rule split of n_cols into nb blocks; split[nb * rows + r] = row end.
+void column_splits(int64_t rows, int64_t n_cols, int nb, const int64_t* row_ptr,
+                   const int32_t* col_idx, int64_t* split, cudaStream_t stream);
 
 // ---- K2: tcgen05 split-TF32 GEMM (dense.cpp:37-70) ---------------------------
 // op(A) m x k: element (i, p) at A[i * a_sm + p * a_sk]

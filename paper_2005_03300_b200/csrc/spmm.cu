@@ -11,6 +11,12 @@
 // the group with warp shuffles; every gathered H row is read as LPR*16 B
 // contiguous segments.  Rows of an Erdős–Rényi graph have near-uniform length
 // (binomial degree), so row-group mapping balances without merge-path.
+//
+// Rows are given as [seg_begin[i], seg_end[i]) ranges, so a column block of
+// a CSR matrix (a contiguous sub-range of every sorted row) is processed
+// without copying: the L2-aware blocking in spmm_blocked() runs one pass per
+// column block whose H panel fits in L2 and accumulates the passes in
+// ascending column order — the reference's own order (csr.hpp:68-70).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -53,9 +59,6 @@ __device__ __forceinline__ float4 load_vec(const float* __restrict__ row, int ve
   if (c + 2 < f) r.z = __ldg(row + c + 2);
   return r;
 }
-__device__ __forceinline__ float load_vec1(const float* __restrict__ row, int vec) {
-  return __ldg(row + vec);
-}
 
 __device__ __forceinline__ void store_vec(float* row, int vec, int f, const float4& v) {
   const int c = vec * 4;
@@ -68,13 +71,22 @@ __device__ __forceinline__ void store_vec(float* row, int vec, int f, const floa
   if (c + 2 < f) row[c + 2] = v.z;
 }
 
+struct SpmmArgs {
+  int64_t n_rows;
+  const int64_t* seg_begin;
+  const int64_t* seg_end;
+  const int32_t* col_idx;
+  const float* vals;
+  const float* H;
+  int64_t ldh;
+  int f;
+  float* T;
+  int64_t ldt;
+};
+
 // VEC = 4: 16-byte vectors (requires 16 B aligned rows); VEC = 1: scalars.
 template <int VEC, int LPR, int VPL, bool ACC>
-__global__ void __launch_bounds__(kThreads)
-    spmm_rows_kernel(int64_t n_rows, const int64_t* __restrict__ row_ptr,
-                     const int32_t* __restrict__ col_idx, const float* __restrict__ vals,
-                     const float* __restrict__ H, int64_t ldh, int f, float* __restrict__ T,
-                     int64_t ldt) {
+__global__ void __launch_bounds__(kThreads) spmm_rows_kernel(const SpmmArgs a) {
   using V = typename VecT<VEC>::T;
   constexpr int RPW = 32 / LPR;  // rows per warp
   const int lane = threadIdx.x & 31;
@@ -82,12 +94,16 @@ __global__ void __launch_bounds__(kThreads)
   const int grp = lane / LPR;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5;
   const int64_t row = warp * RPW + grp;
+  const int f = a.f;
   const int nvec = (f + VEC - 1) / VEC;
+  const int32_t* __restrict__ col_idx = a.col_idx;
+  const float* __restrict__ vals = a.vals;
+  const float* __restrict__ H = a.H;
 
   int64_t beg = 0, len = 0;
-  if (row < n_rows) {
-    beg = row_ptr[row];
-    len = row_ptr[row + 1] - beg;
+  if (row < a.n_rows) {
+    beg = a.seg_begin[row];
+    len = a.seg_end[row] - beg;
   }
   // Uniform trip count across the warp so every lane joins the shuffles.
   int64_t maxlen = len;
@@ -97,16 +113,17 @@ __global__ void __launch_bounds__(kThreads)
     maxlen = other > maxlen ? other : maxlen;
   }
 
+  float* trow = a.T + row * a.ldt;
   V acc[VPL];
 #pragma unroll
   for (int i = 0; i < VPL; ++i) {
     zero_vec(acc[i]);
     const int vec = sub + i * LPR;
-    if (ACC && row < n_rows && vec < nvec) {
+    if (ACC && row < a.n_rows && vec < nvec) {
       if constexpr (VEC == 4)
-        acc[i] = load_vec(T + row * ldt, vec, f);
+        acc[i] = load_vec(trow, vec, f);
       else
-        acc[i] = T[row * ldt + vec];
+        acc[i] = trow[vec];
     }
   }
 
@@ -124,7 +141,7 @@ __global__ void __launch_bounds__(kThreads)
       const int cc = __shfl_sync(0xffffffffu, c, src0 + t);
       const float vv = __shfl_sync(0xffffffffu, v, src0 + t);
       if (t < remain) {
-        const float* hrow = H + static_cast<int64_t>(cc) * ldh;
+        const float* hrow = H + static_cast<int64_t>(cc) * a.ldh;
         V hv[VPL];
 #pragma unroll
         for (int i = 0; i < VPL; ++i) {
@@ -134,7 +151,7 @@ __global__ void __launch_bounds__(kThreads)
             if constexpr (VEC == 4)
               hv[i] = load_vec(hrow, vec, f);
             else
-              hv[i] = load_vec1(hrow, vec);
+              hv[i] = __ldg(hrow + vec);
           }
         }
 #pragma unroll
@@ -143,48 +160,42 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
 
-  if (row < n_rows) {
+  if (row < a.n_rows) {
 #pragma unroll
     for (int i = 0; i < VPL; ++i) {
       const int vec = sub + i * LPR;
       if (vec < nvec) {
         if constexpr (VEC == 4)
-          store_vec(T + row * ldt, vec, f, acc[i]);
+          store_vec(trow, vec, f, acc[i]);
         else
-          T[row * ldt + vec] = acc[i];
+          trow[vec] = acc[i];
       }
     }
   }
 }
 
 template <int VEC, int LPR, int VPL>
-void launch_one(int64_t n_rows, const int64_t* rp, const int32_t* ci, const float* v,
-                const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool acc,
-                cudaStream_t s) {
+void launch_one(const SpmmArgs& a, bool acc, cudaStream_t s) {
   constexpr int rows_per_block = (kThreads / 32) * (32 / LPR);
-  const int64_t blocks = ceil_div64(n_rows, rows_per_block);
+  const int64_t blocks = ceil_div64(a.n_rows, rows_per_block);
   if (acc)
-    spmm_rows_kernel<VEC, LPR, VPL, true>
-        <<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(n_rows, rp, ci, v, H, ldh, f, T, ldt);
+    spmm_rows_kernel<VEC, LPR, VPL, true><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a);
   else
-    spmm_rows_kernel<VEC, LPR, VPL, false>
-        <<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(n_rows, rp, ci, v, H, ldh, f, T, ldt);
+    spmm_rows_kernel<VEC, LPR, VPL, false><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a);
   CG_LAUNCH_CHECK();
 }
 
 template <int VEC, int LPR>
-void launch_vpl(int vpl, int64_t n_rows, const int64_t* rp, const int32_t* ci, const float* v,
-                const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool acc,
-                cudaStream_t s) {
+void launch_vpl(int vpl, const SpmmArgs& a, bool acc, cudaStream_t s) {
   switch (vpl) {
-    case 1: return launch_one<VEC, LPR, 1>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
-    case 2: return launch_one<VEC, LPR, 2>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
-    case 3: return launch_one<VEC, LPR, 3>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
-    case 4: return launch_one<VEC, LPR, 4>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
-    case 5: return launch_one<VEC, LPR, 5>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
-    case 6: return launch_one<VEC, LPR, 6>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
-    case 7: return launch_one<VEC, LPR, 7>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
-    default: return launch_one<VEC, LPR, 8>(n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    case 1: return launch_one<VEC, LPR, 1>(a, acc, s);
+    case 2: return launch_one<VEC, LPR, 2>(a, acc, s);
+    case 3: return launch_one<VEC, LPR, 3>(a, acc, s);
+    case 4: return launch_one<VEC, LPR, 4>(a, acc, s);
+    case 5: return launch_one<VEC, LPR, 5>(a, acc, s);
+    case 6: return launch_one<VEC, LPR, 6>(a, acc, s);
+    case 7: return launch_one<VEC, LPR, 7>(a, acc, s);
+    default: return launch_one<VEC, LPR, 8>(a, acc, s);
   }
 }
 
@@ -208,25 +219,48 @@ void pick_shape(int nvec, int* lpr, int* vpl) {
 }
 
 template <int VEC>
-void dispatch(int64_t n_rows, const int64_t* rp, const int32_t* ci, const float* v,
-              const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool acc,
-              cudaStream_t s) {
-  const int nvec = (f + VEC - 1) / VEC;
+void dispatch(const SpmmArgs& a, bool acc, cudaStream_t s) {
+  const int nvec = (a.f + VEC - 1) / VEC;
   int lpr, vpl;
   pick_shape(nvec, &lpr, &vpl);
   switch (lpr) {
-    case 4: return launch_vpl<VEC, 4>(vpl, n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
-    case 8: return launch_vpl<VEC, 8>(vpl, n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
-    case 16: return launch_vpl<VEC, 16>(vpl, n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
-    default: return launch_vpl<VEC, 32>(vpl, n_rows, rp, ci, v, H, ldh, f, T, ldt, acc, s);
+    case 4: return launch_vpl<VEC, 4>(vpl, a, acc, s);
+    case 8: return launch_vpl<VEC, 8>(vpl, a, acc, s);
+    case 16: return launch_vpl<VEC, 16>(vpl, a, acc, s);
+    default: return launch_vpl<VEC, 32>(vpl, a, acc, s);
   }
+}
+
+// split[b * rows + r] = first nonzero of row r with column >= b * step.
+__global__ void column_splits_kernel(int64_t rows, int nb, int64_t step,
+                                     const int64_t* __restrict__ row_ptr,
+                                     const int32_t* __restrict__ col_idx,
+                                     int64_t* __restrict__ split) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int64_t b0 = row_ptr[r], e0 = row_ptr[r + 1];
+  int64_t lo = b0;
+  split[r] = b0;
+  for (int b = 1; b < nb; ++b) {
+    const int64_t key = static_cast<int64_t>(b) * step;
+    int64_t hi = e0;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (col_idx[mid] < key)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    split[static_cast<int64_t>(b) * rows + r] = lo;
+  }
+  split[static_cast<int64_t>(nb) * rows + r] = e0;
 }
 
 }  // namespace
 
-void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
-              const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
-              cudaStream_t stream) {
+void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_end,
+                   const int32_t* col_idx, const float* vals, const float* H, int64_t ldh, int f,
+                   float* T, int64_t ldt, bool accumulate, cudaStream_t stream) {
   if (n_rows <= 0 || f <= 0) return;
   const bool aligned = (ldh % 4 == 0) && (ldt % 4 == 0) &&
                        (reinterpret_cast<uintptr_t>(H) % 16 == 0) &&
@@ -234,12 +268,28 @@ void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, co
   // Column chunks of at most 32 lanes * 8 vectors keep accumulators in registers.
   const int chunk = aligned ? 32 * 8 * 4 : 32 * 8;
   for (int c0 = 0; c0 < f; c0 += chunk) {
-    const int fc = f - c0 < chunk ? f - c0 : chunk;
+    SpmmArgs a{n_rows, seg_begin, seg_end, col_idx, vals, H + c0, ldh, f - c0 < chunk ? f - c0 : chunk,
+               T + c0, ldt};
     if (aligned)
-      dispatch<4>(n_rows, row_ptr, col_idx, vals, H + c0, ldh, fc, T + c0, ldt, accumulate, stream);
+      dispatch<4>(a, accumulate, stream);
     else
-      dispatch<1>(n_rows, row_ptr, col_idx, vals, H + c0, ldh, fc, T + c0, ldt, accumulate, stream);
+      dispatch<1>(a, accumulate, stream);
   }
+}
+
+void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
+              const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
+              cudaStream_t stream) {
+  spmm_segments(n_rows, row_ptr, row_ptr + 1, col_idx, vals, H, ldh, f, T, ldt, accumulate, stream);
+}
+
+void column_splits(int64_t rows, int64_t n_cols, int nb, const int64_t* row_ptr,
+                   const int32_t* col_idx, int64_t* split, cudaStream_t stream) {
+  if (rows <= 0) return;
+  const int64_t step = ceil_div64(n_cols > 0 ? n_cols : 1, nb);
+  column_splits_kernel<<<static_cast<unsigned>(ceil_div64(rows, 256)), 256, 0, stream>>>(
+      rows, nb, step, row_ptr, col_idx, split);
+  CG_LAUNCH_CHECK();
 }
 
 }  // namespace kern

@@ -42,11 +42,22 @@ class TrainerRows final : public Trainer {
       throw std::invalid_argument("run_forward_layer: layer " + std::to_string(l) + " outside [1, " +
                                   std::to_string(num_layers()) + ")");
     const int64_t fin = dims_[static_cast<size_t>(l - 1)];
+    const int64_t fout = dims_[static_cast<size_t>(l)];
     const Mat& h = h_[static_cast<size_t>(l - 1)].m;
+    Mat z = z_[static_cast<size_t>(l - 1)].m;
+    if (reassociate_ && fout < fin) {
+      // Narrow-first propagation: Z = Aᵀ (H W) — the same product as
+      // (Aᵀ H) W, but the broadcast panels and the SpMM are f_out wide.
+      Mat u = view(acc_, h.rows, fout);
+      gemm_aw(h, l - 1, 0, 0, u, false, kern::EPI_NONE, Mat{});
+      stages(at_parts_, u, z);
+      if (!one_d()) row_reduce(z);
+      finish_layer(l, z);
+      return;
+    }
     Mat t = view(acc_, h.rows, fin);
     stages(at_parts_, h, t);
     if (!one_d()) row_reduce(t);
-    Mat z = z_[static_cast<size_t>(l - 1)].m;
     if (l + 1 == num_layers()) {
       gemm_aw(t, l - 1, 0, 0, z, false, kern::EPI_NONE, Mat{});
       // log_softmax (dense.cpp:94-107) fused with nll_tile (dense.cpp:109-136).
@@ -121,6 +132,20 @@ class TrainerRows final : public Trainer {
       if (comm) CG_CUDA(cudaEventRecord(ev_free_[b], cs_));
     }
     if (idx == 0) CG_CUDA(cudaMemsetAsync(out.p, 0, out.rows * out.ld * sizeof(float), cs_));
+  }
+
+  // Activation of a finished pre-activation tile: ReLU, or the fused
+  // log_softmax + NLL on the output layer.
+  void finish_layer(int l, const Mat& z) {
+    Mat hl = h_[static_cast<size_t>(l)].m;
+    if (l + 1 == num_layers()) {
+      Mat g = g_[static_cast<size_t>(l - 1)].m;
+      kern::logsoftmax_nll(z.p, z.rows, static_cast<int>(z.cols), z.ld, 0, static_cast<int>(z.cols), hl.p,
+                           hl.ld, g.p, g.ld, labels_.get(), mask_.get(), train_total_,
+                           loss_partial_.get(), cs_);
+    } else {
+      kern::relu(z.p, z.rows, static_cast<int>(z.cols), z.ld, hl.p, hl.ld, cs_);
+    }
   }
 
   void row_reduce(Mat m) {

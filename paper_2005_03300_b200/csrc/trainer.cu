@@ -1,5 +1,8 @@
 // Trainer base: tiles, weights, streams, shared GEMM/SpMM plumbing, and the
 // device GraphDataset constructors.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.cuh"
@@ -237,7 +240,41 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc) {
     throw std::invalid_argument("spmm: sparse is " + std::to_string(a.n_rows) + "x" +
                                 std::to_string(a.n_cols) + " but dense has " +
                                 std::to_string(h.rows) + " rows");
-  spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, acc);
+  // L2-aware column blocking: when the gathered panel H (n_cols x f) does not
+  // fit the L2 budget, run one pass per column block so every pass gathers
+  // from an L2-resident slice (SURVEY §7 hard parts).
+  const double panel = static_cast<double>(a.n_cols) * h.cols * 4.0;
+  const int nb = static_cast<int>(std::min<double>(64.0, std::ceil(panel / l2_panel_bytes())));
+  if (nb <= 1 || a.nnz == 0 || out.rows != a.n_rows || out.cols != h.cols) {
+    spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, acc);
+    return;
+  }
+  auto key = std::make_pair(static_cast<const void*>(a.row_ptr.get()), nb);
+  auto it = splits_.find(key);
+  if (it == splits_.end()) {
+    DevBuf<int64_t> tbl(static_cast<size_t>((nb + 1) * a.n_rows));
+    kern::column_splits(a.n_rows, a.n_cols, nb, a.row_ptr.get(), a.col_idx.get(), tbl.get(), cs_);
+    it = splits_.emplace(key, std::move(tbl)).first;
+  }
+  const int64_t* split = it->second.get();
+  const int slot = prof_begin();
+  for (int b = 0; b < nb; ++b)
+    kern::spmm_segments(a.n_rows, split + b * a.n_rows, split + (b + 1) * a.n_rows, a.col_idx.get(),
+                        a.vals.get(), h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld,
+                        acc || b > 0, cs_);
+  if (slot >= 0) {
+    const double f = static_cast<double>(h.cols), r = static_cast<double>(a.n_rows);
+    const double bytes = 8.0 * (r + 1) + 8.0 * a.nnz + 4.0 * f * h.rows + 4.0 * f * r * (acc ? 2 : 1);
+    prof_end(slot, "spmm", h.cols, bytes, 2.0 * a.nnz * f);
+  }
+}
+
+double Trainer::l2_panel_bytes() {
+  static const double v = [] {
+    const char* e = std::getenv("CAGNET_L2_PANEL_MB");
+    return (e ? std::atof(e) : 96.0) * 1048576.0;
+  }();
+  return v > 0 ? v : 1e30;
 }
 
 void Trainer::spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32_t* ci,
@@ -300,9 +337,13 @@ void Trainer::collect_profile() {
 double Trainer::step_host(const float* x_tile, const int32_t* labels_tile) {
   CG_CUDA(cudaSetDevice(device_));
   const Mat& h0 = h_.at(0).m;
-  if (h0.rows && h0.cols)
-    CG_CUDA(cudaMemcpy2DAsync(h0.p, h0.ld * sizeof(float), x_tile, h0.cols * sizeof(float),
-                              h0.cols * sizeof(float), h0.rows, cudaMemcpyHostToDevice, cs_));
+  if (h0.rows && h0.cols) {
+    // One contiguous DMA (pitched 2D copies run row by row), then re-pitch on the GPU.
+    stage_.resize(static_cast<size_t>(h0.rows * h0.cols));
+    CG_CUDA(cudaMemcpyAsync(stage_.get(), x_tile, h0.rows * h0.cols * sizeof(float),
+                            cudaMemcpyHostToDevice, cs_));
+    kern::copy2d(h0.p, h0.ld, stage_.get(), h0.cols, h0.rows, h0.cols, cs_);
+  }
   if (h0.rows)
     CG_CUDA(cudaMemcpyAsync(labels_.get(), labels_tile, h0.rows * sizeof(int32_t),
                             cudaMemcpyHostToDevice, cs_));

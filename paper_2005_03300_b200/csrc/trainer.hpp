@@ -9,6 +9,7 @@
 
 #include <nccl.h>
 
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -106,6 +107,9 @@ class Trainer {
     double ms = 0, bytes = 0, flops = 0;
   };
   void set_timing(bool on) { timing_ = on; }
+  // Narrow-first propagation Aᵀ(H W) when f_out < f_in (block-row strategies).
+  void set_reassociate(bool on) { reassociate_ = on; }
+  bool reassociate() const { return reassociate_; }
   void reset_profile() {
     collect_profile();
     profile_.clear();
@@ -150,6 +154,7 @@ class Trainer {
     double bytes = 0, flops = 0;
   };
   bool timing_ = false;
+  bool reassociate_ = false;
   std::vector<ProfRec> recs_;
   size_t recs_used_ = 0;
   std::vector<ProfEntry> profile_;
@@ -173,6 +178,10 @@ class Trainer {
   DevBuf<uint8_t> mask_;
   std::vector<DeviceCsr> a_parts_, at_parts_;
   DevBuf<double> loss_partial_;
+  DevBuf<float> stage_;  // host-input staging for step_host
+  // Column-block split tables of the local CSR parts, keyed by (row_ptr, blocks).
+  std::map<std::pair<const void*, int>, DevBuf<int64_t>> splits_;
+  static double l2_panel_bytes();
   DevBuf<double> losses_dev_;
   int epochs_done_ = 0;
   int epochs_read_ = 0;

@@ -55,6 +55,18 @@ def test_single_rank_matches_serial(cg, orc, strat):
     assert all(v == 0 for c in led.values() for v in c.values())  # P = 1 meters nothing
 
 
+@pytest.mark.parametrize("kind", ["1d", "1.5d"])
+def test_reassociated_matches_serial(cg, orc, kind):
+    """Narrow-first propagation Aᵀ(H W): same GCN, f_out-wide panels."""
+    dims = [40, 12, 7, 5]
+    data = cg.generate_dataset(96, 9.0, dims[0], dims[-1], 7, 8, 9)
+    model = cg.init_glorot(dims, 3, 0.25)
+    od = orc.generate_dataset(96, 9.0, dims[0], dims[-1], 7, 8, 9)
+    losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.25, 3)
+    out = run_single(cg, data, model, cg.Strategy(kind, 1, 1, 0, reassociate=True), 3)
+    assert max_rel_error(out, losses, h, y, g, w) < TOL
+
+
 def test_pinned_loss_trace_fp32(cg):
     expected = [1.4676915537761182, 1.3547714828994135, 1.3527671034478277,
                 1.3514914086563463, 1.3507757616337233]
@@ -134,6 +146,21 @@ DIST = {  # name -> (kind, P, repl, block, n, dims)   (tests/golden/make_golden.
     "15d_p8_c2": ("1.5d", 8, 2, 0, 20, [8, 6, 4]),
     "3d_p8": ("3d", 8, 1, 0, 9, [8, 8, 4]),
 }
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("kind,P,repl", [("1d", 2, 1), ("1.5d", 4, 2), ("1d", 4, 1)])
+def test_distributed_reassociated(cg, orc, need_gpus, kind, P, repl):
+    need_gpus(P)
+    dims = [24, 8, 6]
+    model = cg.init_glorot(dims, 5, 0.5)
+    out = cg.run_distributed(lambda dev: cg.generate_dataset(50, 6.0, 24, 6, 2, 3, 4, device=dev),
+                             model, cg.Strategy(kind, P, repl, reassociate=True), 3)
+    od = orc.generate_dataset(50, 6.0, 24, 6, 2, 3, 4)
+    losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.5, 3)
+    res = dict(losses=out.losses, h_final=out.h_final, y=out.y_final, g=out.g_final,
+               w=out.model.weights)
+    assert max_rel_error(res, losses, h, y, g, w) < TOL
 
 
 @pytest.mark.multigpu
