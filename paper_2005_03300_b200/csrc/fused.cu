@@ -160,6 +160,18 @@ __global__ void transpose2d_kernel(float* __restrict__ dst, int64_t ldd,
   }
 }
 
+__global__ void mask_relu_prime_kernel(float* __restrict__ g, int64_t ldg,
+                                       const float* __restrict__ z, int64_t ldz, int64_t rows,
+                                       int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / cols, c = e % cols;
+    const float x = g[r * ldg + c];
+    g[r * ldg + c] = z[r * ldz + c] > 0.f ? x : x * 0.f;
+  }
+}
+
 __global__ void fill_kernel(float* p, int64_t count, float v) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -227,6 +239,13 @@ void relu(const float* Z, int64_t rows, int cols, int64_t ldz, float* H, int64_t
 void sgd(float* W, const float* Y, int64_t count, float lr, cudaStream_t stream) {
   if (count <= 0) return;
   sgd_kernel<<<grid_for(count), 256, 0, stream>>>(W, Y, count, lr);
+  CG_LAUNCH_CHECK();
+}
+
+void mask_relu_prime(float* g, int64_t ldg, const float* z, int64_t ldz, int64_t rows,
+                     int64_t cols, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return;
+  mask_relu_prime_kernel<<<grid_for(rows * cols), 256, 0, stream>>>(g, ldg, z, ldz, rows, cols);
   CG_LAUNCH_CHECK();
 }
 

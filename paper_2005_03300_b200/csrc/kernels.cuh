@@ -65,6 +65,9 @@ void logsoftmax_nll_blocks(const float* base, int parts, const int* widths, int6
 void relu(const float* Z, int64_t rows, int cols, int64_t ldz, float* H, int64_t ldh,
           cudaStream_t stream);
 void sgd(float* W, const float* Y, int64_t count, float lr, cudaStream_t stream);
+// g[r, c] *= 1[z[r, c] > 0]   (hadamard with relu_prime, dense.cpp:72-92)
+void mask_relu_prime(float* g, int64_t ldg, const float* z, int64_t ldz, int64_t rows,
+                     int64_t cols, cudaStream_t stream);
 // dst[r, 0:cols] = src[r, 0:cols] for strided row-major blocks.
 void copy2d(float* dst, int64_t ldd, const float* src, int64_t lds, int64_t rows, int64_t cols,
             cudaStream_t stream);

@@ -85,8 +85,8 @@ struct SpmmArgs {
 };
 
 // VEC = 4: 16-byte vectors (requires 16 B aligned rows); VEC = 1: scalars.
-template <int VEC, int LPR, int VPL, bool ACC>
-__global__ void __launch_bounds__(kThreads) spmm_rows_kernel(const SpmmArgs a) {
+template <int VEC, int LPR, int VPL, bool ACC, bool TAIL>
+__global__ void __launch_bounds__(kThreads, VPL == 1 ? 4 : 1) spmm_rows_kernel(const SpmmArgs a) {
   using V = typename VecT<VEC>::T;
   constexpr int RPW = 32 / LPR;  // rows per warp
   const int lane = threadIdx.x & 31;
@@ -128,36 +128,95 @@ __global__ void __launch_bounds__(kThreads) spmm_rows_kernel(const SpmmArgs a) {
   }
 
   const int src0 = grp * LPR;
-  for (int64_t base = 0; base < maxlen; base += LPR) {
-    int c = 0;
-    float v = 0.f;
-    if (base + sub < len) {
-      c = __ldg(col_idx + beg + base + sub);
-      v = __ldg(vals + beg + base + sub);
-    }
-    const int64_t remain = len - base;  // nonzeros of this group left in the chunk
+  if constexpr (VPL > 1) {
+    // Wide rows: every lane already has VPL independent vector gathers per
+    // nonzero in flight; walk the group's nonzeros one at a time.
+    for (int64_t base = 0; base < maxlen; base += LPR) {
+      int c = 0;
+      float v = 0.f;
+      if (base + sub < len) {
+        c = __ldg(col_idx + beg + base + sub);
+        v = __ldg(vals + beg + base + sub);
+      }
+      const int64_t remain = len - base;
 #pragma unroll 4
-    for (int t = 0; t < LPR; ++t) {
-      const int cc = __shfl_sync(0xffffffffu, c, src0 + t);
-      const float vv = __shfl_sync(0xffffffffu, v, src0 + t);
-      if (t < remain) {
-        const float* hrow = H + static_cast<int64_t>(cc) * a.ldh;
-        V hv[VPL];
+      for (int t = 0; t < LPR; ++t) {
+        const int cc = __shfl_sync(0xffffffffu, c, src0 + t);
+        const float vv = __shfl_sync(0xffffffffu, v, src0 + t);
+        if (t < remain) {
+          const float* hrow = H + static_cast<int64_t>(cc) * a.ldh;
+          V hv[VPL];
 #pragma unroll
-        for (int i = 0; i < VPL; ++i) {
-          const int vec = sub + i * LPR;
-          zero_vec(hv[i]);
-          if (vec < nvec) {
-            if constexpr (VEC == 4)
-              hv[i] = load_vec(hrow, vec, f);
-            else
-              hv[i] = __ldg(hrow + vec);
+          for (int i = 0; i < VPL; ++i) {
+            const int vec = sub + i * LPR;
+            zero_vec(hv[i]);
+            if (vec < nvec) {
+              if constexpr (VEC == 4)
+                hv[i] = TAIL ? load_vec(hrow, vec, f)
+                             : __ldg(reinterpret_cast<const float4*>(hrow) + vec);
+              else
+                hv[i] = __ldg(hrow + vec);
+            }
           }
-        }
 #pragma unroll
-        for (int i = 0; i < VPL; ++i) fma_vec(acc[i], vv, hv[i]);
+          for (int i = 0; i < VPL; ++i) fma_vec(acc[i], vv, hv[i]);
+        }
       }
     }
+  } else {
+  // Narrow rows (one vector per lane): a chunk covers U*LPR nonzeros; the
+  // gathers are issued in batches of TB nonzeros, predicated rather than
+  // branched so they are all in flight, and folded in ascending order.
+  constexpr int U = LPR >= 8 ? 1 : 8 / LPR;
+  constexpr int CH = U * LPR;
+  constexpr int TB = VPL >= 8 ? 1 : 8 / VPL;
+  for (int64_t base = 0; base < maxlen; base += CH) {
+    int c[U];
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = base + u * LPR + sub;
+      c[u] = q < len ? __ldg(col_idx + beg + q) : 0;
+      v[u] = q < len ? __ldg(vals + beg + q) : 0.f;
+    }
+#pragma unroll
+    for (int t0 = 0; t0 < CH; t0 += TB) {
+      V hv[TB][VPL];
+      float w[TB];
+#pragma unroll
+      for (int tb = 0; tb < TB; ++tb) {
+        const int t = t0 + tb;
+        if (t < CH) {
+          const int cc = __shfl_sync(0xffffffffu, c[t / LPR], src0 + t % LPR);
+          w[tb] = __shfl_sync(0xffffffffu, v[t / LPR], src0 + t % LPR);
+          const bool live = base + t < len;
+          const float* hrow = H + static_cast<int64_t>(cc) * a.ldh;
+#pragma unroll
+          for (int i = 0; i < VPL; ++i) {
+            const int vec = sub + i * LPR;
+            V zero;
+            zero_vec(zero);
+            // Select form (not a branch) so every gather is issued up front;
+            // dead slots read nothing and contribute w = 0 times 0.
+            if constexpr (VEC == 4)
+              hv[tb][i] = (live && vec < nvec)
+                              ? (TAIL ? load_vec(hrow, vec, f)
+                                      : __ldg(reinterpret_cast<const float4*>(hrow) + vec))
+                              : zero;
+            else
+              hv[tb][i] = (live && vec < nvec) ? __ldg(hrow + vec) : zero;
+          }
+        }
+      }
+#pragma unroll
+      for (int tb = 0; tb < TB; ++tb) {
+        if (t0 + tb < CH) {
+#pragma unroll
+          for (int i = 0; i < VPL; ++i) fma_vec(acc[i], w[tb], hv[tb][i]);
+        }
+      }
+    }
+  }
   }
 
   if (row < a.n_rows) {
@@ -178,10 +237,20 @@ template <int VEC, int LPR, int VPL>
 void launch_one(const SpmmArgs& a, bool acc, cudaStream_t s) {
   constexpr int rows_per_block = (kThreads / 32) * (32 / LPR);
   const int64_t blocks = ceil_div64(a.n_rows, rows_per_block);
-  if (acc)
-    spmm_rows_kernel<VEC, LPR, VPL, true><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a);
-  else
-    spmm_rows_kernel<VEC, LPR, VPL, false><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(a);
+  const unsigned g = static_cast<unsigned>(blocks);
+  // The scalar-tail path is only compiled in when f is not a multiple of 4.
+  const bool tail = VEC == 4 && (a.f % 4) != 0;
+  if (acc) {
+    if (tail)
+      spmm_rows_kernel<VEC, LPR, VPL, true, true><<<g, kThreads, 0, s>>>(a);
+    else
+      spmm_rows_kernel<VEC, LPR, VPL, true, false><<<g, kThreads, 0, s>>>(a);
+  } else {
+    if (tail)
+      spmm_rows_kernel<VEC, LPR, VPL, false, true><<<g, kThreads, 0, s>>>(a);
+    else
+      spmm_rows_kernel<VEC, LPR, VPL, false, false><<<g, kThreads, 0, s>>>(a);
+  }
   CG_LAUNCH_CHECK();
 }
 

@@ -55,7 +55,16 @@ class TrainerRows final : public Trainer {
       finish_layer(l, z);
       return;
     }
-    Mat t = view(acc_, h.rows, fin);
+    // A widening layer keeps T = Aᵀ H for the narrow-first backward.
+    const bool keep = reassociate_ && fout > fin;
+    if (saved_t_.size() < static_cast<size_t>(num_layers())) {
+      saved_t_.resize(static_cast<size_t>(num_layers()));
+      saved_valid_.assign(static_cast<size_t>(num_layers()), false);
+    }
+    if (keep && saved_t_[static_cast<size_t>(l)].m.p == nullptr)
+      saved_t_[static_cast<size_t>(l)].alloc(h.rows, fin);
+    Mat t = keep ? saved_t_[static_cast<size_t>(l)].m : view(acc_, h.rows, fin);
+    saved_valid_[static_cast<size_t>(l)] = keep;
     stages(at_parts_, h, t);
     if (!one_d()) row_reduce(t);
     if (l + 1 == num_layers()) {
@@ -78,6 +87,30 @@ class TrainerRows final : public Trainer {
     loss_all_reduce(loss_partial_.get());
     for (int l = L - 1; l >= 1; --l) {
       const Mat& g = g_[static_cast<size_t>(l - 1)].m;
+      if (reassociate_ && saved_t_ok(l)) {
+        // Narrow-first backward for a widening layer (f_out > f_in):
+        //   Y = Hᵀ (A G) = (Aᵀ H)ᵀ G = Tᵀ G with T kept from the forward pass;
+        //   G_prev = (A (G Wᵀ)) ⊙ relu′(Z_prev): the SpMM runs f_in wide.
+        Mat y = Y_[static_cast<size_t>(l - 1)].m;
+        if (grid_.col_of(rank_) == 0)
+          gemm_hts(saved_t_[static_cast<size_t>(l)].m, g, y, false);
+        else
+          CG_CUDA(cudaMemsetAsync(y.p, 0, y.rows * y.ld * sizeof(float), cs_));
+        ms_after_cs();
+        comm_->all_reduce(grid_.world(), y.p, static_cast<size_t>(y.rows * y.cols), ncclFloat32,
+                          Category::Reduce, words(y), ms_);
+        cs_after_ms();
+        if (l >= 2) {
+          Mat gp = g_[static_cast<size_t>(l - 2)].m;
+          Mat u = view(acc_, g.rows, dims_[static_cast<size_t>(l - 1)]);
+          gemm_swt(g, l - 1, 0, 0, u, false, kern::EPI_NONE, nullptr);
+          stages(a_parts_, u, gp);
+          if (!one_d()) row_reduce(gp);
+          const Mat& zp = z_[static_cast<size_t>(l - 2)].m;
+          kern::mask_relu_prime(gp.p, gp.ld, zp.p, zp.ld, gp.rows, gp.cols, cs_);
+        }
+        continue;
+      }
       Mat s = view(acc_, g.rows, dims_[static_cast<size_t>(l)]);
       stages(a_parts_, g, s);
       if (!one_d()) row_reduce(s);
@@ -155,8 +188,14 @@ class TrainerRows final : public Trainer {
     cs_after_ms();
   }
 
+  bool saved_t_ok(int l) const {
+    return static_cast<size_t>(l) < saved_valid_.size() && saved_valid_[static_cast<size_t>(l)];
+  }
+
   OwnedMat acc_;
   OwnedMat panel_[2];
+  std::vector<OwnedMat> saved_t_;  // T = Aᵀ H of widening layers (narrow-first backward)
+  std::vector<bool> saved_valid_;
 };
 
 }  // namespace
