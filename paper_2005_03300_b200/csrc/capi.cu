@@ -143,7 +143,7 @@ int cagnet_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
     cagnet::require(n_rows == 0 || (row_ptr && T), "spmm: null row_ptr or output");
     cagnet::require(nnz == 0 || (col_idx && vals && H), "spmm: null input arrays");
     cagnet::kern::spmm_csr(n_rows, row_ptr, col_idx, vals, H, ldh, f, T, ldt, accumulate != 0,
-                           as_stream(stream));
+                           as_stream(stream), nnz);
   });
 }
 

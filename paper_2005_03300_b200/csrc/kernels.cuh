@@ -14,13 +14,14 @@ namespace kern {
 // T[i, 0:f] = (accumulate ? T[i, 0:f] : 0) + sum_k vals[k] * H[col[k], 0:f]
 // with the nonzeros of each row folded in ascending order (the reference's
 // accumulation order), one fp32 FMA per term.
+// nnz (optional, -1 = unknown) sizes the row teams of the narrow-row kernel.
 void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
               const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
-              cudaStream_t stream);
+              cudaStream_t stream, int64_t nnz = -1);
 // Same, with row i's nonzeros given as [seg_begin[i], seg_end[i]).
 void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_end,
                    const int32_t* col_idx, const float* vals, const float* H, int64_t ldh, int f,
-                   float* T, int64_t ldt, bool accumulate, cudaStream_t stream);
+                   float* T, int64_t ldt, bool accumulate, cudaStream_t stream, int64_t nnz = -1);
 // split[b * rows + r] (b = 0..nb) = first nonzero of row r in column block b
 // of the ceiling-rule split of n_cols into nb blocks; split[nb * rows + r] = row end.
 void column_splits(int64_t rows, int64_t n_cols, int nb, const int64_t* row_ptr,

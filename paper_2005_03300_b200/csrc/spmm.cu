@@ -82,6 +82,7 @@ struct SpmmArgs {
   int f;
   float* T;
   int64_t ldt;
+  double mean_row_nnz;  // host-side hint for the row-team shape
 };
 
 // VEC = 4: 16-byte vectors (requires 16 B aligned rows); VEC = 1: scalars.
@@ -287,9 +288,120 @@ void pick_shape(int nvec, int* lpr, int* vpl) {
   *vpl = best_v < 1 ? 1 : best_v;
 }
 
+// Narrow rows (f <= 32): a team of QPR x LV lanes owns one output row; LV
+// lanes cover the row's float4 vectors and the QPR sub-teams stride over the
+// row's nonzeros (sub-team q takes q, q+QPR, ...), so every lane streams
+// independent gathers with no shuffles in the loop (U in flight); the QPR
+// partial sums are folded with xor shuffles at the end (deterministic order).
+template <int LV, int QPR, int U, bool ACC, bool TAIL>
+__global__ void __launch_bounds__(kThreads, 4) spmm_nzpar_kernel(const SpmmArgs a) {
+  constexpr int TEAM = LV * QPR;
+  constexpr int RPW = 32 / TEAM;
+  const int lane = threadIdx.x & 31;
+  const int vec = lane % LV;
+  const int q = (lane % TEAM) / LV;
+  const int64_t row =
+      ((static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5) * RPW + lane / TEAM;
+  const int f = a.f;
+  const int nvec = (f + 3) / 4;
+  const bool vec_ok = vec < nvec;
+  const int32_t* __restrict__ col_idx = a.col_idx;
+  const float* __restrict__ vals = a.vals;
+  const float4* __restrict__ H4 = reinterpret_cast<const float4*>(a.H);
+  const int64_t ldh4 = a.ldh / 4;
+
+  int64_t p = 0, e = 0;
+  if (row < a.n_rows) {
+    p = a.seg_begin[row] + q;
+    e = a.seg_end[row];
+  }
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto gather = [&](int c) -> float4 {
+    if (!vec_ok) return make_float4(0.f, 0.f, 0.f, 0.f);
+    if (TAIL) return load_vec(a.H + static_cast<int64_t>(c) * a.ldh, vec, f);
+    return __ldg(H4 + static_cast<int64_t>(c) * ldh4 + vec);
+  };
+  for (; p + (U - 1) * QPR < e; p += U * QPR) {
+    float4 h[U];
+    float w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = __ldg(col_idx + p + u * QPR);
+      w[u] = __ldg(vals + p + u * QPR);
+      h[u] = gather(c);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) fma_vec(acc, w[u], h[u]);
+  }
+  for (; p < e; p += QPR) fma_vec(acc, __ldg(vals + p), gather(__ldg(col_idx + p)));
+#pragma unroll
+  for (int o = LV; o < TEAM; o <<= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+    acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+  }
+  if (row < a.n_rows && q == 0 && vec_ok) {
+    float* trow = a.T + row * a.ldt;
+    if (ACC) {
+      const float4 old = load_vec(trow, vec, f);
+      acc.x = old.x + acc.x;
+      acc.y = old.y + acc.y;
+      acc.z = old.z + acc.z;
+      acc.w = old.w + acc.w;
+    }
+    store_vec(trow, vec, f, acc);
+  }
+}
+
+template <int LV, int QPR>
+void launch_nzpar(const SpmmArgs& a, bool acc, cudaStream_t s) {
+  constexpr int rows_per_block = (kThreads / 32) * (32 / (LV * QPR));
+  const unsigned g = static_cast<unsigned>(ceil_div64(a.n_rows, rows_per_block));
+  const bool tail = (a.f % 4) != 0;
+  if (acc) {
+    if (tail)
+      spmm_nzpar_kernel<LV, QPR, 4, true, true><<<g, kThreads, 0, s>>>(a);
+    else
+      spmm_nzpar_kernel<LV, QPR, 4, true, false><<<g, kThreads, 0, s>>>(a);
+  } else {
+    if (tail)
+      spmm_nzpar_kernel<LV, QPR, 4, false, true><<<g, kThreads, 0, s>>>(a);
+    else
+      spmm_nzpar_kernel<LV, QPR, 4, false, false><<<g, kThreads, 0, s>>>(a);
+  }
+  CG_LAUNCH_CHECK();
+}
+
+template <int LV>
+void launch_nzpar_q(int qpr, const SpmmArgs& a, bool acc, cudaStream_t s) {
+  switch (qpr) {
+    case 1: return launch_nzpar<LV, 1>(a, acc, s);
+    case 2: if constexpr (LV <= 16) return launch_nzpar<LV, 2>(a, acc, s); break;
+    case 4: if constexpr (LV <= 8) return launch_nzpar<LV, 4>(a, acc, s); break;
+    default: if constexpr (LV <= 4) return launch_nzpar<LV, 8>(a, acc, s); break;
+  }
+  launch_nzpar<LV, 1>(a, acc, s);
+}
+
 template <int VEC>
 void dispatch(const SpmmArgs& a, bool acc, cudaStream_t s) {
   const int nvec = (a.f + VEC - 1) / VEC;
+  if (VEC == 4 && nvec <= 8) {
+    // Sub-teams per row from the mean row length (8 nonzeros per sub-team
+    // at least), capped by the warp width.
+    const int lv = nvec <= 1 ? 1 : nvec <= 2 ? 2 : nvec <= 4 ? 4 : 8;
+    int qpr = 32 / lv;
+    const double mean = a.mean_row_nnz;
+    while (qpr > 1 && mean < 8.0 * qpr) qpr >>= 1;
+    if (qpr > 8) qpr = 8;
+    switch (lv) {
+      case 1: return launch_nzpar_q<1>(qpr, a, acc, s);
+      case 2: return launch_nzpar_q<2>(qpr, a, acc, s);
+      case 4: return launch_nzpar_q<4>(qpr, a, acc, s);
+      default: return launch_nzpar_q<8>(qpr, a, acc, s);
+    }
+  }
   int lpr, vpl;
   pick_shape(nvec, &lpr, &vpl);
   switch (lpr) {
@@ -329,8 +441,9 @@ __global__ void column_splits_kernel(int64_t rows, int nb, int64_t step,
 
 void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_end,
                    const int32_t* col_idx, const float* vals, const float* H, int64_t ldh, int f,
-                   float* T, int64_t ldt, bool accumulate, cudaStream_t stream) {
+                   float* T, int64_t ldt, bool accumulate, cudaStream_t stream, int64_t nnz) {
   if (n_rows <= 0 || f <= 0) return;
+  const double mean = nnz >= 0 ? static_cast<double>(nnz) / static_cast<double>(n_rows) : 64.0;
   const bool aligned = (ldh % 4 == 0) && (ldt % 4 == 0) &&
                        (reinterpret_cast<uintptr_t>(H) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(T) % 16 == 0);
@@ -338,7 +451,7 @@ void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_
   const int chunk = aligned ? 32 * 8 * 4 : 32 * 8;
   for (int c0 = 0; c0 < f; c0 += chunk) {
     SpmmArgs a{n_rows, seg_begin, seg_end, col_idx, vals, H + c0, ldh, f - c0 < chunk ? f - c0 : chunk,
-               T + c0, ldt};
+               T + c0, ldt, mean};
     if (aligned)
       dispatch<4>(a, accumulate, stream);
     else
@@ -348,8 +461,9 @@ void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_
 
 void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
               const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
-              cudaStream_t stream) {
-  spmm_segments(n_rows, row_ptr, row_ptr + 1, col_idx, vals, H, ldh, f, T, ldt, accumulate, stream);
+              cudaStream_t stream, int64_t nnz) {
+  spmm_segments(n_rows, row_ptr, row_ptr + 1, col_idx, vals, H, ldh, f, T, ldt, accumulate, stream,
+                nnz);
 }
 
 void column_splits(int64_t rows, int64_t n_cols, int nb, const int64_t* row_ptr,

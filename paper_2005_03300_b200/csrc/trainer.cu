@@ -261,7 +261,7 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc) {
   for (int b = 0; b < nb; ++b)
     kern::spmm_segments(a.n_rows, split + b * a.n_rows, split + (b + 1) * a.n_rows, a.col_idx.get(),
                         a.vals.get(), h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld,
-                        acc || b > 0, cs_);
+                        acc || b > 0, cs_, a.nnz / nb);
   if (slot >= 0) {
     const double f = static_cast<double>(h.cols), r = static_cast<double>(a.n_rows);
     const double bytes = 8.0 * (r + 1) + 8.0 * a.nnz + 4.0 * f * h.rows + 4.0 * f * r * (acc ? 2 : 1);
@@ -282,7 +282,7 @@ void Trainer::spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32
   if (out.rows != rows || out.cols != h.cols)
     throw std::invalid_argument("spmm: accumulator shape mismatch");
   const int slot = prof_begin();
-  kern::spmm_csr(rows, rp, ci, v, h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld, acc, cs_);
+  kern::spmm_csr(rows, rp, ci, v, h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld, acc, cs_, nnz);
   if (slot >= 0) {
     // B = 8(r+1) + 8 nnz + 4 f c + 4 f r (1 + acc); F = 2 nnz f.
     const double f = static_cast<double>(h.cols), r = static_cast<double>(rows);

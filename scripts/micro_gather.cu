@@ -77,6 +77,35 @@ __global__ void __launch_bounds__(256) k_lpr4u(int n, const int64_t* rp, const i
   if (row < n) T[row * 4 + sub] = acc;
 }
 
+// (g): QPR quads (4 lanes) per row, each quad strides over the row's nonzeros
+// (no shuffles in the loop), U independent gathers per lane in flight,
+// quad partial sums reduced with xor shuffles at the end.
+template <int QPR, int U>
+__global__ void __launch_bounds__(256) k_qpr(int n, const int64_t* rp, const int* ci, const float* v, const float4* H, float4* T) {
+  constexpr int LPR = 4 * QPR, RPW = 32 / LPR;
+  const int lane = threadIdx.x & 31, sub = lane & 3, q = (lane % LPR) >> 2, grp = lane / LPR;
+  const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) / 32 * RPW + grp;
+  int64_t b = 0, e = 0;
+  if (row < n) { b = rp[row]; e = rp[row + 1]; }
+  float4 acc = make_float4(0, 0, 0, 0);
+  int64_t p = b + q;
+  for (; p + (U - 1) * QPR < e; p += U * QPR) {
+    float4 h[U]; float w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) { const int c = __ldg(ci + p + u * QPR); w[u] = __ldg(v + p + u * QPR); h[u] = __ldg(H + (int64_t)c * 4 + sub); }
+#pragma unroll
+    for (int u = 0; u < U; ++u) { acc.x = fmaf(w[u], h[u].x, acc.x); acc.y = fmaf(w[u], h[u].y, acc.y); acc.z = fmaf(w[u], h[u].z, acc.z); acc.w = fmaf(w[u], h[u].w, acc.w); }
+  }
+  for (; p < e; p += QPR) { const int c = __ldg(ci + p); const float w = __ldg(v + p); const float4 h = __ldg(H + (int64_t)c * 4 + sub);
+    acc.x = fmaf(w, h.x, acc.x); acc.y = fmaf(w, h.y, acc.y); acc.z = fmaf(w, h.z, acc.z); acc.w = fmaf(w, h.w, acc.w); }
+#pragma unroll
+  for (int o = 4; o < LPR; o <<= 1) {
+    acc.x += __shfl_xor_sync(~0u, acc.x, o); acc.y += __shfl_xor_sync(~0u, acc.y, o);
+    acc.z += __shfl_xor_sync(~0u, acc.z, o); acc.w += __shfl_xor_sync(~0u, acc.w, o);
+  }
+  if (row < n && q == 0) T[row * 4 + sub] = acc;
+}
+
 // (c): warp per row, lane per nonzero, 4 x float4 per lane, butterfly reduce.
 template <bool NA>
 __global__ void __launch_bounds__(256) k_lane_nnz(int n, const int64_t* rp, const int* ci, const float* v, const float4* H, float4* T) {
@@ -163,6 +192,11 @@ int main() {
   run("stream col/val", [&] { k_stream<<<148 * 8, 256>>>(nnz, d_ci, d_v, d_o); });
   run("lpr4 ldg", [&] { k_lpr4<false, 4><<<b4, 256>>>(n, d_rp, d_ci, d_v, d_H, d_T); });
   run("lpr4 L1::no_allocate", [&] { k_lpr4<true, 4><<<b4, 256>>>(n, d_rp, d_ci, d_v, d_H, d_T); });
+  run("qpr8 U=2", [&] { k_qpr<8, 2><<<(n + 7) / 8, 256>>>(n, d_rp, d_ci, d_v, d_H, d_T); });
+  run("qpr8 U=4", [&] { k_qpr<8, 4><<<(n + 7) / 8, 256>>>(n, d_rp, d_ci, d_v, d_H, d_T); });
+  run("qpr8 U=8", [&] { k_qpr<8, 8><<<(n + 7) / 8, 256>>>(n, d_rp, d_ci, d_v, d_H, d_T); });
+  run("qpr4 U=4", [&] { k_qpr<4, 4><<<(n + 15) / 16, 256>>>(n, d_rp, d_ci, d_v, d_H, d_T); });
+  run("qpr2 U=4", [&] { k_qpr<2, 4><<<(n + 31) / 32, 256>>>(n, d_rp, d_ci, d_v, d_H, d_T); });
   run("lpr4u U=1", [&] { k_lpr4u<1><<<b4, 256>>>(n, d_rp, d_ci, d_v, d_H, d_T); });
   run("lpr4u U=2", [&] { k_lpr4u<2><<<b4, 256>>>(n, d_rp, d_ci, d_v, d_H, d_T); });
   run("lpr4u U=4", [&] { k_lpr4u<4><<<b4, 256>>>(n, d_rp, d_ci, d_v, d_H, d_T); });

@@ -72,7 +72,7 @@ int main(int argc, char** argv) {
     cagnet::DevBuf<float> H(static_cast<size_t>(n) * ld), T(static_cast<size_t>(n) * ld);
     CG_CUDA(cudaMemset(H.get(), 0, static_cast<size_t>(n) * ld * 4));
     auto launch = [&] {
-      cagnet::kern::spmm_csr(n, d_rp.get(), d_ci.get(), d_v.get(), H.get(), ld, f, T.get(), ld, false, 0);
+      cagnet::kern::spmm_csr(n, d_rp.get(), d_ci.get(), d_v.get(), H.get(), ld, f, T.get(), ld, false, 0, nnz);
     };
     launch();
     CG_CUDA(cudaDeviceSynchronize());
