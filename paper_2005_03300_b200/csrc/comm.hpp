@@ -68,6 +68,14 @@ class Comm {
                   ncclDataType_t t, Category cat, const std::vector<uint64_t>& slot_words,
                   cudaStream_t s);
 
+  // Fuse the collectives issued in between into one NCCL launch.
+  void group_start() {
+    if (ranks_ > 1) CG_NCCL(ncclGroupStart());
+  }
+  void group_end() {
+    if (ranks_ > 1) CG_NCCL(ncclGroupEnd());
+  }
+
   // Unmetered world all-gather for setup metadata (tile shapes).
   void setup_all_gather(const void* send, void* recv, size_t count, ncclDataType_t t,
                         cudaStream_t s);

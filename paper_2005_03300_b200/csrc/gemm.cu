@@ -15,6 +15,7 @@
 // mbarrier releases the stage, and four epilogue warps drain TMEM with
 // tcgen05.ld and apply the fused epilogue (ReLU + save Z, or ⊙ relu′(Z)).
 #include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -137,7 +138,6 @@ struct Stager {
   }
 };
 
-
 __device__ __forceinline__ float apply_epilogue(const Params& p, int64_t r, int64_t c, float v) {
   if (p.accumulate) v += p.C[r * p.ldc + c];
   if (p.epilogue == EPI_RELU) {
@@ -156,9 +156,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tf32x3_kernel(const Params p
   constexpr uint32_t B_BYTES = BN * BK * 4;
   constexpr uint32_t STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
-  constexpr uint32_t IDESC = tc::idesc_tf32(BM, BN, 0, 0);  // both operands K-major in smem
+  // Both operands K-major in smem.  (MN-major tf32 operands need the
+  // SWIZZLE_128B_BASE32B layout — cute sm100 builders; the plain MN-major
+  // layouts return zeros — so MN-contiguous operands are transposed while
+  // staging instead.)
+  constexpr uint32_t IDESC = tc::idesc_tf32(BM, BN, 0, 0);
 
-  extern __shared__ __align__(1024) char smem[];
+  extern __shared__ __align__(1024) char smem_raw[];
+  // Swizzled (mode 3) tiles need 1024 B alignment; the allocation carries 1 KB slack.
+  char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 2 * STAGE_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 2 * STAGE_BYTES + 16);
 
@@ -274,7 +280,7 @@ __global__ void splitk_reduce_kernel(const Params p, int splits) {
 
 template <int BN, int AMODE, int BMODE>
 void launch_bn(const Params& p, dim3 grid, cudaStream_t s) {
-  constexpr int smem = 2 * (2 * BM * BK * 4 + 2 * BN * BK * 4) + 64;
+  constexpr int smem = 2 * (2 * BM * BK * 4 + 2 * BN * BK * 4) + 64 + 1024;
   auto kfn = gemm_tf32x3_kernel<BN, AMODE, BMODE>;
   static std::atomic<uint64_t> configured{0};  // one bit per device
   const int dev = current_device();
@@ -309,6 +315,15 @@ void launch_bmode(int bmode, int bn, const Params& p, dim3 grid, cudaStream_t s)
 
 bool aligned16(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
 
+// CAGNET_GEMM_TMA=0 forces the register-staged kernel (A/B comparisons).
+bool gemm_tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CAGNET_GEMM_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // 0: K contiguous & vectorisable, 1: MN contiguous & vectorisable, 2: generic.
 int pick_mode(const float* base, int64_t s_mn, int64_t s_k) {
   if (!aligned16(base)) return 2;
@@ -321,6 +336,7 @@ int pick_mode(const float* base, int64_t s_mn, int64_t s_k) {
 
 void gemm_tf32x3(const GemmDesc& d, cudaStream_t stream) {
   if (d.m <= 0 || d.n <= 0) return;
+  if (gemm_tma_enabled() && gemm_tma_try(d, stream)) return;
   Params p{};
   p.m = d.m;
   p.n = d.n;

@@ -34,6 +34,18 @@ class TrainerRows final : public Trainer {
     const int64_t step = ceil_div64(data_.n, blocks());
     acc_.alloc(rows.size(), maxf);
     for (int i = 0; i < 2; ++i) panel_[i].alloc(step, maxf);
+    // Coalesced stages: this column's stage panels land side by side in one
+    // buffer (one fused NCCL group) and a single SpMM runs over the block row
+    // restricted to the stage columns [c_lo, c_hi).
+    const int j = grid_.col_of(rank_);
+    chunk_ok_ = stage_group().size() > 1 && chunk_end(j) > chunk_begin(j) + 1;
+    if (chunk_ok_) {
+      c_lo_ = block_range(data_.n, blocks(), chunk_begin(j)).begin;
+      c_hi_ = block_range(data_.n, blocks(), chunk_end(j) - 1).end;
+      a_chunk_ = extract_block_device(data_.adj, rows.begin, rows.end, c_lo_, c_hi_, cs_);
+      at_chunk_ = extract_block_device(data_.adj_t, rows.begin, rows.end, c_lo_, c_hi_, cs_);
+      gbuf_.alloc(c_hi_ - c_lo_, kCoalesceMaxF);
+    }
     CG_CUDA(cudaDeviceSynchronize());
   }
 
@@ -148,6 +160,29 @@ class TrainerRows final : public Trainer {
     const int j = grid_.col_of(rank_);
     const Group& grp = stage_group();
     const bool comm = grp.size() > 1;
+    if (chunk_ok_ && mine.cols <= kCoalesceMaxF) {
+      // Narrow panels: latency, not bandwidth, bounds each stage, so the
+      // stage broadcasts go out as one NCCL group (same calls, same ledger)
+      // into adjacent slots and one SpMM consumes them all.
+      const DeviceCsr& blk = &parts == &a_parts_ ? a_chunk_ : at_chunk_;
+      Mat g{gbuf_.m.p, c_hi_ - c_lo_, mine.cols, mine.ld};
+      ms_after_cs();
+      const int own = one_d() ? rank_ : grid_.row_of(rank_);
+      if (own >= chunk_begin(j) && own < chunk_end(j)) {
+        const BlockRange r = block_range(data_.n, blocks(), own);
+        kern::copy2d(g.p + (r.begin - c_lo_) * g.ld, g.ld, mine.p, mine.ld, mine.rows, mine.cols, ms_);
+      }
+      comm_->group_start();
+      for (int q = chunk_begin(j); q < chunk_end(j); ++q) {
+        const BlockRange r = block_range(data_.n, blocks(), q);
+        const int root = one_d() ? q : grid_.rank_at(q, j);
+        bcast_mat(grp, root, Mat{g.p + (r.begin - c_lo_) * g.ld, r.size(), g.cols, g.ld}, Category::DBcast);
+      }
+      comm_->group_end();
+      cs_after_ms();
+      spmm(blk, g, out, false);
+      return;
+    }
     ms_after_cs();
     int idx = 0;
     for (int q = chunk_begin(j); q < chunk_end(j); ++q, ++idx) {
@@ -192,8 +227,14 @@ class TrainerRows final : public Trainer {
     return static_cast<size_t>(l) < saved_valid_.size() && saved_valid_[static_cast<size_t>(l)];
   }
 
+  static constexpr int64_t kCoalesceMaxF = 64;
+
   OwnedMat acc_;
   OwnedMat panel_[2];
+  bool chunk_ok_ = false;
+  int64_t c_lo_ = 0, c_hi_ = 0;
+  DeviceCsr a_chunk_, at_chunk_;  // block row restricted to this column's stage columns
+  OwnedMat gbuf_;                 // stage panels side by side
   std::vector<OwnedMat> saved_t_;  // T = Aᵀ H of widening layers (narrow-first backward)
   std::vector<bool> saved_valid_;
 };

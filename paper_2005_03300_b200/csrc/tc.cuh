@@ -127,11 +127,18 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* out) {
   for (int i = 0; i < 16; ++i) out[i] = __uint_as_float(r[i]);
 }
 
-// Round-to-nearest TF32 (low 13 mantissa bits cleared).
+// Round-to-nearest (ties away) TF32 with two integer ALU ops: add half an
+// ulp of the 10-bit mantissa, clear the low 13 bits (same result as
+// cvt.rna.tf32.f32 for finite inputs, without the conversion pipe).
 __device__ __forceinline__ float to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+// Split x = hi + lo with hi exact in TF32 and lo = x - hi exact in fp32; the
+// tensor core reads only the top 19 bits of lo, an error below 2^-22 |x|.
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  hi = to_tf32(x);
+  lo = x - hi;
 }
 
 }  // namespace tc
