@@ -9,7 +9,6 @@ namespace kern {
 namespace {
 
 constexpr int kMaxParts = 8;
-constexpr int kLossBlocks = 1024;
 
 struct RowBlocks {
   const float* base;
@@ -82,6 +81,76 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Row-team variant for the common case (cols <= TPR * NV): TPR lanes own a
+// row, each keeps its NV columns in registers, so the row is read once and
+// every reduction is a few xor shuffles; one warp covers 32 / TPR rows and
+// the grid covers every row (no serial row loop per warp).
+template <int TPR, int NV, bool SINGLE>
+__global__ void __launch_bounds__(256)
+    logsoftmax_nll_rows_kernel(const RowBlocks zb, int64_t rows, int c0, int c1, float* logp,
+                               int64_t ldl, float* G, int64_t ldg,
+                               const int32_t* __restrict__ labels,
+                               const uint8_t* __restrict__ mask, double inv_total,
+                               double* __restrict__ partials) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % TPR;
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / TPR;
+  const int cols = zb.offs[zb.parts];
+  const bool live = r < rows;
+  float z[NV];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int j = sub + i * TPR;
+    z[i] = -INFINITY;
+    if (live && j < cols) z[i] = SINGLE ? zb.base[r * zb.ld + j] : load_col(zb, r, j);
+    mx = fmaxf(mx, z[i]);
+  }
+#pragma unroll
+  for (int o = TPR / 2; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    if (sub + i * TPR < cols) s += expf(z[i] - mx);
+#pragma unroll
+  for (int o = TPR / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  double loss = 0.0;
+  if (live) {
+    const float lse = logf(s);
+    const bool train = mask == nullptr || mask[r] != 0;
+    const int y = labels ? labels[r] : -1;
+    const float inv = static_cast<float>(inv_total);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int j = sub + i * TPR;
+      if (j >= c0 && j < c1) {
+        const float lp = (z[i] - mx) - lse;
+        if (logp) logp[r * ldl + (j - c0)] = lp;
+        if (G) {
+          float g = 0.f;
+          if (train) {
+            g = expf(lp) * inv;
+            if (j == y) g -= inv;
+          }
+          G[r * ldg + (j - c0)] = g;
+        }
+        if (train && j == y) loss = -static_cast<double>(lp);
+      }
+    }
+  }
+  // Deterministic block reduction in fp64.
+  __shared__ double red[8];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, o);
+  if (lane == 0) red[threadIdx.x >> 5] = loss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+    partials[blockIdx.x] = t;
+  }
+}
+
 __global__ void sum_partials_kernel(const double* __restrict__ partials, int count,
                                     double* out) {
   __shared__ double red[256];
@@ -96,18 +165,44 @@ __global__ void sum_partials_kernel(const double* __restrict__ partials, int cou
   if (threadIdx.x == 0) *out = red[0];
 }
 
+template <int TPR>
+void launch_lsm_rows(const RowBlocks& zb, int64_t rows, int c0, int c1, float* logp, int64_t ldl,
+                     float* G, int64_t ldg, const int32_t* labels, const uint8_t* mask,
+                     double inv, double* partials, int64_t blocks, cudaStream_t s) {
+  const unsigned g = static_cast<unsigned>(blocks);
+  if (zb.parts == 1)
+    logsoftmax_nll_rows_kernel<TPR, 8, true><<<g, 256, 0, s>>>(zb, rows, c0, c1, logp, ldl, G, ldg,
+                                                               labels, mask, inv, partials);
+  else
+    logsoftmax_nll_rows_kernel<TPR, 8, false><<<g, 256, 0, s>>>(zb, rows, c0, c1, logp, ldl, G, ldg,
+                                                                labels, mask, inv, partials);
+}
+
 void launch_lsm(const RowBlocks& zb, int64_t rows, int c0, int c1, float* logp, int64_t ldl,
                 float* G, int64_t ldg, const int32_t* labels, const uint8_t* mask,
                 int64_t train_total, double* loss_out, cudaStream_t s) {
-  const int sms = num_sms(current_device());
-  int64_t blocks = ceil_div64(rows > 0 ? rows : 1, 8);
-  if (blocks > 4 * sms) blocks = 4 * sms;
-  if (blocks > kLossBlocks) blocks = kLossBlocks;
-  double* partials = nullptr;
-  CG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&partials), kLossBlocks * sizeof(double), s));
+  const int cols = zb.offs[zb.parts];
   const double inv = train_total > 0 ? 1.0 / static_cast<double>(train_total) : 0.0;
-  logsoftmax_nll_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
-      zb, rows, c0, c1, logp, ldl, G, ldg, labels, mask, inv, partials);
+  const int tpr = cols <= 64 ? 8 : 32;
+  int64_t blocks;
+  if (cols <= 8 * 32) {
+    blocks = ceil_div64(rows > 0 ? rows : 1, 256 / tpr);
+  } else {
+    const int sms = num_sms(current_device());
+    blocks = ceil_div64(rows > 0 ? rows : 1, 8);
+    if (blocks > 4 * sms) blocks = 4 * sms;
+  }
+  double* partials = nullptr;
+  CG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&partials), blocks * sizeof(double), s));
+  if (cols <= 8 * 32) {
+    if (tpr == 8)
+      launch_lsm_rows<8>(zb, rows, c0, c1, logp, ldl, G, ldg, labels, mask, inv, partials, blocks, s);
+    else
+      launch_lsm_rows<32>(zb, rows, c0, c1, logp, ldl, G, ldg, labels, mask, inv, partials, blocks, s);
+  } else {
+    logsoftmax_nll_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(
+        zb, rows, c0, c1, logp, ldl, G, ldg, labels, mask, inv, partials);
+  }
   CG_LAUNCH_CHECK();
   if (loss_out) {
     sum_partials_kernel<<<1, 256, 0, s>>>(partials, static_cast<int>(blocks), loss_out);
@@ -116,12 +211,26 @@ void launch_lsm(const RowBlocks& zb, int64_t rows, int c0, int c1, float* logp, 
   CG_CUDA(cudaFreeAsync(partials, s));
 }
 
+// (row, col) of flat element e; 32-bit division whenever the extent allows.
+__device__ __forceinline__ void split_index(int64_t e, int64_t cols, int64_t total, int64_t& r,
+                                            int64_t& c) {
+  if (total < (int64_t{1} << 31)) {
+    const uint32_t q = static_cast<uint32_t>(e) / static_cast<uint32_t>(cols);
+    r = q;
+    c = static_cast<uint32_t>(e) - q * static_cast<uint32_t>(cols);
+  } else {
+    r = e / cols;
+    c = e % cols;
+  }
+}
+
 __global__ void relu_kernel(const float* __restrict__ Z, int64_t rows, int cols, int64_t ldz,
                             float* __restrict__ H, int64_t ldh) {
   const int64_t total = rows * cols;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = e / cols, c = e % cols;
+    int64_t r, c;
+    split_index(e, cols, total, r, c);
     const float z = Z[r * ldz + c];
     H[r * ldh + c] = z > 0.f ? z : 0.f;
   }
@@ -139,7 +248,8 @@ __global__ void copy2d_kernel(float* __restrict__ dst, int64_t ldd, const float*
   const int64_t total = rows * cols;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = e / cols, c = e % cols;
+    int64_t r, c;
+    split_index(e, cols, total, r, c);
     dst[r * ldd + c] = src[r * lds + c];
   }
 }
@@ -166,7 +276,8 @@ __global__ void mask_relu_prime_kernel(float* __restrict__ g, int64_t ldg,
   const int64_t total = rows * cols;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = e / cols, c = e % cols;
+    int64_t r, c;
+    split_index(e, cols, total, r, c);
     const float x = g[r * ldg + c];
     g[r * ldg + c] = z[r * ldz + c] > 0.f ? x : x * 0.f;
   }

@@ -17,6 +17,8 @@
 // without copying: the L2-aware blocking in spmm_blocked() runs one pass per
 // column block whose H panel fits in L2 and accumulates the passes in
 // ascending column order — the reference's own order (csr.hpp:68-70).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -36,6 +38,19 @@ template <>
 struct VecT<1> {
   using T = float;
 };
+
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float4 ldg_policy(const float4* p, uint64_t pol) {
+  float4 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
 
 __device__ __forceinline__ void fma_vec(float4& acc, float v, const float4& h) {
   acc.x = fmaf(v, h.x, acc.x);
@@ -293,47 +308,61 @@ void pick_shape(int nvec, int* lpr, int* vpl) {
 // row's nonzeros (sub-team q takes q, q+QPR, ...), so every lane streams
 // independent gathers with no shuffles in the loop (U in flight); the QPR
 // partial sums are folded with xor shuffles at the end (deterministic order).
-template <int LV, int QPR, int U, bool ACC, bool TAIL>
-__global__ void __launch_bounds__(kThreads, 4) spmm_nzpar_kernel(const SpmmArgs a) {
+template <int LV, int QPR, int U, bool ACC, bool TAIL, int NT = kThreads, int HINT = 0,
+          bool FULLV = false>
+__global__ void __launch_bounds__(NT, 1024 / NT) spmm_nzpar_kernel(const SpmmArgs a) {
   constexpr int TEAM = LV * QPR;
   constexpr int RPW = 32 / TEAM;
   const int lane = threadIdx.x & 31;
   const int vec = lane % LV;
   const int q = (lane % TEAM) / LV;
   const int64_t row =
-      ((static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5) * RPW + lane / TEAM;
+      ((static_cast<int64_t>(blockIdx.x) * NT + threadIdx.x) >> 5) * RPW + lane / TEAM;
+  uint64_t pol = 0;
+  if (HINT) pol = l2_evict_last_policy();
   const int f = a.f;
   const int nvec = (f + 3) / 4;
-  const bool vec_ok = vec < nvec;
-  const int32_t* __restrict__ col_idx = a.col_idx;
-  const float* __restrict__ vals = a.vals;
-  const float4* __restrict__ H4 = reinterpret_cast<const float4*>(a.H);
-  const int64_t ldh4 = a.ldh / 4;
+  // Lanes past the row's last vector idle on the gathers (only when nvec < LV).
+  const bool vec_ok = FULLV || vec < nvec;
+  // Row c of H starts c * ldh * 4 bytes in: one 32x32->64 multiply-add.
+  const char* __restrict__ hbase = reinterpret_cast<const char*>(a.H) + vec * 16;
+  const uint32_t ldh_bytes = static_cast<uint32_t>(a.ldh * 4);
 
-  int64_t p = 0, e = 0;
+  const int32_t* __restrict__ cp = a.col_idx;
+  const float* __restrict__ vp = a.vals;
+  const int32_t* ce = cp;
   if (row < a.n_rows) {
-    p = a.seg_begin[row] + q;
-    e = a.seg_end[row];
+    const int64_t b = a.seg_begin[row];
+    ce = cp + a.seg_end[row];
+    cp += b + q;
+    vp += b + q;
   }
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   auto gather = [&](int c) -> float4 {
     if (!vec_ok) return make_float4(0.f, 0.f, 0.f, 0.f);
     if (TAIL) return load_vec(a.H + static_cast<int64_t>(c) * a.ldh, vec, f);
-    return __ldg(H4 + static_cast<int64_t>(c) * ldh4 + vec);
+    const float4* src = reinterpret_cast<const float4*>(
+        hbase + static_cast<uint64_t>(static_cast<uint32_t>(c)) * ldh_bytes);
+    if (HINT) return ldg_policy(src, pol);
+    return __ldg(src);
   };
-  for (; p + (U - 1) * QPR < e; p += U * QPR) {
+  // The CSR arrays are streamed once: evict-first so they do not push the
+  // gathered H rows out of L2.
+  auto ld_c = [&](const int32_t* p) { return HINT ? __ldcs(p) : __ldg(p); };
+  auto ld_v = [&](const float* p) { return HINT ? __ldcs(p) : __ldg(p); };
+  for (; cp + (U - 1) * QPR < ce; cp += U * QPR, vp += U * QPR) {
     float4 h[U];
     float w[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int c = __ldg(col_idx + p + u * QPR);
-      w[u] = __ldg(vals + p + u * QPR);
+      const int c = ld_c(cp + u * QPR);
+      w[u] = ld_v(vp + u * QPR);
       h[u] = gather(c);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) fma_vec(acc, w[u], h[u]);
   }
-  for (; p < e; p += QPR) fma_vec(acc, __ldg(vals + p), gather(__ldg(col_idx + p)));
+  for (; cp < ce; cp += QPR, vp += QPR) fma_vec(acc, ld_v(vp), gather(ld_c(cp)));
 #pragma unroll
   for (int o = LV; o < TEAM; o <<= 1) {
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -354,23 +383,50 @@ __global__ void __launch_bounds__(kThreads, 4) spmm_nzpar_kernel(const SpmmArgs 
   }
 }
 
-template <int LV, int QPR>
-void launch_nzpar(const SpmmArgs& a, bool acc, cudaStream_t s) {
-  constexpr int rows_per_block = (kThreads / 32) * (32 / (LV * QPR));
+template <int LV, int QPR, int U, int NT, int HINT>
+void launch_nzpar_v(const SpmmArgs& a, bool acc, cudaStream_t s) {
+  constexpr int rows_per_block = (NT / 32) * (32 / (LV * QPR));
   const unsigned g = static_cast<unsigned>(ceil_div64(a.n_rows, rows_per_block));
   const bool tail = (a.f % 4) != 0;
+  const bool full = !tail && (a.f / 4) == LV;
   if (acc) {
     if (tail)
-      spmm_nzpar_kernel<LV, QPR, 4, true, true><<<g, kThreads, 0, s>>>(a);
+      spmm_nzpar_kernel<LV, QPR, U, true, true, NT, 0><<<g, NT, 0, s>>>(a);
+    else if (full)
+      spmm_nzpar_kernel<LV, QPR, U, true, false, NT, HINT, true><<<g, NT, 0, s>>>(a);
     else
-      spmm_nzpar_kernel<LV, QPR, 4, true, false><<<g, kThreads, 0, s>>>(a);
+      spmm_nzpar_kernel<LV, QPR, U, true, false, NT, HINT><<<g, NT, 0, s>>>(a);
   } else {
     if (tail)
-      spmm_nzpar_kernel<LV, QPR, 4, false, true><<<g, kThreads, 0, s>>>(a);
+      spmm_nzpar_kernel<LV, QPR, U, false, true, NT, 0><<<g, NT, 0, s>>>(a);
+    else if (full)
+      spmm_nzpar_kernel<LV, QPR, U, false, false, NT, HINT, true><<<g, NT, 0, s>>>(a);
     else
-      spmm_nzpar_kernel<LV, QPR, 4, false, false><<<g, kThreads, 0, s>>>(a);
+      spmm_nzpar_kernel<LV, QPR, U, false, false, NT, HINT><<<g, NT, 0, s>>>(a);
   }
   CG_LAUNCH_CHECK();
+}
+
+// Tuning knob for experiments (CAGNET_SPMM_TUNE=<variant>); 0 = the default
+// (128-thread CTAs, U = 4 gathers in flight per lane, no cache hints — the
+// fastest on the Reddit-shaped graph: 0.548 ms vs 0.565 ms with L2 evict hints
+// and 0.561 ms with 256-thread CTAs at f = 16).
+int spmm_tune() {
+  static const int v = [] {
+    const char* e = getenv("CAGNET_SPMM_TUNE");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <int LV, int QPR>
+void launch_nzpar(const SpmmArgs& a, bool acc, cudaStream_t s) {
+  switch (spmm_tune()) {
+    case 1: return launch_nzpar_v<LV, QPR, 4, kThreads, 0>(a, acc, s);
+    case 2: return launch_nzpar_v<LV, QPR, 4, 128, 1>(a, acc, s);
+    case 3: return launch_nzpar_v<LV, QPR, 8, 128, 0>(a, acc, s);
+    default: return launch_nzpar_v<LV, QPR, 4, 128, 0>(a, acc, s);
+  }
 }
 
 template <int LV>
