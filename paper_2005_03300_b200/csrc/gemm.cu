@@ -324,6 +324,15 @@ bool gemm_tma_enabled() {
   return on;
 }
 
+// CAGNET_GEMM_TM=0 disables the A-in-TMEM kernel (A/B comparisons).
+bool gemm_tm_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CAGNET_GEMM_TM");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // 0: K contiguous & vectorisable, 1: MN contiguous & vectorisable, 2: generic.
 int pick_mode(const float* base, int64_t s_mn, int64_t s_k) {
   if (!aligned16(base)) return 2;
@@ -336,6 +345,7 @@ int pick_mode(const float* base, int64_t s_mn, int64_t s_k) {
 
 void gemm_tf32x3(const GemmDesc& d, cudaStream_t stream) {
   if (d.m <= 0 || d.n <= 0) return;
+  if (gemm_tm_enabled() && gemm_tm_try(d, stream)) return;
   if (gemm_tma_enabled() && gemm_tma_try(d, stream)) return;
   Params p{};
   p.m = d.m;

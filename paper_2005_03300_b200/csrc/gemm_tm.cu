@@ -1,0 +1,580 @@
+// K2c — persistent, warp-specialised tcgen05 split-TF32 GEMM whose A operand
+// is staged in TENSOR MEMORY, for the GCN's tall-skinny contractions
+// (gemm_add, dense.cpp:37-70):
+//   T·W / H·W / S·Wᵀ : A = rows of a dense tile (K contiguous), B = W resident
+//   Hᵀ·S             : A = Hᵀ (M contiguous in memory, K = graph rows),
+//                      B = S streamed alongside A, split-K across CTAs.
+//
+// Why TMEM: with N <= 64 the kernel moves ~16 KB of A per 4 K-steps of tiny
+// MMAs, so shared-memory traffic, not the tensor pipe, was the ceiling of the
+// smem-operand kernel (TMA write + read + hi/lo write-back + three MMA reads
+// of A ≈ 7x the tile).  Here the TMA tile is read once by the converter warps
+// (thread = TMEM lane = output row), split into hi = tf32_rn(x) and
+// lo = x - hi in registers, and written to TMEM with tcgen05.st; the MMAs read
+// A from TMEM ("TS" form).  The reading thread picks the element order, so the
+// M-contiguous Hᵀ tile is transposed for free (tf32 smem operands must be
+// K-major).  B is stacked as [B_hi; B_lo] (2·BN rows, K-major SWIZZLE_128B),
+// so one N = 2·BN MMA gives A_hi·B_hi and A_hi·B_lo side by side and one
+// N = BN MMA adds A_lo·B_hi onto the second half:
+//   C = D[:, 0:BN] + D[:, BN:2BN]      (split-TF32, error ~2^-21 relative).
+//
+// Roles (one CTA per SM):
+//   warp 0      TMA producer: A tile (+ S tile when streamed) per k-block;
+//   warp 1      MMA issuer (one elected lane), TMEM allocator;
+//   warps 2-5   converters (TMA smem → hi/lo → TMEM; streamed B → [hi; lo]
+//               smem tile), then the epilogue of each finished tile
+//               (tcgen05.ld of the accumulator chains, fused ReLU / ⊙relu′ /
+//               accumulate, or the split-K partial).
+// Accumulator chains (k-step kk → chain kk % CH) keep several independent
+// MMAs in flight; two accumulator sets overlap tile t's epilogue with tile
+// t+1's MMAs when TMEM allows.
+#include <cuda.h>
+
+#include <atomic>
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "tc.cuh"
+
+namespace cagnet {
+namespace kern {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;
+constexpr int kConv = 128;
+constexpr int kThreads = 64 + kConv;
+constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
+constexpr int kMaxStages = 8;
+constexpr int kTmemStages = 4;            // A (hi + lo) stages in TMEM
+constexpr int kMaxResidentB = 96 * 1024;  // bytes of resident [B_hi; B_lo]
+
+template <int BN>
+struct Cfg {
+  static constexpr int CH = BN <= 16 ? 4 : BN <= 48 ? 2 : 1;       // accumulator chains
+  static constexpr int SETS = (BN == 48) ? 1 : 2;                  // accumulator sets
+  static constexpr uint32_t SET_COLS = CH * 2 * BN;
+  static constexpr uint32_t A_COLS = kTmemStages * 2 * BK;         // hi + lo per stage
+  static constexpr uint32_t D_BASE = A_COLS;
+  static constexpr uint32_t COLS = A_COLS + SETS * SET_COLS;
+  static_assert(COLS <= 512, "TMEM budget");
+  static constexpr uint32_t B_TILE = 2 * BN * BK * 4;              // [hi; lo] k-block
+  static constexpr uint32_t S_TILE = BN * BK * 4;                  // raw streamed S k-block
+};
+
+struct TmParams {
+  int64_t m, n, k;
+  const float* B;
+  int64_t b_sk, b_sn;
+  float* C;
+  int64_t ldc;
+  int accumulate;
+  int epilogue;
+  const float* aux;
+  int64_t ldaux;
+  float* aux_out;
+  int64_t ldao;
+  float* partial;   // split-K workspace [splits][m][n]; nullptr = direct epilogue
+  int64_t k_chunk;  // K per split (multiple of BK)
+  int nkb_res;      // k-blocks of resident B (0 when streamed)
+  int m_tiles;
+};
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1) << 16;          // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;  // SBO = 8 rows x 128 B
+  d |= static_cast<uint64_t>(1) << 46;          // sm_100 descriptor version
+  d |= static_cast<uint64_t>(2) << 61;          // SWIZZLE_128B
+  return d;
+}
+
+// Byte offset of (row, k) in a [rows x 32] fp32 SWIZZLE_128B tile.
+__device__ __forceinline__ uint32_t sw128_off(int row, int k) {
+  return static_cast<uint32_t>(row * 128 + ((((k >> 2) ^ (row & 7))) << 4) + (k & 3) * 4);
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t smem, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(bar)) : "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B[smem].
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 32 lanes x 32 bit, 32 consecutive columns per thread.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ float epilogue_value(const TmParams& p, int64_t r, int64_t c, float v) {
+  if (p.accumulate) v += p.C[r * p.ldc + c];
+  if (p.epilogue == EPI_RELU) {
+    if (p.aux_out) p.aux_out[r * p.ldao + c] = v > 0.f ? v : 0.f;
+  } else if (p.epilogue == EPI_RELU_PRIME) {
+    v = p.aux[r * p.ldaux + c] > 0.f ? v : v * 0.f;
+  }
+  return v;
+}
+
+// AMODE 0: A tile = 128 rows x 32 k, K contiguous (TMA SWIZZLE_128B).
+// AMODE 1: A tile = 32 k x 128 m, M contiguous (TMA, no swizzle) — Hᵀ.
+// BSTREAM: B (k x n, n contiguous) arrives by TMA with every k-block.
+template <int BN, int AMODE, bool BSTREAM>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                   const TmParams p, int ns) {
+  using K = Cfg<BN>;
+  constexpr int CH = K::CH;
+  constexpr uint32_t IDESC_HL = tc::idesc_tf32(BM, 2 * BN, 0, 0);  // A_hi · [B_hi; B_lo]
+  constexpr uint32_t IDESC_L = tc::idesc_tf32(BM, BN, 0, 0);       // A_lo · B_hi
+  constexpr int SB = kTmemStages;  // streamed [hi; lo] B stages (recycled with the TMEM stage)
+
+  extern __shared__ char smem_raw[];
+  char* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  char* a_ring = smem;                                  // ns x 16 KB
+  char* s_ring = a_ring + ns * A_TILE;                  // ns x S_TILE (streamed B raw)
+  char* b_cat = s_ring + (BSTREAM ? ns * K::S_TILE : 0);  // resident nkb or SB stages
+  const int b_slots = BSTREAM ? SB : p.nkb_res;
+  uint64_t* full = reinterpret_cast<uint64_t*>(b_cat + b_slots * K::B_TILE);
+  uint64_t* sempty = full + kMaxStages;       // smem stage read by the converters
+  uint64_t* conv = sempty + kMaxStages;       // [kTmemStages] TMEM A stage written
+  uint64_t* tempty = conv + kTmemStages;      // [kTmemStages] TMEM A stage consumed by MMA
+  uint64_t* afull = tempty + kTmemStages;     // [2] accumulator set complete
+  uint64_t* aempty = afull + 2;               // [2] accumulator set drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+
+  if (tid == 0) {
+    for (int s = 0; s < ns; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&sempty[s], kConv / 32);
+    }
+    for (int s = 0; s < kTmemStages; ++s) {
+      tc::mbar_init(&conv[s], kConv / 32);
+      tc::mbar_init(&tempty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&afull[i], 1);
+      tc::mbar_init(&aempty[i], kConv / 32);
+    }
+    tc::fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap)) : "memory");
+    if (BSTREAM)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&bmap)) : "memory");
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+
+  if (!BSTREAM) {
+    // Resident [B_hi; B_lo]: element (kk, j) of op(B) → rows j and BN + j,
+    // column kk % 32 of k-block kk / 32.
+    for (int e = tid; e < p.nkb_res * BN * BK; e += kThreads) {
+      const int kb = e / (BN * BK);
+      const int rem = e % (BN * BK);
+      const int j = rem / BK, kk = rem % BK;
+      const int64_t gk = static_cast<int64_t>(kb) * BK + kk;
+      const float x =
+          (gk < p.k && j < p.n) ? __ldg(p.B + gk * p.b_sk + static_cast<int64_t>(j) * p.b_sn) : 0.f;
+      const float h = tc::to_tf32(x);
+      char* t = b_cat + kb * K::B_TILE;
+      *reinterpret_cast<float*>(t + sw128_off(j, kk)) = h;
+      *reinterpret_cast<float*>(t + sw128_off(BN + j, kk)) = x - h;
+    }
+    tc::fence_proxy_async_smem();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // Work list: tiles (m_tile, split) strided over the grid.
+  const int splits = static_cast<int>((p.k + p.k_chunk - 1) / p.k_chunk);
+  const int tiles = p.m_tiles * splits;
+  const int my_tiles = tiles > static_cast<int>(blockIdx.x)
+                           ? (tiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+                           : 0;
+  auto tile_of = [&](int t, int& m_tile, int& split, int& nkb) {
+    const int id = static_cast<int>(blockIdx.x) + t * static_cast<int>(gridDim.x);
+    m_tile = id % p.m_tiles;
+    split = id / p.m_tiles;
+    const int64_t k0 = static_cast<int64_t>(split) * p.k_chunk;
+    const int64_t k1 = k0 + p.k_chunk < p.k ? k0 + p.k_chunk : p.k;
+    nkb = static_cast<int>((k1 - k0 + BK - 1) / BK);
+  };
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (elect_one()) {
+      int64_t g = 0;
+      for (int t = 0; t < my_tiles; ++t) {
+        int m_tile, split, nkb;
+        tile_of(t, m_tile, split, nkb);
+        const int64_t kb0 = static_cast<int64_t>(split) * (p.k_chunk / BK);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const int s = static_cast<int>(g % ns);
+          if (g >= ns) tc::mbar_wait(&sempty[s], static_cast<uint32_t>(((g / ns) - 1) & 1));
+          tc::mbar_arrive_expect_tx(&full[s], A_TILE + (BSTREAM ? K::S_TILE : 0));
+          const int kcoord = static_cast<int>((kb0 + kb) * BK);
+          if (AMODE == 0)
+            tma_load_2d(tc::smem_u32(a_ring + s * A_TILE), &amap, tc::smem_u32(&full[s]), kcoord,
+                        m_tile * BM);
+          else
+            tma_load_2d(tc::smem_u32(a_ring + s * A_TILE), &amap, tc::smem_u32(&full[s]),
+                        m_tile * BM, kcoord);
+          if (BSTREAM)
+            tma_load_2d(tc::smem_u32(s_ring + s * K::S_TILE), &bmap, tc::smem_u32(&full[s]), 0,
+                        kcoord);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    int64_t g = 0;
+    for (int t = 0; t < my_tiles; ++t) {
+      int m_tile, split, nkb;
+      tile_of(t, m_tile, split, nkb);
+      const int set = K::SETS == 2 ? (t & 1) : 0;
+      const int use = K::SETS == 2 ? (t >> 1) : t;  // how often this set was used before
+      if (use >= 1) tc::mbar_wait(&aempty[set], static_cast<uint32_t>((use - 1) & 1));
+      const uint32_t dset = tmem + K::D_BASE + set * K::SET_COLS;
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        const int ts = static_cast<int>(g % kTmemStages);
+        tc::mbar_wait(&conv[ts], static_cast<uint32_t>((g / kTmemStages) & 1));
+        tc::tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a_hi = tmem + ts * 2 * BK;
+          const uint32_t a_lo = a_hi + BK;
+          const uint32_t bt = tc::smem_u32(b_cat + (BSTREAM ? ts : kb) * K::B_TILE);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t d = dset + (kk % CH) * 2 * BN;
+            const uint64_t bdesc = sw128_desc(bt + kk * 32);
+            mma_tf32_ts(d, a_hi + kk * 8, bdesc, IDESC_HL, (kb > 0) || (kk >= CH));
+            mma_tf32_ts(d + BN, a_lo + kk * 8, bdesc, IDESC_L, 1);
+          }
+          tc::mma_commit(&tempty[ts]);
+          if (kb == nkb - 1) tc::mma_commit(&afull[set]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- converters + epilogue ----------------
+    const int ct = tid - 64;       // 0..127
+    const int lane_q = warp & 3;   // TMEM lane quarter of this warp
+    const int row = lane_q * 32 + (tid & 31);  // tile row = TMEM lane
+    const uint32_t lane_bits = static_cast<uint32_t>(lane_q * 32) << 16;
+    int64_t g = 0;
+    for (int t = 0; t < my_tiles; ++t) {
+      int m_tile, split, nkb;
+      tile_of(t, m_tile, split, nkb);
+      for (int kb = 0; kb < nkb; ++kb, ++g) {
+        const int s = static_cast<int>(g % ns);
+        const int ts = static_cast<int>(g % kTmemStages);
+        tc::mbar_wait(&full[s], static_cast<uint32_t>((g / ns) & 1));
+        const char* at = a_ring + s * A_TILE;
+        uint32_t hi[BK], lo[BK];
+        if (AMODE == 0) {
+#pragma unroll
+          for (int c = 0; c < BK / 4; ++c) {
+            const float4 v = *reinterpret_cast<const float4*>(
+                at + row * 128 + ((c ^ (row & 7)) << 4));
+            const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float h = tc::to_tf32(x[j]);
+              hi[4 * c + j] = __float_as_uint(h);
+              lo[4 * c + j] = __float_as_uint(x[j] - h);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < BK; ++kk) {
+            const float x = *reinterpret_cast<const float*>(at + kk * (BM * 4) + row * 4);
+            const float h = tc::to_tf32(x);
+            hi[kk] = __float_as_uint(h);
+            lo[kk] = __float_as_uint(x - h);
+          }
+        }
+        // The TMEM stage (and the streamed-B slot) was consumed by MMA g - stages.
+        if (g >= kTmemStages)
+          tc::mbar_wait(&tempty[ts], static_cast<uint32_t>(((g / kTmemStages) - 1) & 1));
+        tc::tc_fence_after();
+        if (BSTREAM) {
+          // Raw S k-block [32 k][BN j] → K-major [B_hi; B_lo] rows j / BN + j.
+          const char* st = s_ring + s * K::S_TILE;
+          char* bt = b_cat + ts * K::B_TILE;
+#pragma unroll
+          for (int i = 0; i < (BN * BK) / kConv; ++i) {
+            const int e = i * kConv + ct;
+            const int kk = e / BN, j = e % BN;
+            const float x = *reinterpret_cast<const float*>(st + (kk * BN + j) * 4);
+            const float h = tc::to_tf32(x);
+            *reinterpret_cast<float*>(bt + sw128_off(j, kk)) = h;
+            *reinterpret_cast<float*>(bt + sw128_off(BN + j, kk)) = x - h;
+          }
+          tc::fence_proxy_async_smem();
+        }
+        const uint32_t a_hi = tmem + lane_bits + ts * 2 * BK;
+        tmem_st32(a_hi, hi);
+        tmem_st32(a_hi + BK, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc::tc_fence_before();
+        __syncwarp();
+        if ((tid & 31) == 0) {
+          mbar_arrive(&sempty[s]);
+          mbar_arrive(&conv[ts]);
+        }
+
+        if (kb == nkb - 1) {
+          // Tile finished: drain the accumulator set.
+          const int set = K::SETS == 2 ? (t & 1) : 0;
+          const int use = K::SETS == 2 ? (t >> 1) : t;
+          tc::mbar_wait(&afull[set], static_cast<uint32_t>(use & 1));
+          tc::tc_fence_after();
+          const int64_t r = static_cast<int64_t>(m_tile) * BM + row;
+          const uint32_t base = tmem + lane_bits + K::D_BASE + set * K::SET_COLS;
+#pragma unroll 1
+          for (int cb = 0; cb < BN / 16; ++cb) {
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.f;
+#pragma unroll 1
+            for (int c = 0; c < CH; ++c) {
+              float w[16], u[16];
+              tc::tmem_ld16(base + c * 2 * BN + cb * 16, w);
+              tc::tmem_ld16(base + c * 2 * BN + BN + cb * 16, u);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] += w[j] + u[j];
+            }
+            if (r < p.m) {
+              if (p.partial) {
+                float* dst = p.partial + (static_cast<int64_t>(split) * p.m + r) * p.n;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                  const int64_t c = cb * 16 + j;
+                  if (c < p.n) dst[c] = v[j];
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                  const int64_t c = cb * 16 + j;
+                  if (c < p.n) p.C[r * p.ldc + c] = epilogue_value(p, r, c, v[j]);
+                }
+              }
+            }
+          }
+          tc::tc_fence_before();
+          __syncwarp();
+          if ((tid & 31) == 0) mbar_arrive(&aempty[set]);
+        }
+      }
+    }
+  }
+
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+// Deterministic split-K fold: C = epilogue((acc ? C : 0) + sum_s partial[s]).
+__global__ void tm_reduce_kernel(const TmParams p, int splits) {
+  const int64_t total = p.m * p.n;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / p.n, c = e % p.n;
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += p.partial[static_cast<int64_t>(z) * total + e];
+    p.C[r * p.ldc + c] = epilogue_value(p, r, c, s);
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult r;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r) != cudaSuccess ||
+        r != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return static_cast<EncodeTiledFn>(nullptr);
+    }
+    return reinterpret_cast<EncodeTiledFn>(q);
+  }();
+  return fn;
+}
+
+bool encode_2d(CUtensorMap* map, const float* base, uint64_t inner, uint64_t outer,
+               uint64_t stride_elems, uint32_t box_inner, uint32_t box_outer, bool swizzle128) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {stride_elems * 4};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, int AMODE, bool BSTREAM>
+void launch_tm(const CUtensorMap& amap, const CUtensorMap& bmap, const TmParams& p, int grid,
+               cudaStream_t s) {
+  using K = Cfg<BN>;
+  const size_t fixed = 1024 + static_cast<size_t>(BSTREAM ? kTmemStages : p.nkb_res) * K::B_TILE +
+                       (3 * kMaxStages + 4 * kTmemStages + 8) * 8;
+  const size_t per_stage = A_TILE + (BSTREAM ? K::S_TILE : 0);
+  int ns = static_cast<int>((227 * 1024 - fixed) / per_stage);
+  if (ns > kMaxStages) ns = kMaxStages;
+  const size_t smem = fixed + static_cast<size_t>(ns) * per_stage;
+  auto kfn = gemm_tm_kernel<BN, AMODE, BSTREAM>;
+  static std::atomic<uint64_t> configured{0};
+  const uint64_t bit = 1ull << (current_device() & 63);
+  if (!(configured.load() & bit)) {
+    CG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    configured.fetch_or(bit);
+  }
+  kfn<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(amap, bmap, p, ns);
+  CG_LAUNCH_CHECK();
+}
+
+template <int AMODE, bool BSTREAM>
+void launch_bn(int bn, const CUtensorMap& amap, const CUtensorMap& bmap, const TmParams& p,
+               int grid, cudaStream_t s) {
+  switch (bn) {
+    case 16: return launch_tm<16, AMODE, BSTREAM>(amap, bmap, p, grid, s);
+    case 32: return launch_tm<32, AMODE, BSTREAM>(amap, bmap, p, grid, s);
+    case 48: return launch_tm<48, AMODE, BSTREAM>(amap, bmap, p, grid, s);
+    default: return launch_tm<64, AMODE, BSTREAM>(amap, bmap, p, grid, s);
+  }
+}
+
+bool aligned16(const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; }
+
+}  // namespace
+
+bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
+  if (d.m <= 0 || d.n <= 0 || d.k <= 0 || d.n > 64) return false;
+  if (!aligned16(d.A)) return false;
+  const int bn = d.n <= 16 ? 16 : d.n <= 32 ? 32 : d.n <= 48 ? 48 : 64;
+  const int sms = num_sms(current_device());
+  const int64_t m_tiles = ceil_div64(d.m, BM);
+
+  TmParams p{};
+  p.m = d.m;
+  p.n = d.n;
+  p.k = d.k;
+  p.B = d.B;
+  p.b_sk = d.b_sk;
+  p.b_sn = d.b_sn;
+  p.C = d.C;
+  p.ldc = d.ldc;
+  p.accumulate = d.accumulate ? 1 : 0;
+  p.epilogue = d.epilogue;
+  p.aux = d.aux;
+  p.ldaux = d.ldaux;
+  p.aux_out = d.aux_out;
+  p.ldao = d.ldao;
+  p.m_tiles = static_cast<int>(m_tiles);
+
+  CUtensorMap amap, bmap;
+  std::memset(&bmap, 0, sizeof(bmap));
+  const bool a_k = d.a_sk == 1 && d.a_sm % 4 == 0 && d.a_sm >= d.k;
+  const bool a_m = d.a_sm == 1 && d.a_sk % 4 == 0 && d.a_sk >= d.m;
+  const bool b_stream_ok = d.b_sn == 1 && d.b_sk % 4 == 0 && aligned16(d.B) && d.b_sk >= d.n;
+
+  if (a_k) {
+    // T·W / S·Wᵀ: W resident, no split (K is a feature width).
+    const int nkb = static_cast<int>(ceil_div64(d.k, BK));
+    if (static_cast<int64_t>(nkb) * 2 * bn * BK * 4 > kMaxResidentB) return false;
+    if (!encode_2d(&amap, d.A, static_cast<uint64_t>(d.k), static_cast<uint64_t>(d.m),
+                   static_cast<uint64_t>(d.a_sm), BK, BM, true))
+      return false;
+    p.nkb_res = nkb;
+    p.k_chunk = static_cast<int64_t>(nkb) * BK;
+    const int grid = static_cast<int>(m_tiles < sms ? m_tiles : sms);
+    launch_bn<0, false>(bn, amap, bmap, p, grid, stream);
+    return true;
+  }
+  if (a_m && b_stream_ok) {
+    // Hᵀ·S: K = graph rows, split across CTAs, S streamed with H.
+    if (!encode_2d(&amap, d.A, static_cast<uint64_t>(d.m), static_cast<uint64_t>(d.k),
+                   static_cast<uint64_t>(d.a_sk), BM, BK, false))
+      return false;
+    if (!encode_2d(&bmap, d.B, static_cast<uint64_t>(d.n), static_cast<uint64_t>(d.k),
+                   static_cast<uint64_t>(d.b_sk), static_cast<uint32_t>(bn), BK, false))
+      return false;
+    const int64_t kblocks = ceil_div64(d.k, BK);
+    int64_t splits = ceil_div64(sms, m_tiles);
+    if (splits > kblocks) splits = kblocks;
+    if (splits < 1) splits = 1;
+    p.k_chunk = ceil_div64(kblocks, splits) * BK;
+    splits = ceil_div64(d.k, p.k_chunk);
+    float* work = nullptr;
+    if (splits > 1) {
+      CG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&work),
+                              static_cast<size_t>(splits) * d.m * d.n * sizeof(float), stream));
+      p.partial = work;
+    }
+    const int64_t tiles = m_tiles * splits;
+    const int grid = static_cast<int>(tiles < sms ? tiles : sms);
+    launch_bn<1, true>(bn, amap, bmap, p, grid, stream);
+    if (splits > 1) {
+      const int64_t total = d.m * d.n;
+      const int blocks = static_cast<int>(ceil_div64(total, 256) < 4 * sms ? ceil_div64(total, 256) : 4 * sms);
+      tm_reduce_kernel<<<blocks, 256, 0, stream>>>(p, static_cast<int>(splits));
+      CG_LAUNCH_CHECK();
+      CG_CUDA(cudaFreeAsync(work, stream));
+    }
+    return true;
+  }
+  return false;
+}
+
+}  // namespace kern
+}  // namespace cagnet

@@ -50,6 +50,10 @@ void gemm_tf32x3(const GemmDesc& d, cudaStream_t stream);
 // Persistent TMA-fed variant for row-major A (16 B rows), N <= 64 and a B that
 // fits in shared memory; returns false (nothing launched) when not applicable.
 bool gemm_tma_try(const GemmDesc& d, cudaStream_t stream);
+// A-in-TMEM variant (gemm_tm.cu): row-major A with B resident (T·W, S·Wᵀ) or
+// M-contiguous A with B streamed and split-K (Hᵀ·S); N <= 64.  Returns false
+// (nothing launched) when the shape or layout does not apply.
+bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream);
 
 // ---- K3: fused elementwise ----------------------------------------------------
 // log_softmax_rows + nll_tile (dense.cpp:94-136) over full rows of Z; writes

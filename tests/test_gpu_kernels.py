@@ -116,16 +116,56 @@ def test_gemm_split_tf32(cg, orc, torch, m, n, k, ta, tb, acc):
     assert rel(got, want) < 2e-6, rel(got, want)
 
 
-def test_gemm_epilogues(cg, orc, torch):
+# Padded (16 B-aligned) leading dimensions, as the trainers lay tiles out:
+# these take the TMA-fed A-in-TMEM kernel (gemm_tm.cu), including the
+# streamed-B split-K path of Hᵀ·S and multi-tile persistent CTAs.
+TM_CASES = [
+    # (m, n, k, ta, tb)
+    (40000, 16, 602, 0, 0),    # T·W, Reddit layer 1 (many tiles per CTA)
+    (3000, 41, 16, 0, 0),      # T·W, output layer (BN = 48)
+    (3000, 16, 41, 0, 1),      # S·Wᵀ
+    (1000, 64, 130, 0, 0),     # BN = 64
+    (777, 32, 70, 0, 0),       # ragged M tile, BN = 32
+    (602, 16, 20000, 1, 0),    # Hᵀ·S split-K, 5 M tiles
+    (16, 41, 30000, 1, 0),     # Hᵀ·S, m < 128 (OOB-filled tile), BN = 48
+    (300, 24, 12345, 1, 0),    # ragged K
+    (16, 16, 100, 1, 0),       # K smaller than one k-block per split
+]
+
+
+@pytest.mark.parametrize("m,n,k,ta,tb", TM_CASES)
+@pytest.mark.parametrize("acc", [0, 1])
+def test_gemm_padded_ld(cg, orc, torch, m, n, k, ta, tb, acc):
+    rng = np.random.default_rng(m * 13 + n * 5 + k)
+    a = rng.standard_normal((k, m) if ta else (m, k))
+    b = rng.standard_normal((n, k) if tb else (k, n))
+    c0 = rng.standard_normal((m, n)) if acc else np.zeros((m, n))
+    want = c0 + orc.gemm(a, b, bool(ta), bool(tb))
+    lda = (a.shape[1] + 3) // 4 * 4
+    ldb = (b.shape[1] + 3) // 4 * 4
+    ldc = (n + 3) // 4 * 4
+    A = padded(torch, a, lda)
+    B = padded(torch, b, ldb)
+    Cm = padded(torch, c0, ldc)
+    cg.check(cg.lib.cagnet_gemm_f32(ta, tb, m, n, k, A.data_ptr(), lda, B.data_ptr(), ldb,
+                                    Cm.data_ptr(), ldc, acc, 0, None, 0, None, 0, stream(torch)))
+    torch.cuda.synchronize()
+    got = Cm.cpu().numpy()[:, :n]
+    assert rel(got, want) < 2e-6, rel(got, want)
+
+
+@pytest.mark.parametrize("pad", [False, True])
+def test_gemm_epilogues(cg, orc, torch, pad):
     rng = np.random.default_rng(4)
     m, n, k = 777, 16, 41
     a = rng.standard_normal((m, k))
     w = rng.standard_normal((k, n))
     z = orc.gemm(a, w)
-    A, W = dev(torch, a.astype(np.float32)), dev(torch, w.astype(np.float32))
+    lda = 44 if pad else k
+    A, W = padded(torch, a, lda), dev(torch, w.astype(np.float32))
     Z = torch.zeros((m, n), device="cuda")
     H = torch.zeros((m, n), device="cuda")
-    cg.check(cg.lib.cagnet_gemm_f32(0, 0, m, n, k, A.data_ptr(), k, W.data_ptr(), n, Z.data_ptr(), n,
+    cg.check(cg.lib.cagnet_gemm_f32(0, 0, m, n, k, A.data_ptr(), lda, W.data_ptr(), n, Z.data_ptr(), n,
                                     0, 1, None, 0, H.data_ptr(), n, stream(torch)))
     torch.cuda.synchronize()
     assert rel(Z.cpu().numpy(), z) < 2e-6
