@@ -88,6 +88,19 @@ CAGNET_API int cagnet_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t nnz, 
                         const int32_t* col_idx, const float* vals, const float* H, int64_t ldh,
                         int32_t f, float* T, int64_t ldt, int accumulate, void* stream);
 
+/* spmm (csr.cpp:181-185) fused with the next dense step of the GCN layer, for
+ * f <= 32 and 16 B-aligned rows (ldh, ldt multiples of 4): t = A·H (row by
+ * row, in registers); raw_out (optional) = t; z = W ? t·W : t with W f x fo
+ * (element (k, c) at W[k*w_sk + c*w_sn], fo <= 64; gemm, dense.cpp:37-70);
+ * z *= 1[mask > 0] when mask (hadamard with relu_prime, dense.cpp:72-92);
+ * T = z; relu_out (optional) = relu(z) (dense.cpp:72-80). */
+CAGNET_API int cagnet_spmm_fused_f32(int64_t n_rows, int64_t n_cols, int64_t nnz,
+                          const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
+                          const float* H, int64_t ldh, int32_t f, const float* W, int64_t w_sk,
+                          int64_t w_sn, int32_t fo, const float* mask, int64_t mask_ld, float* T,
+                          int64_t ldt, float* relu_out, int64_t relu_ld, float* raw_out,
+                          int64_t raw_ld, void* stream);
+
 /* gemm_add / gemm (dense.cpp:37-70; dense.hpp:63-71): C (+)= op(A) op(B) on
  * tcgen05 tensor cores, split-TF32 (3 MMAs: hi*hi + hi*lo + lo*hi), fp32
  * accumulation in TMEM.  op(A) is m x k, op(B) is k x n; A is stored

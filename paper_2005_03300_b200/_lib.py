@@ -54,6 +54,8 @@ SIGNATURES = {
     "cagnet_grid_group": [i32, i32, i32, i32, i32, _i32p, C.POINTER(i32)],
     "cagnet_tile_geometry": [i32, i32, i32, i64, i32, i64, _i64p],
     "cagnet_spmm_csr_f32": [i64, i64, i64, vp, vp, vp, vp, i64, i32, vp, i64, i32, vp],
+    "cagnet_spmm_fused_f32": [i64, i64, i64, vp, vp, vp, vp, i64, i32, vp, i64, i64, i32, vp, i64,
+                              vp, i64, vp, i64, vp, i64, vp],
     "cagnet_gemm_f32": [i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, i32, vp, i64,
                         vp, i64, vp],
     "cagnet_logsoftmax_nll_f32": [vp, i64, i32, i64, i32, i32, vp, i64, vp, i64, vp, vp, i64,

@@ -57,6 +57,9 @@ class Strategy:
     # Extension (not in the reference): narrow-first propagation Aᵀ(H W) for
     # layers with f_out < f_in on the block-row strategies (1D / 1.5D).
     reassociate: bool = False
+    # Fused SpMM row epilogues (1D): 0 = off, 1 = ReLU / ⊙relu′ inside the
+    # SpMM (default), 2 = also the small dense T·W / S·Wᵀ transforms.
+    fuse: int = 1
 
     @property
     def kind_id(self) -> int:
@@ -326,6 +329,7 @@ class Trainer:
         self.dims = [int(d) for d in dims]
         if strat.reassociate:
             check(lib.cagnet_trainer_set_option(self.h, b"reassociate", 1))
+        check(lib.cagnet_trainer_set_option(self.h, b"fuse", int(strat.fuse)))
 
     # lifecycle -------------------------------------------------------------
     def distribute(self):

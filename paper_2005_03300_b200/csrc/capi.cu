@@ -147,6 +147,39 @@ int cagnet_spmm_csr_f32(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64
   });
 }
 
+int cagnet_spmm_fused_f32(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* row_ptr,
+                          const int32_t* col_idx, const float* vals, const float* H, int64_t ldh,
+                          int32_t f, const float* W, int64_t w_sk, int64_t w_sn, int32_t fo,
+                          const float* mask, int64_t mask_ld, float* T, int64_t ldt,
+                          float* relu_out, int64_t relu_ld, float* raw_out, int64_t raw_ld,
+                          void* stream) {
+  return guarded([&] {
+    cagnet::require(n_rows >= 0 && n_cols >= 0 && nnz >= 0 && f >= 0, "spmm_fused: negative shape");
+    cagnet::require(f <= cagnet::kern::kSpmmEpiMaxF, "spmm_fused: f > 32");
+    const int32_t width = W ? fo : f;
+    cagnet::require(!W || (fo > 0 && fo <= cagnet::kern::kSpmmEpiMaxFo), "spmm_fused: fo outside [1, 64]");
+    cagnet::require(ldh >= f && ldt >= width, "spmm_fused: leading dimension too small");
+    cagnet::require(!mask || mask_ld >= width, "spmm_fused: mask leading dimension too small");
+    cagnet::require(!relu_out || relu_ld >= width, "spmm_fused: relu_out leading dimension too small");
+    cagnet::require(!raw_out || raw_ld >= f, "spmm_fused: raw_out leading dimension too small");
+    cagnet::require(n_rows == 0 || (row_ptr && T), "spmm_fused: null row_ptr or output");
+    cagnet::require(nnz == 0 || (col_idx && vals && H), "spmm_fused: null input arrays");
+    cagnet::kern::SpmmEpi e;
+    e.W = W;
+    e.w_sk = w_sk;
+    e.w_sn = w_sn;
+    e.fo = W ? fo : 0;
+    e.mask = mask;
+    e.mask_ld = mask_ld;
+    e.relu_out = relu_out;
+    e.relu_ld = relu_ld;
+    e.raw_out = raw_out;
+    e.raw_ld = raw_ld;
+    cagnet::kern::spmm_csr(n_rows, row_ptr, col_idx, vals, H, ldh, f, T, ldt, false,
+                           as_stream(stream), nnz, &e);
+  });
+}
+
 int cagnet_gemm_f32(int ta, int tb, int64_t m, int64_t n, int64_t k, const float* A, int64_t lda,
                     const float* B, int64_t ldb, float* C, int64_t ldc, int accumulate, int epilogue,
                     const float* aux, int64_t ldaux, float* aux_out, int64_t ldao, void* stream) {
@@ -585,6 +618,8 @@ int cagnet_trainer_set_option(cagnet_trainer_t t, const char* name, int64_t valu
       t->t->set_reassociate(value != 0);
     else if (n == "timing")
       t->t->set_timing(value != 0);
+    else if (n == "fuse")
+      t->t->set_fuse(static_cast<int>(value));
     else
       throw std::invalid_argument("trainer option: unknown option '" + n + "'");
   });

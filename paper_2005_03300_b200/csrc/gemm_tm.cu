@@ -22,15 +22,18 @@
 //   warp 0      TMA producer: A tile (+ S tile when streamed) per k-block;
 //   warp 1      MMA issuer (one elected lane), TMEM allocator;
 //   warps 2-5   converters (TMA smem → hi/lo → TMEM; streamed B → [hi; lo]
-//               smem tile), then the epilogue of each finished tile
-//               (tcgen05.ld of the accumulator chains, fused ReLU / ⊙relu′ /
-//               accumulate, or the split-K partial).
+//               smem tile);
+//   warps 6-9   epilogue of each finished tile: tcgen05.ld of the accumulator
+//               chains → a staged smem tile → coalesced row-major stores with
+//               the fused ReLU / ⊙relu′ / accumulate (or the split-K partial),
+//               so conversion of tile t+1 never waits for tile t's stores.
 // Accumulator chains (k-step kk → chain kk % CH) keep several independent
 // MMAs in flight; two accumulator sets overlap tile t's epilogue with tile
 // t+1's MMAs when TMEM allows.
 #include <cuda.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -43,24 +46,33 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;
-constexpr int kConv = 128;
-constexpr int kThreads = 64 + kConv;
+constexpr int kConv = 128;                // converter threads (warps 2-5)
+constexpr int kEpi = 128;                 // epilogue threads (warps 6-9)
+constexpr int kThreads = 64 + kConv + kEpi;
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr int kMaxStages = 8;
-constexpr int kTmemStages = 4;            // A (hi + lo) stages in TMEM
+constexpr int kMaxTmemStages = 8;         // A (hi + lo) stages in TMEM (upper bound)
 constexpr int kMaxResidentB = 96 * 1024;  // bytes of resident [B_hi; B_lo]
 
-template <int BN>
+// TMEM budget (512 columns): accumulator sets x chains x 2 BN, the rest holds
+// A stages of 64 columns (hi + lo).  The split-K Hᵀ·S kernel has one tile per
+// CTA, so one accumulator set and deeper A staging (the MMA-completion round
+// trip, not bandwidth, bounds a shallow ring).
+template <int BN, bool BSTREAM>
 struct Cfg {
   static constexpr int CH = BN <= 16 ? 4 : BN <= 48 ? 2 : 1;       // accumulator chains
-  static constexpr int SETS = (BN == 48) ? 1 : 2;                  // accumulator sets
+  static constexpr int SETS = (BSTREAM || BN == 48) ? 1 : 2;       // accumulator sets
   static constexpr uint32_t SET_COLS = CH * 2 * BN;
-  static constexpr uint32_t A_COLS = kTmemStages * 2 * BK;         // hi + lo per stage
+  static constexpr int TS_FIT = (512 - SETS * SET_COLS) / (2 * BK);
+  static constexpr int TSTAGES = TS_FIT > kMaxTmemStages ? kMaxTmemStages : TS_FIT;
+  static constexpr uint32_t A_COLS = TSTAGES * 2 * BK;             // hi + lo per stage
   static constexpr uint32_t D_BASE = A_COLS;
   static constexpr uint32_t COLS = A_COLS + SETS * SET_COLS;
-  static_assert(COLS <= 512, "TMEM budget");
+  static_assert(COLS <= 512 && TSTAGES >= 2, "TMEM budget");
   static constexpr uint32_t B_TILE = 2 * BN * BK * 4;              // [hi; lo] k-block
   static constexpr uint32_t S_TILE = BN * BK * 4;                  // raw streamed S k-block
+  static constexpr int EP_LD = BN + 4;                             // staged output row (floats)
+  static constexpr uint32_t EP_BYTES = BM * EP_LD * 4;
 };
 
 struct TmParams {
@@ -79,6 +91,8 @@ struct TmParams {
   int64_t k_chunk;  // K per split (multiple of BK)
   int nkb_res;      // k-blocks of resident B (0 when streamed)
   int m_tiles;
+  int chains;       // accumulator chains in use (1 for short K: nothing to overlap)
+  int dbg;          // timing experiments only (CAGNET_GEMM_DBG): 1 skip st, 2 skip mma, 4 skip epi stores
 };
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -161,8 +175,8 @@ template <int BN, int AMODE, bool BSTREAM>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    const TmParams p, int ns) {
-  using K = Cfg<BN>;
-  constexpr int CH = K::CH;
+  using K = Cfg<BN, BSTREAM>;
+  constexpr int kTmemStages = K::TSTAGES;
   constexpr uint32_t IDESC_HL = tc::idesc_tf32(BM, 2 * BN, 0, 0);  // A_hi · [B_hi; B_lo]
   constexpr uint32_t IDESC_L = tc::idesc_tf32(BM, BN, 0, 0);       // A_lo · B_hi
   constexpr int SB = kTmemStages;  // streamed [hi; lo] B stages (recycled with the TMEM stage)
@@ -173,7 +187,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   char* s_ring = a_ring + ns * A_TILE;                  // ns x S_TILE (streamed B raw)
   char* b_cat = s_ring + (BSTREAM ? ns * K::S_TILE : 0);  // resident nkb or SB stages
   const int b_slots = BSTREAM ? SB : p.nkb_res;
-  uint64_t* full = reinterpret_cast<uint64_t*>(b_cat + b_slots * K::B_TILE);
+  float* ep = reinterpret_cast<float*>(b_cat + b_slots * K::B_TILE);  // [BM][EP_LD]
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(ep) + K::EP_BYTES);
   uint64_t* sempty = full + kMaxStages;       // smem stage read by the converters
   uint64_t* conv = sempty + kMaxStages;       // [kTmemStages] TMEM A stage written
   uint64_t* tempty = conv + kTmemStages;      // [kTmemStages] TMEM A stage consumed by MMA
@@ -195,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&afull[i], 1);
-      tc::mbar_init(&aempty[i], kConv / 32);
+      tc::mbar_init(&aempty[i], kEpi / 32);
     }
     tc::fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap)) : "memory");
@@ -287,9 +302,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t bt = tc::smem_u32(b_cat + (BSTREAM ? ts : kb) * K::B_TILE);
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t d = dset + (kk % CH) * 2 * BN;
+            if (p.dbg & 2) break;
+            const int ch = kk % p.chains;
+            const uint32_t d = dset + ch * 2 * BN;
             const uint64_t bdesc = sw128_desc(bt + kk * 32);
-            mma_tf32_ts(d, a_hi + kk * 8, bdesc, IDESC_HL, (kb > 0) || (kk >= CH));
+            mma_tf32_ts(d, a_hi + kk * 8, bdesc, IDESC_HL, (kb > 0) || (kk >= p.chains));
             mma_tf32_ts(d + BN, a_lo + kk * 8, bdesc, IDESC_L, 1);
           }
           tc::mma_commit(&tempty[ts]);
@@ -298,8 +315,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
-  } else {
-    // ---------------- converters + epilogue ----------------
+  } else if (warp < 6) {
+    // ---------------- converters ----------------
     const int ct = tid - 64;       // 0..127
     const int lane_q = warp & 3;   // TMEM lane quarter of this warp
     const int row = lane_q * 32 + (tid & 31);  // tile row = TMEM lane
@@ -356,59 +373,101 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::fence_proxy_async_smem();
         }
         const uint32_t a_hi = tmem + lane_bits + ts * 2 * BK;
-        tmem_st32(a_hi, hi);
-        tmem_st32(a_hi + BK, lo);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if (!(p.dbg & 1)) {
+          tmem_st32(a_hi, hi);
+          tmem_st32(a_hi + BK, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        } else if (hi[0] == 0x7fffffffu && lo[0] == 1u) {
+          ep[0] = 1.f;  // keep the conversion live
+        }
         tc::tc_fence_before();
         __syncwarp();
         if ((tid & 31) == 0) {
           mbar_arrive(&sempty[s]);
           mbar_arrive(&conv[ts]);
         }
-
-        if (kb == nkb - 1) {
-          // Tile finished: drain the accumulator set.
-          const int set = K::SETS == 2 ? (t & 1) : 0;
-          const int use = K::SETS == 2 ? (t >> 1) : t;
-          tc::mbar_wait(&afull[set], static_cast<uint32_t>(use & 1));
-          tc::tc_fence_after();
-          const int64_t r = static_cast<int64_t>(m_tile) * BM + row;
-          const uint32_t base = tmem + lane_bits + K::D_BASE + set * K::SET_COLS;
+      }
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const int et = tid - 64 - kConv;  // 0..127
+    const int lane_q = warp & 3;
+    const int row = lane_q * 32 + (tid & 31);
+    const uint32_t lane_bits = static_cast<uint32_t>(lane_q * 32) << 16;
+    const int n = static_cast<int>(p.n);
+    const int rpp = kEpi / n;          // rows per pass (n <= 64)
+    const int er = et / n, ec = et - er * n;
+    const bool ec_ok = er < rpp;
+    for (int t = 0; t < my_tiles; ++t) {
+      int m_tile, split, nkb;
+      tile_of(t, m_tile, split, nkb);
+      const int set = K::SETS == 2 ? (t & 1) : 0;
+      const int use = K::SETS == 2 ? (t >> 1) : t;
+      tc::mbar_wait(&afull[set], static_cast<uint32_t>(use & 1));
+      tc::tc_fence_after();
+      const uint32_t base = tmem + lane_bits + K::D_BASE + set * K::SET_COLS;
 #pragma unroll 1
-          for (int cb = 0; cb < BN / 16; ++cb) {
-            float v[16];
+      for (int cb = 0; cb < BN / 16; ++cb) {
+        float v[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
 #pragma unroll 1
-            for (int c = 0; c < CH; ++c) {
-              float w[16], u[16];
-              tc::tmem_ld16(base + c * 2 * BN + cb * 16, w);
-              tc::tmem_ld16(base + c * 2 * BN + BN + cb * 16, u);
+        for (int c = 0; c < p.chains; ++c) {
+          uint32_t w[16], u[16];
+          tc::tmem_ld16_nowait(base + c * 2 * BN + cb * 16, w);
+          tc::tmem_ld16_nowait(base + c * 2 * BN + BN + cb * 16, u);
+          tc::tmem_ld_wait();
 #pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] += w[j] + u[j];
+          for (int j = 0; j < 16; ++j) v[j] += __uint_as_float(w[j]) + __uint_as_float(u[j]);
+        }
+        float4* dst = reinterpret_cast<float4*>(ep + row * K::EP_LD + cb * 16);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+      // The accumulator set is free once it sits in shared memory.
+      tc::tc_fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&aempty[set]);
+      asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
+      // Coalesced row-major stores of the tile's valid rows: thread et owns
+      // column ec of rows er, er + rpp, ... (no per-element division); the
+      // loads of each batch of 4 rows are issued before their stores.
+      const int64_t r0 = static_cast<int64_t>(m_tile) * BM;
+      const int rows = static_cast<int>(p.m - r0 < BM ? p.m - r0 : BM);
+      if (ec_ok && !(p.dbg & 4)) {
+        if (p.partial) {
+          float* dst = p.partial + (static_cast<int64_t>(split) * p.m + r0) * p.n + ec;
+          for (int r = er; r < rows; r += rpp) dst[static_cast<int64_t>(r) * p.n] = ep[r * K::EP_LD + ec];
+        } else {
+          for (int rb = er; rb < rows; rb += 4 * rpp) {
+            float v[4], cold[4], ax[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = rb + i * rpp;
+              const int64_t gr = r0 + r;
+              const bool ok = r < rows;
+              v[i] = ok ? ep[r * K::EP_LD + ec] : 0.f;
+              cold[i] = (ok && p.accumulate) ? p.C[gr * p.ldc + ec] : 0.f;
+              ax[i] = (ok && p.epilogue == EPI_RELU_PRIME) ? p.aux[gr * p.ldaux + ec] : 1.f;
             }
-            if (r < p.m) {
-              if (p.partial) {
-                float* dst = p.partial + (static_cast<int64_t>(split) * p.m + r) * p.n;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                  const int64_t c = cb * 16 + j;
-                  if (c < p.n) dst[c] = v[j];
-                }
-              } else {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                  const int64_t c = cb * 16 + j;
-                  if (c < p.n) p.C[r * p.ldc + c] = epilogue_value(p, r, c, v[j]);
-                }
+            for (int i = 0; i < 4; ++i) {
+              const int r = rb + i * rpp;
+              if (r >= rows) break;
+              const int64_t gr = r0 + r;
+              float x = v[i] + cold[i];
+              if (p.epilogue == EPI_RELU) {
+                if (p.aux_out) p.aux_out[gr * p.ldao + ec] = x > 0.f ? x : 0.f;
+              } else if (p.epilogue == EPI_RELU_PRIME) {
+                x = ax[i] > 0.f ? x : x * 0.f;
               }
+              p.C[gr * p.ldc + ec] = x;
             }
           }
-          tc::tc_fence_before();
-          __syncwarp();
-          if ((tid & 31) == 0) mbar_arrive(&aempty[set]);
         }
       }
+      asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
     }
   }
 
@@ -418,14 +477,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // Deterministic split-K fold: C = epilogue((acc ? C : 0) + sum_s partial[s]).
+// One warp per output element: lane i sums splits i, i + 32, ... in order,
+// then a fixed xor tree — the same order on every run.
 __global__ void tm_reduce_kernel(const TmParams p, int splits) {
   const int64_t total = p.m * p.n;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = e / p.n, c = e % p.n;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t e = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; e < total;
+       e += warps) {
     float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += p.partial[static_cast<int64_t>(z) * total + e];
-    p.C[r * p.ldc + c] = epilogue_value(p, r, c, s);
+    for (int z = lane; z < splits; z += 32) s += p.partial[static_cast<int64_t>(z) * total + e];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      const int64_t r = e / p.n, c = e % p.n;
+      p.C[r * p.ldc + c] = epilogue_value(p, r, c, s);
+    }
   }
 }
 
@@ -465,9 +532,10 @@ bool encode_2d(CUtensorMap* map, const float* base, uint64_t inner, uint64_t out
 template <int BN, int AMODE, bool BSTREAM>
 void launch_tm(const CUtensorMap& amap, const CUtensorMap& bmap, const TmParams& p, int grid,
                cudaStream_t s) {
-  using K = Cfg<BN>;
+  using K = Cfg<BN, BSTREAM>;
+  constexpr int kTmemStages = K::TSTAGES;
   const size_t fixed = 1024 + static_cast<size_t>(BSTREAM ? kTmemStages : p.nkb_res) * K::B_TILE +
-                       (3 * kMaxStages + 4 * kTmemStages + 8) * 8;
+                       K::EP_BYTES + (3 * kMaxStages + 4 * kTmemStages + 8) * 8;
   const size_t per_stage = A_TILE + (BSTREAM ? K::S_TILE : 0);
   int ns = static_cast<int>((227 * 1024 - fixed) / per_stage);
   if (ns > kMaxStages) ns = kMaxStages;
@@ -506,6 +574,11 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
   const int64_t m_tiles = ceil_div64(d.m, BM);
 
   TmParams p{};
+  static const int dbg = [] {
+    const char* e = std::getenv("CAGNET_GEMM_DBG");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.dbg = dbg;
   p.m = d.m;
   p.n = d.n;
   p.k = d.k;
@@ -537,6 +610,7 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
       return false;
     p.nkb_res = nkb;
     p.k_chunk = static_cast<int64_t>(nkb) * BK;
+    p.chains = nkb >= 2 ? (bn <= 16 ? 4 : bn <= 48 ? 2 : 1) : 1;
     const int grid = static_cast<int>(m_tiles < sms ? m_tiles : sms);
     launch_bn<0, false>(bn, amap, bmap, p, grid, stream);
     return true;
@@ -550,11 +624,13 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
                    static_cast<uint64_t>(d.b_sk), static_cast<uint32_t>(bn), BK, false))
       return false;
     const int64_t kblocks = ceil_div64(d.k, BK);
-    int64_t splits = ceil_div64(sms, m_tiles);
+    // One tile per CTA, no second wave: floor(SMs / M tiles) splits.
+    int64_t splits = sms / m_tiles;
     if (splits > kblocks) splits = kblocks;
     if (splits < 1) splits = 1;
     p.k_chunk = ceil_div64(kblocks, splits) * BK;
     splits = ceil_div64(d.k, p.k_chunk);
+    p.chains = p.k_chunk / BK >= 2 ? (bn <= 16 ? 4 : bn <= 48 ? 2 : 1) : 1;
     float* work = nullptr;
     if (splits > 1) {
       CG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&work),
@@ -565,8 +641,8 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
     const int grid = static_cast<int>(tiles < sms ? tiles : sms);
     launch_bn<1, true>(bn, amap, bmap, p, grid, stream);
     if (splits > 1) {
-      const int64_t total = d.m * d.n;
-      const int blocks = static_cast<int>(ceil_div64(total, 256) < 4 * sms ? ceil_div64(total, 256) : 4 * sms);
+      const int64_t total = d.m * d.n;  // one warp per element
+      const int blocks = static_cast<int>(ceil_div64(total, 8) < 8 * sms ? ceil_div64(total, 8) : 8 * sms);
       tm_reduce_kernel<<<blocks, 256, 0, stream>>>(p, static_cast<int>(splits));
       CG_LAUNCH_CHECK();
       CG_CUDA(cudaFreeAsync(work, stream));

@@ -11,17 +11,40 @@ namespace cagnet {
 namespace kern {
 
 // ---- K1: CSR SpMM (csr.cpp:164-179) ---------------------------------------
+// Fused row epilogue of a final (non-accumulating) SpMM whose f <= 32: the
+// SpMM row t (f values, still in registers) optionally goes to raw_out, is
+// multiplied by a small dense W (f x fo, element (k, c) at W[k*w_sk + c*w_sn];
+// the next layer's T·W / the backward S·Wᵀ), masked by relu′ (z *= 1[mask >
+// 0], dense.cpp:72-92) and written to T (fo columns, or f without W); relu(z)
+// optionally goes to relu_out.  Replaces a GEMM launch and an elementwise pass
+// that would each re-read the n x f tile.
+struct SpmmEpi {
+  const float* W = nullptr;
+  int64_t w_sk = 0, w_sn = 0;
+  int fo = 0;
+  const float* mask = nullptr;
+  int64_t mask_ld = 0;
+  float* relu_out = nullptr;
+  int64_t relu_ld = 0;
+  float* raw_out = nullptr;
+  int64_t raw_ld = 0;
+};
+constexpr int kSpmmEpiMaxF = 32;
+constexpr int kSpmmEpiMaxFo = 64;
+
 // T[i, 0:f] = (accumulate ? T[i, 0:f] : 0) + sum_k vals[k] * H[col[k], 0:f]
 // with the nonzeros of each row folded in ascending order (the reference's
 // accumulation order), one fp32 FMA per term.
 // nnz (optional, -1 = unknown) sizes the row teams of the narrow-row kernel.
 void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
               const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
-              cudaStream_t stream, int64_t nnz = -1);
+              cudaStream_t stream, int64_t nnz = -1, const SpmmEpi* epi = nullptr);
+
 // Same, with row i's nonzeros given as [seg_begin[i], seg_end[i]).
 void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_end,
                    const int32_t* col_idx, const float* vals, const float* H, int64_t ldh, int f,
-                   float* T, int64_t ldt, bool accumulate, cudaStream_t stream, int64_t nnz = -1);
+                   float* T, int64_t ldt, bool accumulate, cudaStream_t stream, int64_t nnz = -1,
+                   const SpmmEpi* epi = nullptr);
 // split[b * rows + r] (b = 0..nb) = first nonzero of row r in column block b
 // of the ceiling-rule split of n_cols into nb blocks; split[nb * rows + r] = row end.
 void column_splits(int64_t rows, int64_t n_cols, int nb, const int64_t* row_ptr,

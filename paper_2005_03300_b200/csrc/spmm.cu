@@ -98,6 +98,7 @@ struct SpmmArgs {
   float* T;
   int64_t ldt;
   double mean_row_nnz;  // host-side hint for the row-team shape
+  SpmmEpi epi;          // fused row epilogue (EPI kernels only)
 };
 
 // VEC = 4: 16-byte vectors (requires 16 B aligned rows); VEC = 1: scalars.
@@ -303,13 +304,81 @@ void pick_shape(int nvec, int* lpr, int* vpl) {
   *vpl = best_v < 1 ? 1 : best_v;
 }
 
+// Fused epilogue (SpmmEpi) of a row team whose lanes all hold the reduced
+// row: lane vec has columns [4 vec, 4 vec + 4).  With W, team lane tl
+// computes output columns tl, tl + TEAM, ... as sum_k t_k W[k, c] in fp32
+// (t_k fetched by warp shuffles); every lane of the warp runs the shuffle
+// loop, rows past the end only skip the stores.
+template <int LV, int TEAM>
+__device__ __forceinline__ void spmm_row_epilogue(const SpmmArgs& a, int64_t row, int lane, int vec,
+                                                  int q, bool vec_ok, const float4& acc) {
+  const SpmmEpi& e = a.epi;
+  const bool live = row < a.n_rows;
+  const int f = a.f;
+  if (e.raw_out && live && q == 0 && vec_ok) store_vec(e.raw_out + row * e.raw_ld, vec, f, acc);
+  if (e.W == nullptr) {
+    if (!(live && q == 0 && vec_ok)) return;
+    float4 z = acc;
+    if (e.mask) {
+      const float4 m = load_vec(e.mask + row * e.mask_ld, vec, f);
+      z.x = m.x > 0.f ? z.x : z.x * 0.f;
+      z.y = m.y > 0.f ? z.y : z.y * 0.f;
+      z.z = m.z > 0.f ? z.z : z.z * 0.f;
+      z.w = m.w > 0.f ? z.w : z.w * 0.f;
+    }
+    store_vec(a.T + row * a.ldt, vec, f, z);
+    if (e.relu_out)
+      store_vec(e.relu_out + row * e.relu_ld, vec, f,
+                make_float4(fmaxf(z.x, 0.f), fmaxf(z.y, 0.f), fmaxf(z.z, 0.f), fmaxf(z.w, 0.f)));
+    return;
+  }
+  constexpr int SLOTS = (kSpmmEpiMaxFo + TEAM - 1) / TEAM;
+  const int tl = lane % TEAM;
+  const int base = lane - tl;
+  const int nvec = (f + 3) / 4;
+  float z[SLOTS];
+#pragma unroll
+  for (int i = 0; i < SLOTS; ++i) z[i] = 0.f;
+  for (int v4 = 0; v4 < nvec; ++v4) {
+    const int src = base + (v4 % LV);
+    float t[4];
+    t[0] = __shfl_sync(0xffffffffu, acc.x, src);
+    t[1] = __shfl_sync(0xffffffffu, acc.y, src);
+    t[2] = __shfl_sync(0xffffffffu, acc.z, src);
+    t[3] = __shfl_sync(0xffffffffu, acc.w, src);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = 4 * v4 + j;
+      if (k < f) {
+        const float* wk = e.W + k * e.w_sk;
+#pragma unroll
+        for (int i = 0; i < SLOTS; ++i) {
+          const int c = tl + i * TEAM;
+          if (c < e.fo) z[i] = fmaf(t[j], __ldg(wk + c * e.w_sn), z[i]);
+        }
+      }
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int i = 0; i < SLOTS; ++i) {
+    const int c = tl + i * TEAM;
+    if (c < e.fo) {
+      float v = z[i];
+      if (e.mask) v = e.mask[row * e.mask_ld + c] > 0.f ? v : v * 0.f;
+      a.T[row * a.ldt + c] = v;
+      if (e.relu_out) e.relu_out[row * e.relu_ld + c] = fmaxf(v, 0.f);
+    }
+  }
+}
+
 // Narrow rows (f <= 32): a team of QPR x LV lanes owns one output row; LV
 // lanes cover the row's float4 vectors and the QPR sub-teams stride over the
 // row's nonzeros (sub-team q takes q, q+QPR, ...), so every lane streams
 // independent gathers with no shuffles in the loop (U in flight); the QPR
 // partial sums are folded with xor shuffles at the end (deterministic order).
 template <int LV, int QPR, int U, bool ACC, bool TAIL, int NT = kThreads, int HINT = 0,
-          bool FULLV = false>
+          bool FULLV = false, bool EPI = false>
 __global__ void __launch_bounds__(NT, 1024 / NT) spmm_nzpar_kernel(const SpmmArgs a) {
   constexpr int TEAM = LV * QPR;
   constexpr int RPW = 32 / TEAM;
@@ -370,6 +439,10 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmm_nzpar_kernel(const SpmmArg
     acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
     acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
   }
+  if constexpr (EPI) {
+    spmm_row_epilogue<LV, TEAM>(a, row, lane, vec, q, vec_ok, acc);
+    return;
+  }
   if (row < a.n_rows && q == 0 && vec_ok) {
     float* trow = a.T + row * a.ldt;
     if (ACC) {
@@ -384,12 +457,19 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmm_nzpar_kernel(const SpmmArg
 }
 
 template <int LV, int QPR, int U, int NT, int HINT>
-void launch_nzpar_v(const SpmmArgs& a, bool acc, cudaStream_t s) {
+void launch_nzpar_v(const SpmmArgs& a, bool acc, bool epi, cudaStream_t s) {
   constexpr int rows_per_block = (NT / 32) * (32 / (LV * QPR));
   const unsigned g = static_cast<unsigned>(ceil_div64(a.n_rows, rows_per_block));
   const bool tail = (a.f % 4) != 0;
   const bool full = !tail && (a.f / 4) == LV;
-  if (acc) {
+  if (epi) {
+    if (tail)
+      spmm_nzpar_kernel<LV, QPR, U, false, true, NT, 0, false, true><<<g, NT, 0, s>>>(a);
+    else if (full)
+      spmm_nzpar_kernel<LV, QPR, U, false, false, NT, 0, true, true><<<g, NT, 0, s>>>(a);
+    else
+      spmm_nzpar_kernel<LV, QPR, U, false, false, NT, 0, false, true><<<g, NT, 0, s>>>(a);
+  } else if (acc) {
     if (tail)
       spmm_nzpar_kernel<LV, QPR, U, true, true, NT, 0><<<g, NT, 0, s>>>(a);
     else if (full)
@@ -420,28 +500,29 @@ int spmm_tune() {
 }
 
 template <int LV, int QPR>
-void launch_nzpar(const SpmmArgs& a, bool acc, cudaStream_t s) {
+void launch_nzpar(const SpmmArgs& a, bool acc, bool epi, cudaStream_t s) {
+  if (epi) return launch_nzpar_v<LV, QPR, 4, 128, 0>(a, false, true, s);
   switch (spmm_tune()) {
-    case 1: return launch_nzpar_v<LV, QPR, 4, kThreads, 0>(a, acc, s);
-    case 2: return launch_nzpar_v<LV, QPR, 4, 128, 1>(a, acc, s);
-    case 3: return launch_nzpar_v<LV, QPR, 8, 128, 0>(a, acc, s);
-    default: return launch_nzpar_v<LV, QPR, 4, 128, 0>(a, acc, s);
+    case 1: return launch_nzpar_v<LV, QPR, 4, kThreads, 0>(a, acc, false, s);
+    case 2: return launch_nzpar_v<LV, QPR, 4, 128, 1>(a, acc, false, s);
+    case 3: return launch_nzpar_v<LV, QPR, 8, 128, 0>(a, acc, false, s);
+    default: return launch_nzpar_v<LV, QPR, 4, 128, 0>(a, acc, false, s);
   }
 }
 
 template <int LV>
-void launch_nzpar_q(int qpr, const SpmmArgs& a, bool acc, cudaStream_t s) {
+void launch_nzpar_q(int qpr, const SpmmArgs& a, bool acc, bool epi, cudaStream_t s) {
   switch (qpr) {
-    case 1: return launch_nzpar<LV, 1>(a, acc, s);
-    case 2: if constexpr (LV <= 16) return launch_nzpar<LV, 2>(a, acc, s); break;
-    case 4: if constexpr (LV <= 8) return launch_nzpar<LV, 4>(a, acc, s); break;
-    default: if constexpr (LV <= 4) return launch_nzpar<LV, 8>(a, acc, s); break;
+    case 1: return launch_nzpar<LV, 1>(a, acc, epi, s);
+    case 2: if constexpr (LV <= 16) return launch_nzpar<LV, 2>(a, acc, epi, s); break;
+    case 4: if constexpr (LV <= 8) return launch_nzpar<LV, 4>(a, acc, epi, s); break;
+    default: if constexpr (LV <= 4) return launch_nzpar<LV, 8>(a, acc, epi, s); break;
   }
-  launch_nzpar<LV, 1>(a, acc, s);
+  launch_nzpar<LV, 1>(a, acc, epi, s);
 }
 
 template <int VEC>
-void dispatch(const SpmmArgs& a, bool acc, cudaStream_t s) {
+void dispatch(const SpmmArgs& a, bool acc, bool epi, cudaStream_t s) {
   const int nvec = (a.f + VEC - 1) / VEC;
   if (VEC == 4 && nvec <= 8) {
     // Sub-teams per row from the mean row length (8 nonzeros per sub-team
@@ -452,12 +533,13 @@ void dispatch(const SpmmArgs& a, bool acc, cudaStream_t s) {
     while (qpr > 1 && mean < 8.0 * qpr) qpr >>= 1;
     if (qpr > 8) qpr = 8;
     switch (lv) {
-      case 1: return launch_nzpar_q<1>(qpr, a, acc, s);
-      case 2: return launch_nzpar_q<2>(qpr, a, acc, s);
-      case 4: return launch_nzpar_q<4>(qpr, a, acc, s);
-      default: return launch_nzpar_q<8>(qpr, a, acc, s);
+      case 1: return launch_nzpar_q<1>(qpr, a, acc, epi, s);
+      case 2: return launch_nzpar_q<2>(qpr, a, acc, epi, s);
+      case 4: return launch_nzpar_q<4>(qpr, a, acc, epi, s);
+      default: return launch_nzpar_q<8>(qpr, a, acc, epi, s);
     }
   }
+  require(!epi, "spmm: fused epilogue needs f <= 32 and 16 B-aligned rows");
   int lpr, vpl;
   pick_shape(nvec, &lpr, &vpl);
   switch (lpr) {
@@ -497,29 +579,37 @@ __global__ void column_splits_kernel(int64_t rows, int nb, int64_t step,
 
 void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_end,
                    const int32_t* col_idx, const float* vals, const float* H, int64_t ldh, int f,
-                   float* T, int64_t ldt, bool accumulate, cudaStream_t stream, int64_t nnz) {
+                   float* T, int64_t ldt, bool accumulate, cudaStream_t stream, int64_t nnz,
+                   const SpmmEpi* epi) {
   if (n_rows <= 0 || f <= 0) return;
   const double mean = nnz >= 0 ? static_cast<double>(nnz) / static_cast<double>(n_rows) : 64.0;
   const bool aligned = (ldh % 4 == 0) && (ldt % 4 == 0) &&
                        (reinterpret_cast<uintptr_t>(H) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(T) % 16 == 0);
+  if (epi) {
+    require(!accumulate && aligned && f <= kSpmmEpiMaxF && epi->fo <= kSpmmEpiMaxFo,
+            "spmm: fused epilogue needs a final f <= 32 SpMM on 16 B-aligned rows");
+    SpmmArgs a{n_rows, seg_begin, seg_end, col_idx, vals, H, ldh, f, T, ldt, mean, *epi};
+    dispatch<4>(a, false, true, stream);
+    return;
+  }
   // Column chunks of at most 32 lanes * 8 vectors keep accumulators in registers.
   const int chunk = aligned ? 32 * 8 * 4 : 32 * 8;
   for (int c0 = 0; c0 < f; c0 += chunk) {
     SpmmArgs a{n_rows, seg_begin, seg_end, col_idx, vals, H + c0, ldh, f - c0 < chunk ? f - c0 : chunk,
-               T + c0, ldt, mean};
+               T + c0, ldt, mean, SpmmEpi{}};
     if (aligned)
-      dispatch<4>(a, accumulate, stream);
+      dispatch<4>(a, accumulate, false, stream);
     else
-      dispatch<1>(a, accumulate, stream);
+      dispatch<1>(a, accumulate, false, stream);
   }
 }
 
 void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
               const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
-              cudaStream_t stream, int64_t nnz) {
+              cudaStream_t stream, int64_t nnz, const SpmmEpi* epi) {
   spmm_segments(n_rows, row_ptr, row_ptr + 1, col_idx, vals, H, ldh, f, T, ldt, accumulate, stream,
-                nnz);
+                nnz, epi);
 }
 
 void column_splits(int64_t rows, int64_t n_cols, int nb, const int64_t* row_ptr,

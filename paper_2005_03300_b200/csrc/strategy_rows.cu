@@ -57,11 +57,20 @@ class TrainerRows final : public Trainer {
     const int64_t fout = dims_[static_cast<size_t>(l)];
     const Mat& h = h_[static_cast<size_t>(l - 1)].m;
     Mat z = z_[static_cast<size_t>(l - 1)].m;
+    const bool last = l + 1 == num_layers();
     if (reassociate_ && fout < fin) {
       // Narrow-first propagation: Z = Aᵀ (H W) — the same product as
       // (Aᵀ H) W, but the broadcast panels and the SpMM are f_out wide.
       Mat u = view(acc_, h.rows, fout);
       gemm_aw(h, l - 1, 0, 0, u, false, kern::EPI_NONE, Mat{});
+      if (!last && fusable(at_parts_, u)) {
+        // ReLU in the SpMM's row epilogue: Z and H_l in one pass.
+        kern::SpmmEpi e;
+        e.relu_out = h_[static_cast<size_t>(l)].m.p;
+        e.relu_ld = h_[static_cast<size_t>(l)].m.ld;
+        stages(at_parts_, u, z, &e);
+        return;
+      }
       stages(at_parts_, u, z);
       if (!one_d()) row_reduce(z);
       finish_layer(l, z);
@@ -77,6 +86,27 @@ class TrainerRows final : public Trainer {
       saved_t_[static_cast<size_t>(l)].alloc(h.rows, fin);
     Mat t = keep ? saved_t_[static_cast<size_t>(l)].m : view(acc_, h.rows, fin);
     saved_valid_[static_cast<size_t>(l)] = keep;
+    if (fuse_ >= 2 && fout <= kern::kSpmmEpiMaxFo && fusable(at_parts_, h)) {
+      // Z = (Aᵀ H) W_l in the SpMM's row epilogue (+ ReLU into H_l; the
+      // widening layer also keeps T for the narrow-first backward).
+      const Mat& w = W_[static_cast<size_t>(l - 1)].m;
+      kern::SpmmEpi e;
+      e.W = w.p;
+      e.w_sk = w.ld;
+      e.w_sn = 1;
+      e.fo = static_cast<int>(fout);
+      if (keep) {
+        e.raw_out = t.p;
+        e.raw_ld = t.ld;
+      }
+      if (!last) {
+        e.relu_out = h_[static_cast<size_t>(l)].m.p;
+        e.relu_ld = h_[static_cast<size_t>(l)].m.ld;
+      }
+      stages(at_parts_, h, z, &e);
+      if (last) finish_layer(l, z);
+      return;
+    }
     stages(at_parts_, h, t);
     if (!one_d()) row_reduce(t);
     if (l + 1 == num_layers()) {
@@ -116,16 +146,44 @@ class TrainerRows final : public Trainer {
           Mat gp = g_[static_cast<size_t>(l - 2)].m;
           Mat u = view(acc_, g.rows, dims_[static_cast<size_t>(l - 1)]);
           gemm_swt(g, l - 1, 0, 0, u, false, kern::EPI_NONE, nullptr);
+          const Mat& zp = z_[static_cast<size_t>(l - 2)].m;
+          if (fusable(a_parts_, u)) {
+            kern::SpmmEpi e;  // ⊙ relu′(Z_prev) in the SpMM's row epilogue
+            e.mask = zp.p;
+            e.mask_ld = zp.ld;
+            stages(a_parts_, u, gp, &e);
+            continue;
+          }
           stages(a_parts_, u, gp);
           if (!one_d()) row_reduce(gp);
-          const Mat& zp = z_[static_cast<size_t>(l - 2)].m;
           kern::mask_relu_prime(gp.p, gp.ld, zp.p, zp.ld, gp.rows, gp.cols, cs_);
         }
         continue;
       }
       Mat s = view(acc_, g.rows, dims_[static_cast<size_t>(l)]);
-      stages(a_parts_, g, s);
-      if (!one_d()) row_reduce(s);
+      const int64_t fprev = dims_[static_cast<size_t>(l - 1)];
+      bool fused = false;
+      if (fuse_ >= 2 && l >= 2 && fprev <= kern::kSpmmEpiMaxFo && fusable(a_parts_, g)) {
+        // G_prev = (S Wᵀ) ⊙ relu′(Z_prev) in the SpMM's row epilogue; S itself
+        // still lands in `s` for Y = Hᵀ S.
+        const Mat& w = W_[static_cast<size_t>(l - 1)].m;
+        const Mat& zp = z_[static_cast<size_t>(l - 2)].m;
+        Mat gp = g_[static_cast<size_t>(l - 2)].m;
+        kern::SpmmEpi e;
+        e.W = w.p;
+        e.w_sk = 1;
+        e.w_sn = w.ld;
+        e.fo = static_cast<int>(fprev);
+        e.mask = zp.p;
+        e.mask_ld = zp.ld;
+        e.raw_out = s.p;
+        e.raw_ld = s.ld;
+        stages(a_parts_, g, gp, &e);
+        fused = true;
+      } else {
+        stages(a_parts_, g, s);
+        if (!one_d()) row_reduce(s);
+      }
       Mat y = Y_[static_cast<size_t>(l - 1)].m;
       if (grid_.col_of(rank_) == 0)
         gemm_hts(h_[static_cast<size_t>(l - 1)].m, s, y, false);
@@ -135,7 +193,7 @@ class TrainerRows final : public Trainer {
       comm_->all_reduce(grid_.world(), y.p, static_cast<size_t>(y.rows * y.cols), ncclFloat32,
                         Category::Reduce, words(y), ms_);
       cs_after_ms();
-      if (l >= 2) {
+      if (l >= 2 && !fused) {
         const Mat& zp = z_[static_cast<size_t>(l - 2)].m;
         gemm_swt(s, l - 1, 0, 0, g_[static_cast<size_t>(l - 2)].m, false, kern::EPI_RELU_PRIME, &zp);
       }
@@ -156,7 +214,22 @@ class TrainerRows final : public Trainer {
   }
 
   // out = sum over this column's stages q of parts[q] * (tile of rank (q, j)).
-  void stages(const std::vector<DeviceCsr>& parts, const Mat& mine, Mat out) {
+  // True when stages(parts, mine, out) ends in ONE SpMM whose output is final
+  // (1D: no row all-reduce follows) and whose row epilogue can take the next
+  // dense step: P = 1, or the coalesced narrow-panel path; f <= 32; one pass.
+  bool fusable(const std::vector<DeviceCsr>& parts, const Mat& mine) const {
+    if (fuse_ < 1 || !one_d() || mine.cols > kern::kSpmmEpiMaxF) return false;
+    if (stage_group().size() == 1 && chunk_end(0) - chunk_begin(0) == 1)
+      return spmm_single_pass(parts[static_cast<size_t>(chunk_begin(0))], mine);
+    if (chunk_ok_ && mine.cols <= kCoalesceMaxF) {
+      const DeviceCsr& blk = &parts == &a_parts_ ? a_chunk_ : at_chunk_;
+      return spmm_single_pass(blk, Mat{nullptr, c_hi_ - c_lo_, mine.cols, mine.ld});
+    }
+    return false;
+  }
+
+  void stages(const std::vector<DeviceCsr>& parts, const Mat& mine, Mat out,
+              const kern::SpmmEpi* epi = nullptr) {
     const int j = grid_.col_of(rank_);
     const Group& grp = stage_group();
     const bool comm = grp.size() > 1;
@@ -180,9 +253,11 @@ class TrainerRows final : public Trainer {
       }
       comm_->group_end();
       cs_after_ms();
-      spmm(blk, g, out, false);
+      spmm(blk, g, out, false, epi);
       return;
     }
+    if (epi && !(chunk_end(j) - chunk_begin(j) == 1 && !comm))
+      throw std::logic_error("stages: fused epilogue on a multi-stage propagation");
     ms_after_cs();
     int idx = 0;
     for (int q = chunk_begin(j); q < chunk_end(j); ++q, ++idx) {
@@ -196,7 +271,7 @@ class TrainerRows final : public Trainer {
         CG_CUDA(cudaEventRecord(ev_ready_[b], ms_));
         CG_CUDA(cudaStreamWaitEvent(cs_, ev_ready_[b], 0));
       }
-      spmm(parts[static_cast<size_t>(q)], panel, out, idx > 0);
+      spmm(parts[static_cast<size_t>(q)], panel, out, idx > 0, epi);
       if (comm) CG_CUDA(cudaEventRecord(ev_free_[b], cs_));
     }
     if (idx == 0) CG_CUDA(cudaMemsetAsync(out.p, 0, out.rows * out.ld * sizeof(float), cs_));

@@ -235,7 +235,12 @@ void Trainer::cs_after_ms() {
   CG_CUDA(cudaStreamWaitEvent(cs_, ev_ms_, 0));
 }
 
-void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc) {
+bool Trainer::spmm_single_pass(const DeviceCsr& a, const Mat& h) const {
+  const double panel = static_cast<double>(a.n_cols) * h.cols * 4.0;
+  return a.nnz == 0 || std::ceil(panel / l2_panel_bytes()) <= 1.0;
+}
+
+void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi) {
   if (a.n_cols != h.rows)
     throw std::invalid_argument("spmm: sparse is " + std::to_string(a.n_rows) + "x" +
                                 std::to_string(a.n_cols) + " but dense has " +
@@ -245,6 +250,11 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc) {
   // from an L2-resident slice (SURVEY §7 hard parts).
   const double panel = static_cast<double>(a.n_cols) * h.cols * 4.0;
   const int nb = static_cast<int>(std::min<double>(64.0, std::ceil(panel / l2_panel_bytes())));
+  if (epi) {
+    if (acc || nb > 1) throw std::logic_error("spmm: fused epilogue needs one final pass");
+    spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, false, epi);
+    return;
+  }
   if (nb <= 1 || a.nnz == 0 || out.rows != a.n_rows || out.cols != h.cols) {
     spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, acc);
     return;
@@ -278,16 +288,24 @@ double Trainer::l2_panel_bytes() {
 }
 
 void Trainer::spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32_t* ci,
-                       const float* v, const Mat& h, Mat out, bool acc) {
-  if (out.rows != rows || out.cols != h.cols)
+                       const float* v, const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi) {
+  const int64_t width = epi && epi->W ? epi->fo : h.cols;
+  if (out.rows != rows || out.cols != width)
     throw std::invalid_argument("spmm: accumulator shape mismatch");
   const int slot = prof_begin();
-  kern::spmm_csr(rows, rp, ci, v, h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld, acc, cs_, nnz);
+  kern::spmm_csr(rows, rp, ci, v, h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld, acc, cs_, nnz,
+                 epi);
   if (slot >= 0) {
-    // B = 8(r+1) + 8 nnz + 4 f c + 4 f r (1 + acc); F = 2 nnz f.
+    // B = 8(r+1) + 8 nnz + 4 f c + 4 f r (1 + acc); F = 2 nnz f;
+    // plus the fused epilogue's extra row traffic (raw copy, relu′ mask, relu).
     const double f = static_cast<double>(h.cols), r = static_cast<double>(rows);
-    const double bytes = 8.0 * (r + 1) + 8.0 * nnz + 4.0 * f * h.rows + 4.0 * f * r * (acc ? 2 : 1);
-    prof_end(slot, "spmm", h.cols, bytes, 2.0 * nnz * f);
+    double bytes = 8.0 * (r + 1) + 8.0 * nnz + 4.0 * f * h.rows + 4.0 * f * r * (acc ? 2 : 1);
+    if (epi) {
+      const double fo = static_cast<double>(width);
+      bytes += 4.0 * r * (fo - f) + (epi->raw_out ? 4.0 * r * f : 0.0) +
+               (epi->mask ? 4.0 * r * fo : 0.0) + (epi->relu_out ? 4.0 * r * fo : 0.0);
+    }
+    prof_end(slot, "spmm", h.cols, bytes, 2.0 * nnz * f + (epi && epi->W ? 2.0 * r * f * width : 0.0));
   }
 }
 
@@ -380,7 +398,10 @@ void Trainer::run_gemm(const kern::GemmDesc& d, const char* kind) {
   if (slot >= 0) {
     // 4 (m k + k n + m n) algorithmic bytes, 2 m n k flops.
     const double m = static_cast<double>(d.m), n = static_cast<double>(d.n), k = static_cast<double>(d.k);
-    prof_end(slot, kind, d.k, 4.0 * (m * k + k * n + m * n * (d.accumulate ? 2 : 1)) +
+    // Named by the feature width of the streamed operand: f_in for T·W / S·Wᵀ,
+    // the width of H for Hᵀ·S (whose K is the graph dimension).
+    const bool hts = std::string(kind) == "gemm_hts";
+    prof_end(slot, kind, hts ? d.m : d.k, 4.0 * (m * k + k * n + m * n * (d.accumulate ? 2 : 1)) +
                                   (d.epilogue == kern::EPI_RELU ? 4.0 * m * n : 0.0) +
                                   (d.epilogue == kern::EPI_RELU_PRIME ? 4.0 * m * n : 0.0),
              2.0 * m * n * k);

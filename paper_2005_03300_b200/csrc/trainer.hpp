@@ -110,6 +110,12 @@ class Trainer {
   // Narrow-first propagation Aᵀ(H W) when f_out < f_in (block-row strategies).
   void set_reassociate(bool on) { reassociate_ = on; }
   bool reassociate() const { return reassociate_; }
+  // Fused SpMM row epilogues (block-row strategies, 1D): 0 = none,
+  // 1 = elementwise (ReLU, ⊙relu′; default), 2 = also the small dense
+  // transforms (T·W, S·Wᵀ) — per-row W reads compete with the gathers for
+  // the L1 data pipe, so level 2 is slower on B200 and kept for comparison.
+  void set_fuse(int level) { fuse_ = level; }
+  int fuse() const { return fuse_; }
   void reset_profile() {
     collect_profile();
     profile_.clear();
@@ -127,9 +133,14 @@ class Trainer {
   void init_tiles();  // h/z/g tile shapes from tile_rows/tile_cols, labels, H0
   void ms_after_cs();
   void cs_after_ms();
-  void spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc);
+  // out (+)= a · h.  With epi (f <= 32, acc = false, one pass) the layer's
+  // next dense step runs in the SpMM's row epilogue (kern::SpmmEpi).
+  void spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc,
+            const kern::SpmmEpi* epi = nullptr);
   void spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32_t* ci, const float* v,
-                const Mat& h, Mat out, bool acc);
+                const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi = nullptr);
+  // True when spmm(a, h, ...) is a single kernel pass (no L2 column blocking).
+  bool spmm_single_pass(const DeviceCsr& a, const Mat& h) const;
   // C (+)= A · W[r0:r0+k, c0:c0+n]
   void gemm_aw(const Mat& a, int l, int64_t r0, int64_t c0, Mat c, bool acc, int epi,
                Mat aux_out);
@@ -155,6 +166,7 @@ class Trainer {
   };
   bool timing_ = false;
   bool reassociate_ = false;
+  int fuse_ = 1;
   std::vector<ProfRec> recs_;
   size_t recs_used_ = 0;
   std::vector<ProfEntry> profile_;

@@ -61,6 +61,47 @@ def test_spmm_matches_oracle(cg, orc, torch, f, acc):
         assert rel(got, want) < 1e-6, (f, ld)
 
 
+# Fused SpMM row epilogue (the GCN layer's next dense step): raw copy, dense
+# transform by a small W (both storage orders, i.e. T·W and S·Wᵀ), relu′ mask,
+# relu output — against the oracle's spmm / gemm / relu compositions.
+@pytest.mark.parametrize("f,fo,tw", [(16, 16, 0), (16, 41, 0), (41 - 25, 16, 1), (8, 64, 0),
+                                     (24, 16, 1), (32, 24, 0), (4, 0, 0), (16, 0, 0), (13, 0, 0)])
+@pytest.mark.parametrize("deg", [3.0, 40.0])
+def test_spmm_fused_epilogue(cg, orc, torch, f, fo, tw, deg):
+    n = 900
+    a = orc.normalize(orc.er_generate(n, deg, 5))
+    rng = np.random.default_rng(f * 100 + fo)
+    h = rng.standard_normal((n, f))
+    t = orc.spmm(a, h, np.zeros((n, f)))
+    width = fo if fo else f
+    if fo:
+        w = rng.standard_normal((fo, f) if tw else (f, fo))
+        z = orc.gemm(t, w, False, bool(tw))
+    else:
+        w, z = None, t
+    mask = rng.standard_normal((n, width))
+    g = cg.csr_upload(a.row_ptr, a.col_idx, n, a.vals)
+    rp, ci, v = g.device_ptrs()
+    ldh, ldz = (f + 3) // 4 * 4, (width + 3) // 4 * 4
+    H = padded(torch, h, ldh)
+    M = padded(torch, mask, ldz)
+    W = dev(torch, w.astype(np.float32)) if fo else None
+    w_sk, w_sn = ((1, f) if tw else (fo, 1)) if fo else (0, 0)
+    for use_mask in (False, True):
+        T = torch.zeros((n, ldz), device="cuda")
+        R = torch.zeros((n, ldz), device="cuda")
+        RAW = torch.zeros((n, ldh), device="cuda")
+        cg.check(cg.lib.cagnet_spmm_fused_f32(
+            n, n, a.nnz, rp, ci, v, H.data_ptr(), ldh, f, W.data_ptr() if fo else None, w_sk, w_sn,
+            fo, M.data_ptr() if use_mask else None, ldz, T.data_ptr(), ldz, R.data_ptr(), ldz,
+            RAW.data_ptr(), ldh, stream(torch)))
+        torch.cuda.synchronize()
+        want = z * (mask > 0) if use_mask else z
+        assert rel(RAW.cpu().numpy()[:, :f], t) < 1e-6
+        assert rel(T.cpu().numpy()[:, :width], want) < 2e-6
+        assert rel(R.cpu().numpy()[:, :width], np.maximum(want, 0)) < 2e-6
+
+
 def test_spmm_empty_rows_and_zero_nnz(cg, orc, torch):
     rp = np.array([0, 0, 2, 2, 3], np.int64)
     ci = np.array([1, 3, 0], np.int64)

@@ -56,14 +56,17 @@ def test_single_rank_matches_serial(cg, orc, strat):
 
 
 @pytest.mark.parametrize("kind", ["1d", "1.5d"])
-def test_reassociated_matches_serial(cg, orc, kind):
-    """Narrow-first propagation Aᵀ(H W): same GCN, f_out-wide panels."""
-    dims = [40, 12, 7, 5]
+@pytest.mark.parametrize("fuse", [0, 1, 2])
+@pytest.mark.parametrize("dims", [[40, 12, 7, 5], [40, 16, 16, 24], [20, 16, 41]])
+def test_reassociated_matches_serial(cg, orc, kind, fuse, dims):
+    """Narrow-first propagation Aᵀ(H W): same GCN, f_out-wide panels; with and
+    without the fused SpMM row epilogues (ReLU, T·W, S·Wᵀ ⊙ relu′, relu′);
+    Reddit-shaped widths (narrow, equal and widening output layers)."""
     data = cg.generate_dataset(96, 9.0, dims[0], dims[-1], 7, 8, 9)
     model = cg.init_glorot(dims, 3, 0.25)
     od = orc.generate_dataset(96, 9.0, dims[0], dims[-1], 7, 8, 9)
     losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.25, 3)
-    out = run_single(cg, data, model, cg.Strategy(kind, 1, 1, 0, reassociate=True), 3)
+    out = run_single(cg, data, model, cg.Strategy(kind, 1, 1, 0, reassociate=True, fuse=fuse), 3)
     assert max_rel_error(out, losses, h, y, g, w) < TOL
 
 
