@@ -33,6 +33,7 @@
 #include <cuda.h>
 
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -71,8 +72,8 @@ struct Cfg {
   static_assert(COLS <= 512 && TSTAGES >= 2, "TMEM budget");
   static constexpr uint32_t B_TILE = 2 * BN * BK * 4;              // [hi; lo] k-block
   static constexpr uint32_t S_TILE = BN * BK * 4;                  // raw streamed S k-block
-  static constexpr int EP_LD = BN + 4;                             // staged output row (floats)
-  static constexpr uint32_t EP_BYTES = BM * EP_LD * 4;
+  static constexpr int EP_LD = BN;                                 // staged output row (floats)
+  static constexpr uint32_t EP_BYTES = BM * EP_LD * 4;             // one [BM][BN] TMA box
 };
 
 struct TmParams {
@@ -93,7 +94,26 @@ struct TmParams {
   int m_tiles;
   int chains;       // accumulator chains in use (1 for short K: nothing to overlap)
   int dbg;          // timing experiments only (CAGNET_GEMM_DBG): 1 skip st, 2 skip mma, 4 skip epi stores
+  // Contiguous operands move as ONE bulk copy per k-block instead of a tensor
+  // box of many narrow rows (64 B rows cost the TMA one request each):
+  const float* A;
+  int64_t a_ld;     // row stride of A in memory (elements)
+  int a_bulk;       // AMODE 0: tile = 128 x a_ld (a_ld <= 32); AMODE 1: k-block = 32 x a_ld (m <= 128)
+  int s_bulk;       // streamed S k-block = 32 x b_sk contiguous floats (b_sk <= BN)
+  int tstore;       // epilogue through TMA tensor stores (C / aux_out / partial maps)
+  int64_t pld;      // row stride of the split-K partial rows (multiple of 4)
+  int64_t mpad;     // rows per split in the partial buffer (m rounded up to BM)
+  unsigned long long* trace;  // dev timing trace of CTA 0 (CAGNET_GEMM_TRACE), else null
 };
+
+// Timing trace (development only): slot = event * 64 + g for g < 64.
+__device__ __forceinline__ void trace_at(const TmParams& p, int ev, int64_t g) {
+  if (p.trace != nullptr && blockIdx.x == 0 && g < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[ev * 64 + g] = t;
+  }
+}
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
@@ -118,6 +138,27 @@ __device__ __forceinline__ void tma_load_2d(uint32_t smem, const CUtensorMap* ma
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
+
+// 1D bulk copy global → shared, completing on an mbarrier (bytes % 16 == 0).
+__device__ __forceinline__ void bulk_load(uint32_t smem, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -174,6 +215,7 @@ __device__ __forceinline__ float epilogue_value(const TmParams& p, int64_t r, in
 template <int BN, int AMODE, bool BSTREAM>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tm_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                   const __grid_constant__ CUtensorMap cmap, const __grid_constant__ CUtensorMap xmap,
                    const TmParams p, int ns) {
   using K = Cfg<BN, BSTREAM>;
   constexpr int kTmemStages = K::TSTAGES;
@@ -187,14 +229,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   char* s_ring = a_ring + ns * A_TILE;                  // ns x S_TILE (streamed B raw)
   char* b_cat = s_ring + (BSTREAM ? ns * K::S_TILE : 0);  // resident nkb or SB stages
   const int b_slots = BSTREAM ? SB : p.nkb_res;
-  float* ep = reinterpret_cast<float*>(b_cat + b_slots * K::B_TILE);  // [BM][EP_LD]
-  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(ep) + K::EP_BYTES);
+  float* ep = reinterpret_cast<float*>(b_cat + b_slots * K::B_TILE);  // [BM][BN] output tile
+  float* ep2 = ep + BM * K::EP_LD;  // relu output / loaded relu′ mask (second box)
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(ep) + 2 * K::EP_BYTES);
   uint64_t* sempty = full + kMaxStages;       // smem stage read by the converters
   uint64_t* conv = sempty + kMaxStages;       // [kTmemStages] TMEM A stage written
   uint64_t* tempty = conv + kTmemStages;      // [kTmemStages] TMEM A stage consumed by MMA
   uint64_t* afull = tempty + kTmemStages;     // [2] accumulator set complete
   uint64_t* aempty = afull + 2;               // [2] accumulator set drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
+  uint64_t* eload = aempty + 2;               // epilogue's C / mask tile loads
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(eload + 1);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -212,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(&afull[i], 1);
       tc::mbar_init(&aempty[i], kEpi / 32);
     }
+    tc::mbar_init(eload, 1);
     tc::fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap)) : "memory");
     if (BSTREAM)
@@ -267,17 +312,39 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int s = static_cast<int>(g % ns);
           if (g >= ns) tc::mbar_wait(&sempty[s], static_cast<uint32_t>(((g / ns) - 1) & 1));
-          tc::mbar_arrive_expect_tx(&full[s], A_TILE + (BSTREAM ? K::S_TILE : 0));
-          const int kcoord = static_cast<int>((kb0 + kb) * BK);
-          if (AMODE == 0)
-            tma_load_2d(tc::smem_u32(a_ring + s * A_TILE), &amap, tc::smem_u32(&full[s]), kcoord,
-                        m_tile * BM);
-          else
-            tma_load_2d(tc::smem_u32(a_ring + s * A_TILE), &amap, tc::smem_u32(&full[s]),
-                        m_tile * BM, kcoord);
-          if (BSTREAM)
-            tma_load_2d(tc::smem_u32(s_ring + s * K::S_TILE), &bmap, tc::smem_u32(&full[s]), 0,
-                        kcoord);
+          const int64_t kg = (kb0 + kb) * BK;
+          const int kcoord = static_cast<int>(kg);
+          const int kval = static_cast<int>(p.k - kg < BK ? p.k - kg : BK);
+          uint32_t a_bytes = A_TILE, s_bytes = BSTREAM ? K::S_TILE : 0;
+          if (p.a_bulk) {
+            if (AMODE == 0) {
+              const int64_t r0 = static_cast<int64_t>(m_tile) * BM;
+              const int rows = static_cast<int>(p.m - r0 < BM ? p.m - r0 : BM);
+              a_bytes = static_cast<uint32_t>(rows * p.a_ld * 4);
+            } else {
+              a_bytes = static_cast<uint32_t>(kval * p.a_ld * 4);
+            }
+          }
+          if (BSTREAM && p.s_bulk) s_bytes = static_cast<uint32_t>(kval * p.b_sk * 4);
+          trace_at(p, 0, g);
+          tc::mbar_arrive_expect_tx(&full[s], a_bytes + s_bytes);
+          const uint32_t a_dst = tc::smem_u32(a_ring + s * A_TILE);
+          if (p.a_bulk) {
+            const float* src = AMODE == 0 ? p.A + static_cast<int64_t>(m_tile) * BM * p.a_ld
+                                          : p.A + kg * p.a_ld;
+            bulk_load(a_dst, src, a_bytes, tc::smem_u32(&full[s]));
+          } else if (AMODE == 0) {
+            tma_load_2d(a_dst, &amap, tc::smem_u32(&full[s]), kcoord, m_tile * BM);
+          } else {
+            tma_load_2d(a_dst, &amap, tc::smem_u32(&full[s]), m_tile * BM, kcoord);
+          }
+          if (BSTREAM) {
+            const uint32_t s_dst = tc::smem_u32(s_ring + s * K::S_TILE);
+            if (p.s_bulk)
+              bulk_load(s_dst, p.B + kg * p.b_sk, s_bytes, tc::smem_u32(&full[s]));
+            else
+              tma_load_2d(s_dst, &bmap, tc::smem_u32(&full[s]), 0, kcoord);
+          }
         }
       }
     }
@@ -309,8 +376,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_tf32_ts(d, a_hi + kk * 8, bdesc, IDESC_HL, (kb > 0) || (kk >= p.chains));
             mma_tf32_ts(d + BN, a_lo + kk * 8, bdesc, IDESC_L, 1);
           }
+          trace_at(p, 3, g);
           tc::mma_commit(&tempty[ts]);
-          if (kb == nkb - 1) tc::mma_commit(&afull[set]);
+          if (kb == nkb - 1) {
+            tc::mma_commit(&afull[set]);
+            trace_at(p, 5, t);
+          }
         }
         __syncwarp();
       }
@@ -329,9 +400,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = static_cast<int>(g % ns);
         const int ts = static_cast<int>(g % kTmemStages);
         tc::mbar_wait(&full[s], static_cast<uint32_t>((g / ns) & 1));
+        if (ct == 0) trace_at(p, 1, g);
         const char* at = a_ring + s * A_TILE;
         uint32_t hi[BK], lo[BK];
-        if (AMODE == 0) {
+        const int64_t kg = (static_cast<int64_t>(split) * (p.k_chunk / BK) + kb) * BK;
+        const int kval = static_cast<int>(p.k - kg < BK ? p.k - kg : BK);
+        if (p.a_bulk) {
+          // Dense rows of stride a_ld; bytes past the copied extent are stale.
+          const int lda = static_cast<int>(p.a_ld);
+          const float* af = reinterpret_cast<const float*>(at);
+          if (AMODE == 0) {
+            const bool live = static_cast<int64_t>(m_tile) * BM + row < p.m;
+#pragma unroll
+            for (int kk = 0; kk < BK; ++kk) {
+              const float x = (live && kk < kval) ? af[row * lda + kk] : 0.f;
+              const float h = tc::to_tf32(x);
+              hi[kk] = __float_as_uint(h);
+              lo[kk] = __float_as_uint(x - h);
+            }
+          } else {
+            const bool live = row < p.m;
+#pragma unroll
+            for (int kk = 0; kk < BK; ++kk) {
+              const float x = (live && kk < kval) ? af[kk * lda + row] : 0.f;
+              const float h = tc::to_tf32(x);
+              hi[kk] = __float_as_uint(h);
+              lo[kk] = __float_as_uint(x - h);
+            }
+          }
+        } else if (AMODE == 0) {
 #pragma unroll
           for (int c = 0; c < BK / 4; ++c) {
             const float4 v = *reinterpret_cast<const float4*>(
@@ -361,11 +458,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           // Raw S k-block [32 k][BN j] → K-major [B_hi; B_lo] rows j / BN + j.
           const char* st = s_ring + s * K::S_TILE;
           char* bt = b_cat + ts * K::B_TILE;
+          const int sld = p.s_bulk ? static_cast<int>(p.b_sk) : BN;
 #pragma unroll
           for (int i = 0; i < (BN * BK) / kConv; ++i) {
             const int e = i * kConv + ct;
             const int kk = e / BN, j = e % BN;
-            const float x = *reinterpret_cast<const float*>(st + (kk * BN + j) * 4);
+            const float x = (!p.s_bulk || (kk < kval && j < p.n))
+                                ? *reinterpret_cast<const float*>(st + (kk * sld + j) * 4)
+                                : 0.f;
             const float h = tc::to_tf32(x);
             *reinterpret_cast<float*>(bt + sw128_off(j, kk)) = h;
             *reinterpret_cast<float*>(bt + sw128_off(BN + j, kk)) = x - h;
@@ -385,69 +485,117 @@ __global__ void __launch_bounds__(kThreads, 1)
         if ((tid & 31) == 0) {
           mbar_arrive(&sempty[s]);
           mbar_arrive(&conv[ts]);
+          if (ct == 0) trace_at(p, 2, g);
         }
       }
     }
   } else {
     // ---------------- epilogue ----------------
     const int et = tid - 64 - kConv;  // 0..127
+    const bool leader = et == 0;
     const int lane_q = warp & 3;
     const int row = lane_q * 32 + (tid & 31);
     const uint32_t lane_bits = static_cast<uint32_t>(lane_q * 32) << 16;
     const int n = static_cast<int>(p.n);
-    const int rpp = kEpi / n;          // rows per pass (n <= 64)
+    const int rpp = kEpi / n;          // STG path: rows per pass (n <= 64)
     const int er = et / n, ec = et - er * n;
     const bool ec_ok = er < rpp;
+    constexpr int NCH = BN / 4;        // float4 chunks per staged row
+    const bool load_c = p.tstore && p.accumulate && !p.partial;
+    const bool load_x = p.tstore && p.epilogue == EPI_RELU_PRIME && !p.partial;
+    const bool relu_out = p.epilogue == EPI_RELU && p.aux_out != nullptr && !p.partial;
     for (int t = 0; t < my_tiles; ++t) {
       int m_tile, split, nkb;
       tile_of(t, m_tile, split, nkb);
+      const int64_t r0 = static_cast<int64_t>(m_tile) * BM;
+      if (leader && (load_c || load_x)) {
+        tc::mbar_arrive_expect_tx(eload, (load_c ? K::EP_BYTES : 0) + (load_x ? K::EP_BYTES : 0));
+        if (load_c) tma_load_2d(tc::smem_u32(ep), &cmap, tc::smem_u32(eload), 0, static_cast<int>(r0));
+        if (load_x) tma_load_2d(tc::smem_u32(ep2), &xmap, tc::smem_u32(eload), 0, static_cast<int>(r0));
+      }
       const int set = K::SETS == 2 ? (t & 1) : 0;
       const int use = K::SETS == 2 ? (t >> 1) : t;
       tc::mbar_wait(&afull[set], static_cast<uint32_t>(use & 1));
+      if (et == 0) trace_at(p, 4, t);
       tc::tc_fence_after();
       const uint32_t base = tmem + lane_bits + K::D_BASE + set * K::SET_COLS;
-#pragma unroll 1
-      for (int cb = 0; cb < BN / 16; ++cb) {
-        float v[16];
+      float v[BN];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      for (int j = 0; j < BN; ++j) v[j] = 0.f;
 #pragma unroll 1
-        for (int c = 0; c < p.chains; ++c) {
+      for (int c = 0; c < p.chains; ++c) {
+#pragma unroll
+        for (int cb = 0; cb < BN / 16; ++cb) {
           uint32_t w[16], u[16];
           tc::tmem_ld16_nowait(base + c * 2 * BN + cb * 16, w);
           tc::tmem_ld16_nowait(base + c * 2 * BN + BN + cb * 16, u);
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] += __uint_as_float(w[j]) + __uint_as_float(u[j]);
+          for (int j = 0; j < 16; ++j) v[cb * 16 + j] += __uint_as_float(w[j]) + __uint_as_float(u[j]);
         }
-        float4* dst = reinterpret_cast<float4*>(ep + row * K::EP_LD + cb * 16);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
       }
-      // The accumulator set is free once it sits in shared memory.
+      // The accumulator set is free once it sits in registers.
       tc::tc_fence_before();
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(&aempty[set]);
+      if (load_c || load_x) tc::mbar_wait(eload, static_cast<uint32_t>(t & 1));
+      float4* e4 = reinterpret_cast<float4*>(ep + row * K::EP_LD);
+      float4* x4 = reinterpret_cast<float4*>(ep2 + row * K::EP_LD);
+#pragma unroll
+      for (int i = 0; i < NCH; ++i) {
+        const int q = i;
+        float4 z = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        if (load_c) {
+          const float4 o = e4[q];
+          z.x += o.x;
+          z.y += o.y;
+          z.z += o.z;
+          z.w += o.w;
+        }
+        if (load_x) {
+          const float4 m = x4[q];
+          z.x = m.x > 0.f ? z.x : z.x * 0.f;
+          z.y = m.y > 0.f ? z.y : z.y * 0.f;
+          z.z = m.z > 0.f ? z.z : z.z * 0.f;
+          z.w = m.w > 0.f ? z.w : z.w * 0.f;
+        }
+        e4[q] = z;
+        if (p.tstore && relu_out)
+          x4[q] = make_float4(fmaxf(z.x, 0.f), fmaxf(z.y, 0.f), fmaxf(z.z, 0.f), fmaxf(z.w, 0.f));
+      }
+      if (p.tstore) {
+        tc::fence_proxy_async_smem();
+        asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
+        if (leader && !(p.dbg & 4)) {
+          if (p.partial) {
+            tma_store_2d(&cmap, tc::smem_u32(ep), 0, static_cast<int>(static_cast<int64_t>(split) * p.mpad + r0));
+          } else {
+            tma_store_2d(&cmap, tc::smem_u32(ep), 0, static_cast<int>(r0));
+            if (relu_out) tma_store_2d(&xmap, tc::smem_u32(ep2), 0, static_cast<int>(r0));
+          }
+          bulk_commit();
+          bulk_wait_read0();  // staging tiles reusable
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
+        continue;
+      }
       asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
-      // Coalesced row-major stores of the tile's valid rows: thread et owns
-      // column ec of rows er, er + rpp, ... (no per-element division); the
-      // loads of each batch of 4 rows are issued before their stores.
-      const int64_t r0 = static_cast<int64_t>(m_tile) * BM;
+      // Fallback: coalesced row-major stores, thread et owns column ec of rows
+      // er, er + rpp, ...; loads of each batch of 4 rows precede their stores.
       const int rows = static_cast<int>(p.m - r0 < BM ? p.m - r0 : BM);
       if (ec_ok && !(p.dbg & 4)) {
         if (p.partial) {
-          float* dst = p.partial + (static_cast<int64_t>(split) * p.m + r0) * p.n + ec;
-          for (int r = er; r < rows; r += rpp) dst[static_cast<int64_t>(r) * p.n] = ep[r * K::EP_LD + ec];
+          float* dst = p.partial + (static_cast<int64_t>(split) * p.mpad + r0) * p.pld + ec;
+          for (int r = er; r < rows; r += rpp) dst[static_cast<int64_t>(r) * p.pld] = ep[r * K::EP_LD + ec];
         } else {
           for (int rb = er; rb < rows; rb += 4 * rpp) {
-            float v[4], cold[4], ax[4];
+            float x[4], cold[4], ax[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int r = rb + i * rpp;
               const int64_t gr = r0 + r;
               const bool ok = r < rows;
-              v[i] = ok ? ep[r * K::EP_LD + ec] : 0.f;
+              x[i] = ok ? ep[r * K::EP_LD + ec] : 0.f;
               cold[i] = (ok && p.accumulate) ? p.C[gr * p.ldc + ec] : 0.f;
               ax[i] = (ok && p.epilogue == EPI_RELU_PRIME) ? p.aux[gr * p.ldaux + ec] : 1.f;
             }
@@ -456,19 +604,20 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int r = rb + i * rpp;
               if (r >= rows) break;
               const int64_t gr = r0 + r;
-              float x = v[i] + cold[i];
+              float y = x[i] + cold[i];
               if (p.epilogue == EPI_RELU) {
-                if (p.aux_out) p.aux_out[gr * p.ldao + ec] = x > 0.f ? x : 0.f;
+                if (p.aux_out) p.aux_out[gr * p.ldao + ec] = y > 0.f ? y : 0.f;
               } else if (p.epilogue == EPI_RELU_PRIME) {
-                x = ax[i] > 0.f ? x : x * 0.f;
+                y = ax[i] > 0.f ? y : y * 0.f;
               }
-              p.C[gr * p.ldc + ec] = x;
+              p.C[gr * p.ldc + ec] = y;
             }
           }
         }
       }
       asm volatile("bar.sync 1, %0;" ::"r"(kEpi) : "memory");
     }
+    if (leader) bulk_wait0();  // stores globally visible before the CTA retires
   }
 
   tc::tc_fence_before();
@@ -486,11 +635,12 @@ __global__ void tm_reduce_kernel(const TmParams p, int splits) {
   for (int64_t e = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; e < total;
        e += warps) {
     float s = 0.f;
-    for (int z = lane; z < splits; z += 32) s += p.partial[static_cast<int64_t>(z) * total + e];
+    const int64_t r = e / p.n, c = e % p.n;
+    for (int z = lane; z < splits; z += 32)
+      s += p.partial[(static_cast<int64_t>(z) * p.mpad + r) * p.pld + c];
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
-      const int64_t r = e / p.n, c = e % p.n;
       p.C[r * p.ldc + c] = epilogue_value(p, r, c, s);
     }
   }
@@ -530,12 +680,12 @@ bool encode_2d(CUtensorMap* map, const float* base, uint64_t inner, uint64_t out
 }
 
 template <int BN, int AMODE, bool BSTREAM>
-void launch_tm(const CUtensorMap& amap, const CUtensorMap& bmap, const TmParams& p, int grid,
-               cudaStream_t s) {
+void launch_tm(const CUtensorMap& amap, const CUtensorMap& bmap, const CUtensorMap& cmap,
+               const CUtensorMap& xmap, const TmParams& p, int grid, cudaStream_t s) {
   using K = Cfg<BN, BSTREAM>;
   constexpr int kTmemStages = K::TSTAGES;
   const size_t fixed = 1024 + static_cast<size_t>(BSTREAM ? kTmemStages : p.nkb_res) * K::B_TILE +
-                       K::EP_BYTES + (3 * kMaxStages + 4 * kTmemStages + 8) * 8;
+                       2 * K::EP_BYTES + (3 * kMaxStages + 4 * kTmemStages + 10) * 8;
   const size_t per_stage = A_TILE + (BSTREAM ? K::S_TILE : 0);
   int ns = static_cast<int>((227 * 1024 - fixed) / per_stage);
   if (ns > kMaxStages) ns = kMaxStages;
@@ -547,22 +697,41 @@ void launch_tm(const CUtensorMap& amap, const CUtensorMap& bmap, const TmParams&
     CG_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     configured.fetch_or(bit);
   }
-  kfn<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(amap, bmap, p, ns);
+  kfn<<<static_cast<unsigned>(grid), kThreads, smem, s>>>(amap, bmap, cmap, xmap, p, ns);
   CG_LAUNCH_CHECK();
 }
 
+struct Maps {
+  CUtensorMap a, b, c, x;
+};
+
 template <int AMODE, bool BSTREAM>
-void launch_bn(int bn, const CUtensorMap& amap, const CUtensorMap& bmap, const TmParams& p,
-               int grid, cudaStream_t s) {
+void launch_bn(int bn, const Maps& m, const TmParams& p, int grid, cudaStream_t s) {
   switch (bn) {
-    case 16: return launch_tm<16, AMODE, BSTREAM>(amap, bmap, p, grid, s);
-    case 32: return launch_tm<32, AMODE, BSTREAM>(amap, bmap, p, grid, s);
-    case 48: return launch_tm<48, AMODE, BSTREAM>(amap, bmap, p, grid, s);
-    default: return launch_tm<64, AMODE, BSTREAM>(amap, bmap, p, grid, s);
+    case 16: return launch_tm<16, AMODE, BSTREAM>(m.a, m.b, m.c, m.x, p, grid, s);
+    case 32: return launch_tm<32, AMODE, BSTREAM>(m.a, m.b, m.c, m.x, p, grid, s);
+    case 48: return launch_tm<48, AMODE, BSTREAM>(m.a, m.b, m.c, m.x, p, grid, s);
+    default: return launch_tm<64, AMODE, BSTREAM>(m.a, m.b, m.c, m.x, p, grid, s);
   }
 }
 
 bool aligned16(const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; }
+
+// Development trace: event times of CTA 0 relative to the first producer issue.
+void dump_trace(const TmParams& p, cudaStream_t s, const char* what) {
+  if (!p.trace) return;
+  CG_CUDA(cudaStreamSynchronize(s));
+  unsigned long long tr[8 * 64];
+  CG_CUDA(cudaMemcpy(tr, p.trace, sizeof(tr), cudaMemcpyDeviceToHost));
+  const unsigned long long t0 = tr[0];
+  std::fprintf(stderr, "[gemm_tm trace %s m=%lld n=%lld k=%lld] g: issue full conv mma (ns)\n", what,
+               static_cast<long long>(p.m), static_cast<long long>(p.n), static_cast<long long>(p.k));
+  for (int g = 0; g < 24; ++g)
+    std::fprintf(stderr, "  %2d: %8lld %8lld %8lld %8lld   epi[t=%d] %8lld commit %8lld\n", g,
+                 static_cast<long long>(tr[g] - t0), static_cast<long long>(tr[64 + g] - t0),
+                 static_cast<long long>(tr[128 + g] - t0), static_cast<long long>(tr[192 + g] - t0), g,
+                 static_cast<long long>(tr[256 + g] - t0), static_cast<long long>(tr[320 + g] - t0));
+}
 
 }  // namespace
 
@@ -582,6 +751,7 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
   p.m = d.m;
   p.n = d.n;
   p.k = d.k;
+  p.A = d.A;
   p.B = d.B;
   p.b_sk = d.b_sk;
   p.b_sn = d.b_sn;
@@ -594,34 +764,83 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
   p.aux_out = d.aux_out;
   p.ldao = d.ldao;
   p.m_tiles = static_cast<int>(m_tiles);
+  p.pld = round_up(d.n, 4);
+  p.mpad = m_tiles * BM;
+  static unsigned long long* trace = [] {
+    unsigned long long* t = nullptr;
+    if (std::getenv("CAGNET_GEMM_TRACE")) {
+      CG_CUDA(cudaMalloc(&t, 8 * 64 * sizeof(unsigned long long)));
+      CG_CUDA(cudaMemset(t, 0, 8 * 64 * sizeof(unsigned long long)));
+    }
+    return t;
+  }();
+  p.trace = trace;
 
-  CUtensorMap amap, bmap;
-  std::memset(&bmap, 0, sizeof(bmap));
+  Maps maps;
+  std::memset(&maps, 0, sizeof(maps));
   const bool a_k = d.a_sk == 1 && d.a_sm % 4 == 0 && d.a_sm >= d.k;
   const bool a_m = d.a_sm == 1 && d.a_sk % 4 == 0 && d.a_sk >= d.m;
   const bool b_stream_ok = d.b_sn == 1 && d.b_sk % 4 == 0 && aligned16(d.B) && d.b_sk >= d.n;
+  // Epilogue through TMA tensor stores when every output matrix is a
+  // 16 B-aligned row-major tile (the layout the trainers use).
+  auto ok_mat = [](const void* q, int64_t ld) { return q != nullptr && aligned16(q) && ld % 4 == 0; };
+  static const bool tstore_on = [] {
+    const char* e = std::getenv("CAGNET_GEMM_TSTORE");
+    return !(e && e[0] == '0');
+  }();
+  auto epi_maps = [&](bool split) -> bool {
+    if (!tstore_on) return false;
+    if (split) return true;  // partial map set by the caller
+    if (!ok_mat(d.C, d.ldc)) return false;
+    if (d.epilogue == EPI_RELU && d.aux_out && !ok_mat(d.aux_out, d.ldao)) return false;
+    if (d.epilogue == EPI_RELU_PRIME && !ok_mat(d.aux, d.ldaux)) return false;
+    if (!encode_2d(&maps.c, d.C, static_cast<uint64_t>(d.n), static_cast<uint64_t>(d.m),
+                   static_cast<uint64_t>(d.ldc), static_cast<uint32_t>(bn), BM, false))
+      return false;
+    if (d.epilogue == EPI_RELU && d.aux_out)
+      return encode_2d(&maps.x, d.aux_out, static_cast<uint64_t>(d.n), static_cast<uint64_t>(d.m),
+                       static_cast<uint64_t>(d.ldao), static_cast<uint32_t>(bn), BM, false);
+    if (d.epilogue == EPI_RELU_PRIME)
+      return encode_2d(&maps.x, d.aux, static_cast<uint64_t>(d.n), static_cast<uint64_t>(d.m),
+                       static_cast<uint64_t>(d.ldaux), static_cast<uint32_t>(bn), BM, false);
+    return true;
+  };
 
   if (a_k) {
     // T·W / S·Wᵀ: W resident, no split (K is a feature width).
     const int nkb = static_cast<int>(ceil_div64(d.k, BK));
     if (static_cast<int64_t>(nkb) * 2 * bn * BK * 4 > kMaxResidentB) return false;
-    if (!encode_2d(&amap, d.A, static_cast<uint64_t>(d.k), static_cast<uint64_t>(d.m),
-                   static_cast<uint64_t>(d.a_sm), BK, BM, true))
+    p.a_ld = d.a_sm;
+    // (A 128-row tile with a_ld <= 32 is one contiguous range, but reading its
+    // 64 B rows thread-per-row is 16-way bank-conflicted; the SWIZZLE_128B
+    // tensor box reads conflict-free, so bulk stays off for AMODE 0.)
+    p.a_bulk = 0;
+    if (!p.a_bulk && !encode_2d(&maps.a, d.A, static_cast<uint64_t>(d.k), static_cast<uint64_t>(d.m),
+                                static_cast<uint64_t>(d.a_sm), BK, BM, true))
       return false;
     p.nkb_res = nkb;
     p.k_chunk = static_cast<int64_t>(nkb) * BK;
     p.chains = nkb >= 2 ? (bn <= 16 ? 4 : bn <= 48 ? 2 : 1) : 1;
+    p.tstore = epi_maps(false) ? 1 : 0;
     const int grid = static_cast<int>(m_tiles < sms ? m_tiles : sms);
-    launch_bn<0, false>(bn, amap, bmap, p, grid, stream);
+    launch_bn<0, false>(bn, maps, p, grid, stream);
+    dump_trace(p, stream, "aw");
     return true;
   }
   if (a_m && b_stream_ok) {
     // Hᵀ·S: K = graph rows, split across CTAs, S streamed with H.
-    if (!encode_2d(&amap, d.A, static_cast<uint64_t>(d.m), static_cast<uint64_t>(d.k),
-                   static_cast<uint64_t>(d.a_sk), BM, BK, false))
+    p.a_ld = d.a_sk;
+    static const bool bulk_on = [] {
+      const char* e = std::getenv("CAGNET_GEMM_BULK");
+      return e && e[0] == '1';
+    }();
+    p.a_bulk = (bulk_on && m_tiles == 1 && d.a_sk <= BM) ? 1 : 0;  // a 32-row k-block is contiguous
+    p.s_bulk = (bulk_on && d.b_sk <= bn) ? 1 : 0;
+    if (!p.a_bulk && !encode_2d(&maps.a, d.A, static_cast<uint64_t>(d.m), static_cast<uint64_t>(d.k),
+                                static_cast<uint64_t>(d.a_sk), BM, BK, false))
       return false;
-    if (!encode_2d(&bmap, d.B, static_cast<uint64_t>(d.n), static_cast<uint64_t>(d.k),
-                   static_cast<uint64_t>(d.b_sk), static_cast<uint32_t>(bn), BK, false))
+    if (!p.s_bulk && !encode_2d(&maps.b, d.B, static_cast<uint64_t>(d.n), static_cast<uint64_t>(d.k),
+                                static_cast<uint64_t>(d.b_sk), static_cast<uint32_t>(bn), BK, false))
       return false;
     const int64_t kblocks = ceil_div64(d.k, BK);
     // One tile per CTA, no second wave: floor(SMs / M tiles) splits.
@@ -634,12 +853,20 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
     float* work = nullptr;
     if (splits > 1) {
       CG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&work),
-                              static_cast<size_t>(splits) * d.m * d.n * sizeof(float), stream));
+                              static_cast<size_t>(splits) * p.mpad * p.pld * sizeof(float), stream));
       p.partial = work;
+      p.tstore = encode_2d(&maps.c, work, static_cast<uint64_t>(d.n),
+                           static_cast<uint64_t>(splits * p.mpad), static_cast<uint64_t>(p.pld),
+                           static_cast<uint32_t>(bn), BM, false)
+                     ? 1
+                     : 0;
+    } else {
+      p.tstore = epi_maps(false) ? 1 : 0;
     }
     const int64_t tiles = m_tiles * splits;
     const int grid = static_cast<int>(tiles < sms ? tiles : sms);
-    launch_bn<1, true>(bn, amap, bmap, p, grid, stream);
+    launch_bn<1, true>(bn, maps, p, grid, stream);
+    dump_trace(p, stream, "hts");
     if (splits > 1) {
       const int64_t total = d.m * d.n;  // one warp per element
       const int blocks = static_cast<int>(ceil_div64(total, 8) < 8 * sms ? ceil_div64(total, 8) : 8 * sms);

@@ -216,12 +216,21 @@ def test_gemm_epilogues(cg, orc, torch, pad):
     w2 = rng.standard_normal((k, 16))
     aux = rng.standard_normal((m, k))
     want = orc.gemm(s, w2, False, True) * (aux > 0)
-    S, W2, AUX = dev(torch, s.astype(np.float32)), dev(torch, w2.astype(np.float32)), dev(torch, aux.astype(np.float32))
-    G = torch.zeros((m, k), device="cuda")
-    cg.check(cg.lib.cagnet_gemm_f32(0, 1, m, k, 16, S.data_ptr(), 16, W2.data_ptr(), 16, G.data_ptr(), k,
-                                    0, 2, AUX.data_ptr(), k, None, 0, stream(torch)))
+    ldg = 44 if pad else k
+    S, W2 = dev(torch, s.astype(np.float32)), dev(torch, w2.astype(np.float32))
+    AUX = padded(torch, aux, ldg)
+    G = torch.zeros((m, ldg), device="cuda")
+    cg.check(cg.lib.cagnet_gemm_f32(0, 1, m, k, 16, S.data_ptr(), 16, W2.data_ptr(), 16, G.data_ptr(), ldg,
+                                    0, 2, AUX.data_ptr(), ldg, None, 0, stream(torch)))
     torch.cuda.synchronize()
-    assert rel(G.cpu().numpy(), want) < 2e-6
+    assert rel(G.cpu().numpy()[:, :k], want) < 2e-6
+    # relu′ with accumulate (C += S Wᵀ, then the mask)
+    c0 = rng.standard_normal((m, k))
+    G = padded(torch, c0, ldg)
+    cg.check(cg.lib.cagnet_gemm_f32(0, 1, m, k, 16, S.data_ptr(), 16, W2.data_ptr(), 16, G.data_ptr(), ldg,
+                                    1, 2, AUX.data_ptr(), ldg, None, 0, stream(torch)))
+    torch.cuda.synchronize()
+    assert rel(G.cpu().numpy()[:, :k], (c0 + orc.gemm(s, w2, False, True)) * (aux > 0)) < 2e-6
 
 
 def test_gemm_rejects_bad_shapes(cg):
