@@ -29,18 +29,19 @@ METRIC = "GCN epoch time (ms) at 1/2/4/8 B200 per 1D/1.5D/2D/3D; SpMM GB/s vs HB
 REDDIT_N, REDDIT_E = 232965, 114848857
 CONFIGS = {
     # BASELINE.json configs[0]
-    "config1": dict(n=4096, degree=16.0, dims=[128, 16, 8], generator="reference",
+    "config1": dict(n=4096, degree=16.0, dims=[128, 16, 8], generator="reference", sample_div=1,
                     label="ER n=4096 d=16, 2-layer GCN {128,16,8}"),
     # configs[1]/[2]: Reddit-shaped, the bit-exact reference ER generator on the GPU
     "reddit": dict(n=REDDIT_N, degree=REDDIT_E / REDDIT_N, dims=[602, 16, 16, 41],
-                   generator="reference",
+                   generator="reference", sample_div=16,
                    label="Reddit-shaped ER n=232965 nnz=115M f=602, 3-layer GCN {602,16,16,41}"),
     # configs[3]: Amazon-shaped, O(nnz) ER-shaped generator
     "amazon": dict(n=14249639, degree=230788269 / 14249639, dims=[300, 16, 16, 24],
-                   generator="skip",
+                   generator="skip", sample_div=512,
                    label="Amazon-shaped ER n=14.2M nnz=245M f=300, 3-layer GCN {300,16,16,24}"),
     # configs[4]: Protein-shaped (BASELINE's 1.3B edges)
     "protein": dict(n=8745542, degree=1.3e9 / 8745542, dims=[128, 16, 16, 256], generator="skip",
+                    sample_div=256,
                     label="Protein-shaped ER n=8.7M nnz=1.3B f=128, 3-layer GCN {128,16,16,256}"),
 }
 SEEDS = dict(seed_graph=1, seed_features=2, seed_labels=3)
@@ -61,10 +62,14 @@ def parse():
                         "narrow-first A^T (H W) on 1D/1.5D (same product)")
     p.add_argument("--no-alt", action="store_true",
                    help="skip timing the other propagation order")
+    p.add_argument("--fuse", type=int, default=1,
+                   help="fused SpMM row epilogues: 0 off, 1 ReLU/relu' (default), 2 + dense W")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--sample-div", type=int, default=16,
-                   help="CPU sample = the config's graph with n/div vertices, same degree")
+    p.add_argument("--sample-div", type=int, default=0,
+                   help="CPU sample = the config's graph with n/div vertices, same degree "
+                        "(default per config: the reference's O(n^2) ER generator must stay "
+                        "within seconds)")
     return p.parse_args()
 
 
@@ -79,58 +84,62 @@ def dist_env():
 # clocks (nvidia-smi sampled during the timed region)
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clock and clock-event (throttle) reasons of one GPU every
+    ~2 ms through NVML in a thread, so even a short timed region gets
+    samples (nvidia-smi's 100 ms loop missed a 20 ms region)."""
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import pynvml
+            pynvml.nvmlInit()
+            visible = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(visible.split(",")[self.device]) if visible else self.device
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         except Exception:
-            self.proc = None
+            self._t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((mhz, reasons))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = max(mx, float(parts[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"],
+                    "samples": 0}
+        nv = self._nv
+        names = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                 "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                 "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                 "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap,
+                 "hw_power_brake_slowdown": nv.nvmlClocksEventReasonHwPowerBrakeSlowdown}
+        seen = sorted({k for _, r in self.samples for k, bit in names.items() if r & bit})
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": seen, "samples": len(self.samples),
+                "source": "NVML every ~2 ms during the timed region"}
 
 
 # ---------------------------------------------------------------------------
@@ -228,8 +237,8 @@ def run_ours(args, cfg):
         pg = dist
     kind = args.strategy
     repl = args.repl or (2 if kind == "1.5d" else 1)
-    strat = cg.Strategy(kind, N, repl, args.block,
-                        reassociate=not args.reference_order and kind in ("1d", "1.5d"))
+    strat = cg.Strategy(kind, N, repl, args.block, reassociate=not args.reference_order,
+                        fuse=args.fuse)
 
     # NCCL bootstrap for the library's own communicators.
     nid = None
@@ -260,8 +269,9 @@ def run_ours(args, cfg):
     barrier()
 
     # ---- timed region: K epochs, device events on the trainer's stream -------
-    trainer.set_timing(True)
-    trainer.profile_reset()
+    # Each epoch is one replay of the CUDA graph captured from an epoch
+    # (kernels + NCCL collectives); the warm-up above ran the eager epoch and
+    # the capture.
     launches0 = cg.kernel_launches()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -272,22 +282,42 @@ def run_ours(args, cfg):
         end.record(stream)
         barrier()
     launches = cg.kernel_launches() - launches0
-    trainer.set_timing(False)
     losses = trainer.losses()
     ms_total = start.elapsed_time(end)
-    prof = trainer.profile()
 
     ms_t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
     if pg:
         pg.all_reduce(ms_t, op=pg.ReduceOp.MAX)
     ms_step = float(ms_t.item()) / args.steps
 
+    # ---- profiled region: the same K epochs eager, CUDA events per kernel ----
+    # (per-launch durations for the roofline; events cannot sit between the
+    # kernels of a replayed graph without serialising it).
+    trainer.set_timing(True)
+    trainer.profile_reset()
+    s1, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    s1.record(stream)
+    for _ in range(args.steps):
+        trainer.epoch_async()
+    e1.record(stream)
+    barrier()
+    trainer.set_timing(False)
+    prof = trainer.profile()
+    ms_prof_total = s1.elapsed_time(e1)
+    pt = torch.tensor([ms_prof_total], dtype=torch.float64, device="cuda")
+    if pg:
+        pg.all_reduce(pt, op=pg.ReduceOp.MAX)
+    eager_ms_step = float(pt.item()) / args.steps
+    trainer.run_epochs(2)  # re-capture the graph for what follows
+    barrier()
+
     # ---- the other propagation order, same trainer, same timing rules --------
     alt = None
-    if kind in ("1d", "1.5d") and not args.no_alt:
+    if not args.no_alt:
         lib_set = cg.lib.cagnet_trainer_set_option
         cg.check(lib_set(trainer.h, b"reassociate", int(not strat.reassociate)))
-        trainer.run_epochs(1)
+        trainer.run_epochs(2)  # eager epoch + graph capture
         barrier()
         s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s2.record(stream)
@@ -310,7 +340,8 @@ def run_ours(args, cfg):
     x_pin.numpy()[:] = feats
     lab_pin = torch.empty(r1 - r0, dtype=torch.int32, pin_memory=True)
     lab_pin.numpy()[:] = data.labels()[r0:r1]
-    trainer.step_host(x_pin.numpy(), lab_pin.numpy())  # warm
+    for _ in range(2):  # warm: eager epoch, then the graph capture
+        trainer.step_host(x_pin.numpy(), lab_pin.numpy())
     barrier()
     # Per-step wall time (each step_host returns after the loss D2H); the
     # median keeps one host hiccup out of the figure, the mean is reported too.
@@ -341,7 +372,7 @@ def run_ours(args, cfg):
                 "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": load_traffic(dom_name),
                 "bytes_per_launch": bytes_per_launch, "ms_per_launch": round(per_launch_ms, 4),
-                "share_of_step": round(dom["ms"] / max(ms_total, 1e-9), 4),
+                "share_of_step": round(dom["ms"] / max(ms_prof_total, 1e-9), 4),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
 
     if rank != 0:
@@ -371,6 +402,7 @@ def run_ours(args, cfg):
         "data": "synthetic",
         "config": {"workload": cfg["label"], "strategy": kind, "ranks": N, "repl": repl,
                    "block": args.block,
+                   "fuse": args.fuse, "cuda_graph": True,
                    "propagation": "narrow-first A^T (H W)" if strat.reassociate
                    else "reference order (A^T H) W",
                    "generator": cfg["generator"],
@@ -379,6 +411,7 @@ def run_ours(args, cfg):
                 "d2h_bytes_per_step": 8, "stat": "median of per-step wall times, max over ranks",
                 "mean_ms": round(e2e_mean, 4)},
         "gpu_launches": int(launches),
+        "eager_ms_per_step": round(eager_ms_step, 4),
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clk,
@@ -397,6 +430,8 @@ def run_ours(args, cfg):
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
+    if not args.sample_div:
+        args.sample_div = cfg.get("sample_div", 16)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

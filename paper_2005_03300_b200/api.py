@@ -55,11 +55,15 @@ class Strategy:
     repl: int = 1
     block: int = 0
     # Extension (not in the reference): narrow-first propagation Aᵀ(H W) for
-    # layers with f_out < f_in on the block-row strategies (1D / 1.5D).
+    # layers with f_out < f_in (1D / 1.5D: GEMM then SpMM; 2D / 3D: the
+    # row-group GEMM first, then SUMMA propagation of the f_out-wide tiles).
     reassociate: bool = False
     # Fused SpMM row epilogues (1D): 0 = off, 1 = ReLU / ⊙relu′ inside the
     # SpMM (default), 2 = also the small dense T·W / S·Wᵀ transforms.
     fuse: int = 1
+    # Replay each epoch after the first as a captured CUDA graph (kernels and
+    # NCCL collectives in one launch).
+    graph: bool = True
 
     @property
     def kind_id(self) -> int:
@@ -330,6 +334,7 @@ class Trainer:
         if strat.reassociate:
             check(lib.cagnet_trainer_set_option(self.h, b"reassociate", 1))
         check(lib.cagnet_trainer_set_option(self.h, b"fuse", int(strat.fuse)))
+        check(lib.cagnet_trainer_set_option(self.h, b"graph", int(strat.graph)))
 
     # lifecycle -------------------------------------------------------------
     def distribute(self):

@@ -81,6 +81,20 @@ class Comm {
                         cudaStream_t s);
 
   const CommCounter& counter(Category c) const { return counters_[static_cast<int>(c)]; }
+  // Ledger arithmetic for CUDA-graph replays: the counters metered while one
+  // epoch was captured are added again for every replay of that graph.
+  void snapshot(CommCounter* out) const {
+    for (int c = 0; c < kNumCategories; ++c) out[c] = counters_[c];
+  }
+  void add_delta(const CommCounter* before, const CommCounter* after) {
+    for (int c = 0; c < kNumCategories; ++c) {
+      counters_[c].messages += after[c].messages - before[c].messages;
+      counters_[c].words_sent += after[c].words_sent - before[c].words_sent;
+      counters_[c].words_received += after[c].words_received - before[c].words_received;
+      counters_[c].payload_words += after[c].payload_words - before[c].payload_words;
+      counters_[c].calls += after[c].calls - before[c].calls;
+    }
+  }
 
  private:
   ncclComm_t comm_for(const Group& g) const;

@@ -296,6 +296,11 @@ __global__ void f64_to_f32_kernel(const double* __restrict__ s, float* __restric
     d[e] = static_cast<float>(s[e]);
 }
 
+__global__ void push_loss_kernel(double* losses, int* slot, const double* partial) {
+  losses[*slot] = *partial;
+  *slot += 1;
+}
+
 unsigned grid_for(int64_t total) {
   const int sms = num_sms(current_device());
   int64_t b = ceil_div64(total > 0 ? total : 1, 256);
@@ -350,6 +355,11 @@ void relu(const float* Z, int64_t rows, int cols, int64_t ldz, float* H, int64_t
 void sgd(float* W, const float* Y, int64_t count, float lr, cudaStream_t stream) {
   if (count <= 0) return;
   sgd_kernel<<<grid_for(count), 256, 0, stream>>>(W, Y, count, lr);
+  CG_LAUNCH_CHECK();
+}
+
+void push_loss(double* losses, int* slot, const double* partial, cudaStream_t stream) {
+  push_loss_kernel<<<1, 1, 0, stream>>>(losses, slot, partial);
   CG_LAUNCH_CHECK();
 }
 

@@ -96,6 +96,9 @@ void logsoftmax_nll_blocks(const float* base, int parts, const int* widths, int6
 void relu(const float* Z, int64_t rows, int cols, int64_t ldz, float* H, int64_t ldh,
           cudaStream_t stream);
 void sgd(float* W, const float* Y, int64_t count, float lr, cudaStream_t stream);
+// losses[*slot] = *partial; ++*slot — the epoch's loss lands at a device-side
+// index, so a replayed CUDA graph of the epoch appends instead of overwriting.
+void push_loss(double* losses, int* slot, const double* partial, cudaStream_t stream);
 // g[r, c] *= 1[z[r, c] > 0]   (hadamard with relu_prime, dense.cpp:72-92)
 void mask_relu_prime(float* g, int64_t ldg, const float* z, int64_t ldz, int64_t rows,
                      int64_t cols, cudaStream_t stream);

@@ -71,6 +71,7 @@ class TrainerSumma final : public Trainer {
     for (auto& p : dpanel_) p.alloc(step_rows, fcols + chunk_slack);
     partial_.alloc(step_rows, fcols, -1, layers() * sub_step);
     tslice_.alloc(sub_step, fcols);
+    utile_.alloc(sub_step, fcols);
     strip_.alloc(fcols, fcols, fcols);
     gather_.alloc(side() * sub_step, fcols, fcols);
     CG_CUDA(cudaDeviceSynchronize());
@@ -87,34 +88,29 @@ class TrainerSumma final : public Trainer {
     const BlockRange mycur = tile_cols(rank_, wcur);
     const Mat& h = h_[static_cast<size_t>(l - 1)].m;
 
-    // Phase 1: partial = sum_q At[i, (q,k)] * H[(q,k), j]  (chunked panels in 2D).
-    Mat part{partial_.m.p, blockrow.size(), prevc.size(), padded_ld(prevc.size())};
-    propagate(at_parts_[0], /*transpose=*/true, h, chunks(prevc.size()), part);
-    Mat t = fiber_reduce_scatter(part, i);
-
-    // Phase 2: Z = sum_q T[i, q] * W[F_q, F_j].
     Mat z = z_[static_cast<size_t>(l - 1)].m;
     const bool last = l + 1 == num_layers();
-    int total_calls = 0;
-    for (int q = 0; q < side(); ++q) total_calls += static_cast<int>(chunks(block_range(wprev, side(), q).size()).size());
-    int calls = 0;
-    ms_after_cs();
-    for (int q = 0; q < side(); ++q) {
-      const BlockRange fq = block_range(wprev, side(), q);
-      const int troot = grid_.rank_at(i, q, k);
-      const std::vector<BlockRange> chs = chunks(fq.size());
-      const int b = next_buffer();
-      std::vector<Mat> pieces = dense_panel(grid_.row_group(rank_), troot, t, t.rows, fq.size(), chs, b);
-      for (size_t c = 0; c < chs.size(); ++c) {
-        ++calls;
-        const int epi = (calls == total_calls && !last) ? kern::EPI_RELU : kern::EPI_NONE;
-        gemm_aw(pieces[c], l - 1, fq.begin + chs[c].begin, mycur.begin, z, calls > 1, epi,
-                h_[static_cast<size_t>(l)].m);
-      }
-      release_buffer(b);
+    if (reassociate_ && wcur < wprev) {
+      // Narrow-first propagation Z = Aᵀ (H W): the row-group GEMM runs on H
+      // first (U tile: the rank's rows x column block j of f_out), so the
+      // SUMMA panels and the SpMM are f_out / √P wide instead of f_in / √P.
+      Mat u{utile_.m.p, h.rows, mycur.size(), padded_ld(mycur.size())};
+      row_gemm(h, l, wprev, mycur, u, false, Mat{});
+      Mat part{partial_.m.p, blockrow.size(), mycur.size(), padded_ld(mycur.size())};
+      propagate(at_parts_[0], /*transpose=*/true, u, chunks(mycur.size()), part);
+      Mat t = fiber_reduce_scatter(part, i);
+      kern::copy2d(z.p, z.ld, t.p, t.ld, t.rows, t.cols, cs_);
+      if (!last)
+        kern::relu(z.p, z.rows, static_cast<int>(z.cols), z.ld, h_[static_cast<size_t>(l)].m.p,
+                   h_[static_cast<size_t>(l)].m.ld, cs_);
+    } else {
+      // Phase 1: partial = sum_q At[i, (q,k)] * H[(q,k), j]  (chunked panels in 2D).
+      Mat part{partial_.m.p, blockrow.size(), prevc.size(), padded_ld(prevc.size())};
+      propagate(at_parts_[0], /*transpose=*/true, h, chunks(prevc.size()), part);
+      Mat t = fiber_reduce_scatter(part, i);
+      // Phase 2: Z = sum_q T[i, q] * W[F_q, F_j] (+ ReLU into H_l).
+      row_gemm(t, l, wprev, mycur, z, !last, h_[static_cast<size_t>(l)].m);
     }
-    if (total_calls == 0 && !last) kern::relu(z.p, z.rows, static_cast<int>(z.cols), z.ld,
-                                               h_[static_cast<size_t>(l)].m.p, h_[static_cast<size_t>(l)].m.ld, cs_);
 
     if (last) {
       // Whole rows of Z: gather the row group's column tiles (the reference's
@@ -198,6 +194,7 @@ class TrainerSumma final : public Trainer {
   }
 
  private:
+  void begin_epoch() override { slot_ = 0; }
   int side() const { return grid_.rows(); }
   int layers() const { return grid_.layers(); }
 
@@ -212,6 +209,36 @@ class TrainerSumma final : public Trainer {
     }
     for (int64_t s = 0; s < width; s += b) out.push_back(BlockRange{s, std::min(s + b, width)});
     return out;
+  }
+
+  // dst = sum_q src[rows, F_q] * W_{l-1}[F_q, cols] over the row group: the
+  // tiles of src (column blocks F_q of width f_in) are broadcast along the row
+  // (DBcast) and multiplied by the replicated weight slab; relu writes
+  // relu(dst) to relu_out after the last partial product.
+  void row_gemm(const Mat& src, int l, int64_t fin, const BlockRange& cols, Mat dst, bool relu,
+                Mat relu_out) {
+    const int i = grid_.row_of(rank_), k = grid_.layer_of(rank_);
+    int total_calls = 0;
+    for (int q = 0; q < side(); ++q) total_calls += static_cast<int>(chunks(block_range(fin, side(), q).size()).size());
+    int calls = 0;
+    ms_after_cs();
+    for (int q = 0; q < side(); ++q) {
+      const BlockRange fq = block_range(fin, side(), q);
+      const int troot = grid_.rank_at(i, q, k);
+      const std::vector<BlockRange> chs = chunks(fq.size());
+      const int b = next_buffer();
+      std::vector<Mat> pieces = dense_panel(grid_.row_group(rank_), troot, src, src.rows, fq.size(), chs, b);
+      for (size_t c = 0; c < chs.size(); ++c) {
+        ++calls;
+        const int epi = (calls == total_calls && relu) ? kern::EPI_RELU : kern::EPI_NONE;
+        gemm_aw(pieces[c], l - 1, fq.begin + chs[c].begin, cols.begin, dst, calls > 1, epi, relu_out);
+      }
+      release_buffer(b);
+    }
+    if (total_calls == 0) {
+      CG_CUDA(cudaMemsetAsync(dst.p, 0, dst.rows * dst.ld * sizeof(float), cs_));
+      if (relu) kern::relu(dst.p, dst.rows, static_cast<int>(dst.cols), dst.ld, relu_out.p, relu_out.ld, cs_);
+    }
   }
 
   // Double-buffered panel slots: a slot is reused only after the compute
@@ -320,7 +347,7 @@ class TrainerSumma final : public Trainer {
   std::vector<int64_t> shapes_;
   SparsePanel spanel_[2];
   OwnedMat dpanel_[2];
-  OwnedMat partial_, tslice_, strip_, gather_;
+  OwnedMat partial_, tslice_, strip_, gather_, utile_;
   uint64_t slot_ = 0;
 };
 

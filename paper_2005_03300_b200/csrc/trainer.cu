@@ -183,12 +183,15 @@ Trainer::Trainer(const DeviceDataset& data, std::vector<int64_t> dims, const dou
   loss_partial_.resize(1);
   CG_CUDA(cudaMemset(loss_partial_.get(), 0, sizeof(double)));
   losses_dev_.resize(4096);
+  loss_slot_.resize(1);
+  CG_CUDA(cudaMemset(loss_slot_.get(), 0, sizeof(int)));
 }
 
 Trainer::~Trainer() {
   cudaSetDevice(device_);
   if (cs_) cudaStreamSynchronize(cs_);
   if (ms_) cudaStreamSynchronize(ms_);
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   comm_.reset();
   for (cudaEvent_t e : {ev_cs_, ev_ms_, ev_t0_, ev_t1_, ev_ready_[0], ev_ready_[1], ev_free_[0], ev_free_[1]})
     if (e) cudaEventDestroy(e);
@@ -462,17 +465,65 @@ void Trainer::loss_all_reduce(double* partial_dev) {
   ms_after_cs();
   comm_->all_reduce(grid_.world(), partial_dev, 1, ncclFloat64, Category::Reduce, 1, ms_);
   cs_after_ms();
-  if (epochs_done_ - epochs_read_ >= static_cast<int>(losses_dev_.count)) flush_losses();
-  CG_CUDA(cudaMemcpyAsync(losses_dev_.get() + (epochs_done_ - epochs_read_), partial_dev,
-                          sizeof(double), cudaMemcpyDeviceToDevice, cs_));
+  kern::push_loss(losses_dev_.get(), loss_slot_.get(), partial_dev, cs_);
   ++epochs_done_;
+}
+
+void Trainer::epoch_body() {
+  begin_epoch();
+  for (int l = 1; l < num_layers(); ++l) forward_layer(l);
+  backward_and_step();
+  cs_after_ms();  // join the comm stream (graph capture needs every fork joined)
+}
+
+void Trainer::reset_graph() {
+  if (graph_exec_) {
+    CG_CUDA(cudaSetDevice(device_));
+    CG_CUDA(cudaStreamSynchronize(cs_));
+    CG_CUDA(cudaGraphExecDestroy(graph_exec_));
+    graph_exec_ = nullptr;
+  }
+  graph_warm_ = false;
 }
 
 void Trainer::epoch() {
   CG_CUDA(cudaSetDevice(device_));
+  if (epochs_done_ - epochs_read_ >= static_cast<int>(losses_dev_.count)) flush_losses();
+  // Per-kernel timing events stay eager (collect_profile reads every launch).
+  if (!use_graph_ || timing_ || !graph_warm_) {
+    // Eager.  The first graph-mode epoch is eager too: lazy allocations
+    // (split tables, workspaces) and kernel attributes happen outside capture.
+    CG_CUDA(cudaEventRecord(ev_t0_, cs_));
+    epoch_body();
+    CG_CUDA(cudaEventRecord(ev_t1_, cs_));
+    if (use_graph_ && !timing_) graph_warm_ = true;
+    return;
+  }
+  if (!graph_exec_) {
+    comm_->snapshot(ledger_before_);
+    const uint64_t k0 = launch_counter().load();
+    CG_CUDA(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeRelaxed));
+    try {
+      epoch_body();
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(cs_, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaGraph_t g = nullptr;
+    CG_CUDA(cudaStreamEndCapture(cs_, &g));
+    CG_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
+    CG_CUDA(cudaGraphDestroy(g));
+    comm_->snapshot(ledger_after_);  // the capture metered this epoch once
+    graph_kernels_ = launch_counter().load() - k0;
+  } else {
+    comm_->add_delta(ledger_before_, ledger_after_);
+    launch_counter().fetch_add(graph_kernels_);  // the replay runs the captured kernels
+    ++epochs_done_;
+  }
   CG_CUDA(cudaEventRecord(ev_t0_, cs_));
-  for (int l = 1; l < num_layers(); ++l) forward_layer(l);
-  backward_and_step();
+  CG_CUDA(cudaGraphLaunch(graph_exec_, cs_));
   CG_CUDA(cudaEventRecord(ev_t1_, cs_));
 }
 
@@ -480,8 +531,10 @@ void Trainer::flush_losses() {
   sync();
   const int pending = epochs_done_ - epochs_read_;
   std::vector<double> tot(static_cast<size_t>(pending));
-  if (pending)
+  if (pending) {
     CG_CUDA(cudaMemcpy(tot.data(), losses_dev_.get(), pending * sizeof(double), cudaMemcpyDeviceToHost));
+    CG_CUDA(cudaMemset(loss_slot_.get(), 0, sizeof(int)));
+  }
   for (double t : tot) losses_host_.push_back(t / static_cast<double>(train_total_));
   epochs_read_ = epochs_done_;
 }

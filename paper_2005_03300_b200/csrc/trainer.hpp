@@ -76,8 +76,16 @@ class Trainer {
   virtual BlockRange tile_cols(int rank, int64_t width) const = 0;
   virtual int tile_owner(int rank) const { return rank; }
 
-  // dist_common.cpp:97-100.  Losses stay on the device until read.
+  // dist_common.cpp:97-100.  Losses stay on the device until read.  With
+  // graphs on, the second and later epochs replay a CUDA graph captured from
+  // one epoch (kernels, NCCL collectives, cross-stream events): one launch per
+  // epoch, immune to host scheduling jitter between ranks.
   void epoch();
+  void set_graph(bool on) {
+    if (on != use_graph_) reset_graph();
+    use_graph_ = on;
+  }
+  bool graph() const { return use_graph_; }
   std::vector<double> run_epochs(int epochs);
   double last_loss();
   void flush_losses();
@@ -106,15 +114,24 @@ class Trainer {
     int64_t launches = 0;
     double ms = 0, bytes = 0, flops = 0;
   };
-  void set_timing(bool on) { timing_ = on; }
-  // Narrow-first propagation Aᵀ(H W) when f_out < f_in (block-row strategies).
-  void set_reassociate(bool on) { reassociate_ = on; }
+  void set_timing(bool on) {
+    if (on != timing_) reset_graph();
+    timing_ = on;
+  }
+  // Narrow-first propagation Aᵀ(H W) when f_out < f_in (every strategy).
+  void set_reassociate(bool on) {
+    if (on != reassociate_) reset_graph();
+    reassociate_ = on;
+  }
   bool reassociate() const { return reassociate_; }
   // Fused SpMM row epilogues (block-row strategies, 1D): 0 = none,
   // 1 = elementwise (ReLU, ⊙relu′; default), 2 = also the small dense
   // transforms (T·W, S·Wᵀ) — per-row W reads compete with the gathers for
   // the L1 data pipe, so level 2 is slower on B200 and kept for comparison.
-  void set_fuse(int level) { fuse_ = level; }
+  void set_fuse(int level) {
+    if (level != fuse_) reset_graph();
+    fuse_ = level;
+  }
   int fuse() const { return fuse_; }
   void reset_profile() {
     collect_profile();
@@ -129,6 +146,11 @@ class Trainer {
   double step_host(const float* x_tile, const int32_t* labels_tile);
 
  protected:
+  void epoch_body();  // one epoch's launches (eager or under capture)
+  void reset_graph();
+  // Per-epoch reset of strategy-private host state so every epoch issues the
+  // identical launch sequence (required for graph replay).
+  virtual void begin_epoch() {}
   // --- helpers shared by the strategies ---
   void init_tiles();  // h/z/g tile shapes from tile_rows/tile_cols, labels, H0
   void ms_after_cs();
@@ -195,6 +217,12 @@ class Trainer {
   std::map<std::pair<const void*, int>, DevBuf<int64_t>> splits_;
   static double l2_panel_bytes();
   DevBuf<double> losses_dev_;
+  DevBuf<int> loss_slot_;  // device-side write index into losses_dev_
+  bool use_graph_ = false;
+  bool graph_warm_ = false;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  uint64_t graph_kernels_ = 0;  // kernels per replay (added to the launch counter)
+  CommCounter ledger_before_[kNumCategories], ledger_after_[kNumCategories];
   int epochs_done_ = 0;
   int epochs_read_ = 0;
   std::vector<double> losses_host_;

@@ -55,7 +55,7 @@ def test_single_rank_matches_serial(cg, orc, strat):
     assert all(v == 0 for c in led.values() for v in c.values())  # P = 1 meters nothing
 
 
-@pytest.mark.parametrize("kind", ["1d", "1.5d"])
+@pytest.mark.parametrize("kind", ["1d", "1.5d", "2d", "3d"])
 @pytest.mark.parametrize("fuse", [0, 1, 2])
 @pytest.mark.parametrize("dims", [[40, 12, 7, 5], [40, 16, 16, 24], [20, 16, 41]])
 def test_reassociated_matches_serial(cg, orc, kind, fuse, dims):
@@ -68,6 +68,30 @@ def test_reassociated_matches_serial(cg, orc, kind, fuse, dims):
     losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.25, 3)
     out = run_single(cg, data, model, cg.Strategy(kind, 1, 1, 0, reassociate=True, fuse=fuse), 3)
     assert max_rel_error(out, losses, h, y, g, w) < TOL
+
+
+@pytest.mark.parametrize("kind", ["1d", "2d", "3d"])
+def test_graph_replay_matches_eager(cg, kind):
+    """Epochs replayed from the captured CUDA graph are bit-identical to the
+    eager epochs (same kernels, same order); losses land at the device-side
+    slot, so every replay appends its own loss."""
+    dims = [40, 16, 16, 24]
+    data = cg.generate_dataset(96, 9.0, dims[0], dims[-1], 7, 8, 9)
+    model = cg.init_glorot(dims, 3, 0.25)
+    outs = []
+    for graph in (False, True):
+        t = cg.make_trainer(data, model, cg.Strategy(kind, 1, 1, 0, reassociate=True,
+                                                     graph=graph))
+        t.distribute()
+        losses = t.run_epochs(6)
+        more = [t.epoch() for _ in range(3)]
+        outs.append((np.concatenate([losses, more]), [t.weight(l) for l in range(len(dims) - 1)],
+                     t.h_tile(len(dims) - 1)))
+    (l0, w0, h0), (l1, w1, h1) = outs
+    assert len(l1) == 9 and len(set(np.round(l1, 12))) > 1
+    assert np.array_equal(l0, l1)
+    assert all(np.array_equal(a, b) for a, b in zip(w0, w1))
+    assert np.array_equal(h0, h1)
 
 
 def test_pinned_loss_trace_fp32(cg):
@@ -152,8 +176,11 @@ DIST = {  # name -> (kind, P, repl, block, n, dims)   (tests/golden/make_golden.
 
 
 @pytest.mark.multigpu
-@pytest.mark.parametrize("kind,P,repl", [("1d", 2, 1), ("1.5d", 4, 2), ("1d", 4, 1)])
+@pytest.mark.parametrize("kind,P,repl", [("1d", 2, 1), ("1.5d", 4, 2), ("1d", 4, 1), ("2d", 4, 1),
+                                        ("3d", 8, 1)])
 def test_distributed_reassociated(cg, orc, need_gpus, kind, P, repl):
+    """Narrow-first propagation on every strategy (2D/3D: row-group GEMM
+    first, then SUMMA propagation of the f_out-wide U tiles)."""
     need_gpus(P)
     dims = [24, 8, 6]
     model = cg.init_glorot(dims, 5, 0.5)
