@@ -64,6 +64,9 @@ class Strategy:
     # Replay each epoch after the first as a captured CUDA graph (kernels and
     # NCCL collectives in one launch).
     graph: bool = True
+    # 2D / 3D: sparse tiles broadcast once in distribute() and kept resident
+    # (False: the reference's per-stage sparse broadcasts and ledger).
+    resident_sparse: bool = True
 
     @property
     def kind_id(self) -> int:
@@ -335,6 +338,8 @@ class Trainer:
             check(lib.cagnet_trainer_set_option(self.h, b"reassociate", 1))
         check(lib.cagnet_trainer_set_option(self.h, b"fuse", int(strat.fuse)))
         check(lib.cagnet_trainer_set_option(self.h, b"graph", int(strat.graph)))
+        check(lib.cagnet_trainer_set_option(self.h, b"resident_sparse",
+                                            int(strat.resident_sparse)))
 
     # lifecycle -------------------------------------------------------------
     def distribute(self):

@@ -126,6 +126,29 @@ void Comm::all_gather(const Group& g, const void* send, void* recv, size_t slice
   c.messages += g.size() - 1;
 }
 
+void Comm::bcast_all(const Group& g, void* buf, size_t slice_count, ncclDataType_t t,
+                     Category cat, const std::vector<uint64_t>& words, cudaStream_t s) {
+  const int member = g.index_of(rank_);
+  if (g.size() == 1) return;
+  const size_t esize = (t == ncclInt64 || t == ncclUint64 || t == ncclFloat64) ? 8 : 4;
+  char* base = static_cast<char*>(buf);
+  if (slice_count)
+    CG_NCCL(ncclAllGather(base + static_cast<size_t>(member) * slice_count * esize, buf, slice_count,
+                          t, comm_for(g), s));
+  CommCounter& c = ctr(cat);
+  for (int q = 0; q < g.size(); ++q) {
+    const uint64_t w = words.at(static_cast<size_t>(q));
+    c.calls += 1;
+    c.payload_words += w;
+    if (q == member) {
+      c.words_sent += w * (g.size() - 1);
+      c.messages += g.size() - 1;
+    } else {
+      c.words_received += w;
+    }
+  }
+}
+
 void Comm::setup_all_gather(const void* send, void* recv, size_t count, ncclDataType_t t,
                             cudaStream_t s) {
   if (ranks_ == 1) {

@@ -68,6 +68,13 @@ class Comm {
                   ncclDataType_t t, Category cat, const std::vector<uint64_t>& slot_words,
                   cudaStream_t s);
 
+  // Every member broadcasts its slot of `buf` (slot q = [q * slice_count,
+  // (q + 1) * slice_count) elements) to the group: ONE in-place ncclAllGather,
+  // metered exactly like the reference's g.size() broadcasts with roots in
+  // member order and payloads words[q] (same ledger, NVLS/ring-optimal data path).
+  void bcast_all(const Group& g, void* buf, size_t slice_count, ncclDataType_t t, Category cat,
+                 const std::vector<uint64_t>& words, cudaStream_t s);
+
   // Fuse the collectives issued in between into one NCCL launch.
   void group_start() {
     if (ranks_ > 1) CG_NCCL(ncclGroupStart());
@@ -85,6 +92,9 @@ class Comm {
   // epoch was captured are added again for every replay of that graph.
   void snapshot(CommCounter* out) const {
     for (int c = 0; c < kNumCategories; ++c) out[c] = counters_[c];
+  }
+  void restore(const CommCounter* in) {
+    for (int c = 0; c < kNumCategories; ++c) counters_[c] = in[c];
   }
   void add_delta(const CommCounter* before, const CommCounter* after) {
     for (int c = 0; c < kNumCategories; ++c) {

@@ -5,6 +5,8 @@
 // embedding panels down its column group, and the per-column partials meet in
 // a row all-reduce.  Broadcast panels are double-buffered on the comm stream
 // so stage q+1's NCCL broadcast overlaps stage q's SpMM.
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "trainer.hpp"
 
@@ -44,7 +46,8 @@ class TrainerRows final : public Trainer {
       c_hi_ = block_range(data_.n, blocks(), chunk_end(j) - 1).end;
       a_chunk_ = extract_block_device(data_.adj, rows.begin, rows.end, c_lo_, c_hi_, cs_);
       at_chunk_ = extract_block_device(data_.adj_t, rows.begin, rows.end, c_lo_, c_hi_, cs_);
-      gbuf_.alloc(c_hi_ - c_lo_, kCoalesceMaxF);
+      // Rows for whole padded slots (the 1D all-gather writes P equal slots).
+      gbuf_.alloc(std::max(c_hi_ - c_lo_, ceil_div64(data_.n, blocks()) * blocks()), kCoalesceMaxF);
     }
     CG_CUDA(cudaDeviceSynchronize());
   }
@@ -245,13 +248,23 @@ class TrainerRows final : public Trainer {
         const BlockRange r = block_range(data_.n, blocks(), own);
         kern::copy2d(g.p + (r.begin - c_lo_) * g.ld, g.ld, mine.p, mine.ld, mine.rows, mine.cols, ms_);
       }
-      comm_->group_start();
-      for (int q = chunk_begin(j); q < chunk_end(j); ++q) {
-        const BlockRange r = block_range(data_.n, blocks(), q);
-        const int root = one_d() ? q : grid_.rank_at(q, j);
-        bcast_mat(grp, root, Mat{g.p + (r.begin - c_lo_) * g.ld, r.size(), g.cols, g.ld}, Category::DBcast);
+      if (one_d()) {
+        // 1D: every rank roots one stage, so the P broadcasts are an
+        // all-gather of the panel slots (ceil-rule blocks = equal padded slots).
+        const int64_t step = ceil_div64(data_.n, blocks());
+        std::vector<uint64_t> words;
+        for (int q = 0; q < blocks(); ++q)
+          words.push_back(static_cast<uint64_t>(block_range(data_.n, blocks(), q).size() * g.cols));
+        comm_->bcast_all(grp, g.p, static_cast<size_t>(step * g.ld), ncclFloat32, Category::DBcast, words, ms_);
+      } else {
+        comm_->group_start();
+        for (int q = chunk_begin(j); q < chunk_end(j); ++q) {
+          const BlockRange r = block_range(data_.n, blocks(), q);
+          const int root = grid_.rank_at(q, j);
+          bcast_mat(grp, root, Mat{g.p + (r.begin - c_lo_) * g.ld, r.size(), g.cols, g.ld}, Category::DBcast);
+        }
+        comm_->group_end();
       }
-      comm_->group_end();
       cs_after_ms();
       spmm(blk, g, out, false, epi);
       return;

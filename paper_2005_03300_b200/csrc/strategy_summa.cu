@@ -22,6 +22,7 @@ struct SparsePanel {
   DevBuf<int64_t> row_ptr;
   DevBuf<int32_t> col;
   DevBuf<float> vals;
+  int64_t rows = 0, cols = 0, nnz = 0;
 };
 
 class TrainerSumma final : public Trainer {
@@ -62,6 +63,48 @@ class TrainerSumma final : public Trainer {
       sp.col.resize(static_cast<size_t>(max_nnz));
       sp.vals.resize(static_cast<size_t>(max_nnz));
     }
+    // Resident sparse panels: the A / Aᵀ tiles of this rank's row group never
+    // change, so they move once here (unmetered setup, like distribute())
+    // instead of once per SpMM stage (the reference's SBcast).  The dense
+    // H / G / T / S panels still move every layer.
+    resident_[0].clear();
+    resident_[1].clear();
+    if (resident_sparse_ && side() > 1) {
+      CommCounter saved[kNumCategories];
+      comm_->snapshot(saved);
+      ms_after_cs();
+      for (int o = 0; o < 2; ++o) {
+        const DeviceCsr& local = o == 0 ? a_parts_[0] : at_parts_[0];
+        for (int q = 0; q < side(); ++q) {
+          const int aroot = grid_.rank_at(i, q, k);
+          const int64_t* sh = &shapes_[static_cast<size_t>(4 * aroot)];
+          SparsePanel sp;
+          const int64_t nnz = o == 0 ? sh[2] : sh[3];
+          sp.rows = sh[0];
+          sp.cols = sh[1];
+          sp.nnz = nnz;
+          sp.row_ptr.resize(static_cast<size_t>(sh[0] + 1));
+          sp.col.resize(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+          sp.vals.resize(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
+          if (aroot == rank_) {
+            CG_CUDA(cudaMemcpyAsync(sp.row_ptr.get(), local.row_ptr.get(), (sh[0] + 1) * sizeof(int64_t),
+                                    cudaMemcpyDeviceToDevice, ms_));
+            if (nnz) {
+              CG_CUDA(cudaMemcpyAsync(sp.col.get(), local.col_idx.get(), nnz * sizeof(int32_t),
+                                      cudaMemcpyDeviceToDevice, ms_));
+              CG_CUDA(cudaMemcpyAsync(sp.vals.get(), local.vals.get(), nnz * sizeof(float),
+                                      cudaMemcpyDeviceToDevice, ms_));
+            }
+          }
+          comm_->bcast_csr(grid_.row_group(rank_), aroot, sp.row_ptr.get(), sh[0], sp.col.get(),
+                           sp.vals.get(), nnz, Category::SBcast, ms_);
+          resident_[o].push_back(std::move(sp));
+        }
+      }
+      CG_CUDA(cudaStreamSynchronize(ms_));
+      comm_->restore(saved);
+    }
+
     const int64_t step_rows = ceil_div64(std::max<int64_t>(data_.n, 1), side());  // vertex block
     const int64_t sub_step = ceil_div64(std::max<int64_t>(step_rows, 1), layers());
     const int64_t fcols = ceil_div64(maxf, side());
@@ -72,6 +115,8 @@ class TrainerSumma final : public Trainer {
     partial_.alloc(step_rows, fcols, -1, layers() * sub_step);
     tslice_.alloc(sub_step, fcols);
     utile_.alloc(sub_step, fcols);
+    pfull_.alloc(sub_step, maxf);
+    redbuf_.alloc(static_cast<int64_t>(side()) * sub_step, fcols);
     strip_.alloc(fcols, fcols, fcols);
     gather_.alloc(side() * sub_step, fcols, fcols);
     CG_CUDA(cudaDeviceSynchronize());
@@ -94,8 +139,7 @@ class TrainerSumma final : public Trainer {
       // Narrow-first propagation Z = Aᵀ (H W): the row-group GEMM runs on H
       // first (U tile: the rank's rows x column block j of f_out), so the
       // SUMMA panels and the SpMM are f_out / √P wide instead of f_in / √P.
-      Mat u{utile_.m.p, h.rows, mycur.size(), padded_ld(mycur.size())};
-      row_gemm(h, l, wprev, mycur, u, false, Mat{});
+      Mat u = row_gemm_reduce(h, l, wprev, wcur);
       Mat part{partial_.m.p, blockrow.size(), mycur.size(), padded_ld(mycur.size())};
       propagate(at_parts_[0], /*transpose=*/true, u, chunks(mycur.size()), part);
       Mat t = fiber_reduce_scatter(part, i);
@@ -241,6 +285,33 @@ class TrainerSumma final : public Trainer {
     }
   }
 
+  // Narrow-first U[rows, F_j(f_out)] = sum_q H[rows, F_q(f_in)] W[F_q, F_j]:
+  // every rank multiplies its own H column block by its W row slab for all
+  // f_out columns and the row group reduce-scatters the f_out column blocks,
+  // so f_out-wide partials move instead of the f_in-wide H tiles.
+  Mat row_gemm_reduce(const Mat& h, int l, int64_t fin, int64_t fout) {
+    const int j = grid_.col_of(rank_);
+    const BlockRange myin = block_range(fin, side(), j);
+    const int64_t rows = h.rows;
+    const int64_t wslot = ceil_div64(fout, side());
+    const int64_t ld = padded_ld(wslot);
+    Mat full{pfull_.m.p, rows, fout, padded_ld(fout)};
+    gemm_aw(h, l - 1, myin.begin, 0, full, false, kern::EPI_NONE, Mat{});
+    if (side() == 1) return full;
+    std::vector<uint64_t> slot_words;
+    for (int q = 0; q < side(); ++q) {
+      const BlockRange oq = block_range(fout, side(), q);
+      slot_words.push_back(static_cast<uint64_t>(rows * oq.size()));
+      if (oq.size() > 0)
+        kern::copy2d(redbuf_.m.p + q * rows * ld, ld, full.p + oq.begin, full.ld, rows, oq.size(), cs_);
+    }
+    ms_after_cs();
+    comm_->reduce_scatter(grid_.row_group(rank_), redbuf_.m.p, utile_.m.p, static_cast<size_t>(rows * ld),
+                          ncclFloat32, Category::Reduce, slot_words, ms_);
+    cs_after_ms();
+    return Mat{utile_.m.p, rows, block_range(fout, side(), j).size(), ld};
+  }
+
   // Double-buffered panel slots: a slot is reused only after the compute
   // stream finished with its previous contents.
   int next_buffer() {
@@ -293,7 +364,15 @@ class TrainerSumma final : public Trainer {
       const int32_t* ci;
       const float* vv;
       int64_t arows, acols, annz;
-      if (aroot == rank_) {
+      if (!resident_[transpose ? 1 : 0].empty()) {
+        const SparsePanel& sp = resident_[transpose ? 1 : 0][static_cast<size_t>(q)];
+        rp = sp.row_ptr.get();
+        ci = sp.col.get();
+        vv = sp.vals.get();
+        arows = sp.rows;
+        acols = sp.cols;
+        annz = sp.nnz;
+      } else if (aroot == rank_) {
         rp = local.row_ptr.get();
         ci = local.col_idx.get();
         vv = local.vals.get();
@@ -346,8 +425,9 @@ class TrainerSumma final : public Trainer {
 
   std::vector<int64_t> shapes_;
   SparsePanel spanel_[2];
+  std::vector<SparsePanel> resident_[2];  // [A, Aᵀ][q]: row-group tiles kept in HBM
   OwnedMat dpanel_[2];
-  OwnedMat partial_, tslice_, strip_, gather_, utile_;
+  OwnedMat partial_, tslice_, strip_, gather_, utile_, pfull_, redbuf_;
   uint64_t slot_ = 0;
 };
 

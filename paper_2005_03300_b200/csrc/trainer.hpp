@@ -133,6 +133,10 @@ class Trainer {
     fuse_ = level;
   }
   int fuse() const { return fuse_; }
+  // SUMMA (2D/3D): keep the row group's sparse tiles resident after
+  // distribute() instead of re-broadcasting them every SpMM stage.  Set before
+  // distribute(); off reproduces the reference's per-stage SBcast ledger.
+  void set_resident_sparse(bool on) { resident_sparse_ = on; }
   void reset_profile() {
     collect_profile();
     profile_.clear();
@@ -189,6 +193,7 @@ class Trainer {
   bool timing_ = false;
   bool reassociate_ = false;
   int fuse_ = 1;
+  bool resident_sparse_ = true;
   std::vector<ProfRec> recs_;
   size_t recs_used_ = 0;
   std::vector<ProfEntry> profile_;

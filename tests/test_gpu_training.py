@@ -194,13 +194,37 @@ def test_distributed_reassociated(cg, orc, need_gpus, kind, P, repl):
 
 
 @pytest.mark.multigpu
+@pytest.mark.parametrize("kind,P", [("2d", 4), ("3d", 8)])
+def test_resident_sparse_tiles(cg, need_gpus, kind, P):
+    """SUMMA with the sparse tiles kept resident after distribute(): the same
+    numbers bit for bit, and no per-epoch sparse broadcast in the ledger."""
+    need_gpus(P)
+    dims = [8, 6, 4]
+    model = cg.init_glorot(dims, 14, 0.5)
+    outs = []
+    for resident in (False, True):
+        outs.append(cg.run_distributed(
+            lambda dev: cg.generate_dataset(18, 4.0, dims[0], dims[-1], 11, 12, 13, device=dev),
+            model, cg.Strategy(kind, P, 1, 0, resident_sparse=resident), 3))
+    a, b = outs
+    assert np.array_equal(a.losses, b.losses)
+    assert np.array_equal(a.h_final, b.h_final)
+    for r in range(P):
+        assert b.ledger[r]["sbcast"]["calls"] == 0
+        assert a.ledger[r]["sbcast"]["calls"] > 0
+        for cat in ("dbcast", "reduce", "allgather"):
+            assert a.ledger[r][cat] == b.ledger[r][cat]
+
+
+@pytest.mark.multigpu
 @pytest.mark.parametrize("name", list(DIST))
 def test_distributed_matches_reference(cg, need_gpus, name):
     kind, P, repl, block, n, dims = DIST[name]
     need_gpus(P)
     gd = np.load(os.path.join(GOLD, "reference_dist.npz"))
     model = cg.init_glorot(dims, 14, 0.5)
-    strat = cg.Strategy(kind, P, repl, block)
+    # The reference's own communication schedule (per-stage sparse broadcasts).
+    strat = cg.Strategy(kind, P, repl, block, resident_sparse=False)
     out = cg.run_distributed(lambda dev: cg.generate_dataset(n, 4.0, dims[0], dims[-1], 11, 12, 13,
                                                              device=dev), model, strat, 3)
     L = len(dims)
