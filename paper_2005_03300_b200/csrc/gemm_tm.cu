@@ -735,8 +735,31 @@ void dump_trace(const TmParams& p, cudaStream_t s, const char* what) {
 
 }  // namespace
 
+bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream);
+
+// N > 64 (e.g. Protein's 256 classes): column tiles of 64, each a full
+// gemm_tm launch on the matching B / C / aux column slices (A is re-read
+// once per tile; the output stream dominates these shapes).
+bool gemm_tm_wide(const GemmDesc& d, cudaStream_t stream) {
+  for (int64_t c0 = 0; c0 < d.n; c0 += 64) {
+    GemmDesc t = d;
+    t.n = d.n - c0 < 64 ? d.n - c0 : 64;
+    t.B = d.B + c0 * d.b_sn;
+    t.C = d.C + c0;
+    if (d.aux) t.aux = d.aux + c0;
+    if (d.aux_out) t.aux_out = d.aux_out + c0;
+    // Every slice must take the tensor-core path; check the first one.
+    if (!gemm_tm_try(t, stream)) {
+      if (c0 == 0) return false;
+      throw std::logic_error("gemm_tm: column tile rejected after the first");
+    }
+  }
+  return true;
+}
+
 bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
-  if (d.m <= 0 || d.n <= 0 || d.k <= 0 || d.n > 64) return false;
+  if (d.m <= 0 || d.n <= 0 || d.k <= 0) return false;
+  if (d.n > 64) return gemm_tm_wide(d, stream);
   if (!aligned16(d.A)) return false;
   const int bn = d.n <= 16 ? 16 : d.n <= 32 ? 32 : d.n <= 48 ? 48 : 64;
   const int sms = num_sms(current_device());

@@ -239,8 +239,26 @@ void Trainer::cs_after_ms() {
 }
 
 bool Trainer::spmm_single_pass(const DeviceCsr& a, const Mat& h) const {
+  return spmm_passes(a, h) <= 1;
+}
+
+// L2-aware column blocking (SURVEY §7 hard parts).  One pass per column block
+// keeps the gathered H slice L2-resident, but every pass re-reads the row
+// segments and read-modify-writes the n_rows x f output, so it only pays when
+// rows carry many nonzeros per pass.  Measured on B200 (scripts/tune_spmm_big.py):
+// Amazon-shaped (17 nnz/row, 912 MB panel) is fastest unblocked (5.6 ms vs
+// 17 ms in 12 passes); Protein-shaped (150 nnz/row, 560 MB) at ~47 MB panels
+// (15.6 ms vs 24.6 ms unblocked) — the effective L2 capacity for random 64 B
+// gathers is about half the nominal 126 MB.
+int Trainer::spmm_passes(const DeviceCsr& a, const Mat& h) const {
+  if (a.nnz == 0 || a.n_rows == 0) return 1;
   const double panel = static_cast<double>(a.n_cols) * h.cols * 4.0;
-  return a.nnz == 0 || std::ceil(panel / l2_panel_bytes()) <= 1.0;
+  const double per_row = static_cast<double>(a.nnz) / static_cast<double>(a.n_rows);
+  int nb = static_cast<int>(std::min<double>(64.0, std::ceil(panel / l2_panel_bytes())));
+  // Keep >= 12 nonzeros per row per pass; below ~64 per row blocking loses.
+  if (per_row < 64.0) return 1;
+  nb = std::min<int>(nb, static_cast<int>(per_row / 12.0));
+  return nb < 1 ? 1 : nb;
 }
 
 void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi) {
@@ -251,8 +269,7 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const ke
   // L2-aware column blocking: when the gathered panel H (n_cols x f) does not
   // fit the L2 budget, run one pass per column block so every pass gathers
   // from an L2-resident slice (SURVEY §7 hard parts).
-  const double panel = static_cast<double>(a.n_cols) * h.cols * 4.0;
-  const int nb = static_cast<int>(std::min<double>(64.0, std::ceil(panel / l2_panel_bytes())));
+  const int nb = spmm_passes(a, h);
   if (epi) {
     if (acc || nb > 1) throw std::logic_error("spmm: fused epilogue needs one final pass");
     spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, false, epi);
@@ -262,19 +279,26 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const ke
     spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, acc);
     return;
   }
+  // Column blocks materialised once per (matrix, pass count) as contiguous
+  // CSR copies: each pass then streams its own nonzeros (row segments of the
+  // full CSR would be ~50 B scattered DRAM reads per row and pass).
   auto key = std::make_pair(static_cast<const void*>(a.row_ptr.get()), nb);
-  auto it = splits_.find(key);
-  if (it == splits_.end()) {
-    DevBuf<int64_t> tbl(static_cast<size_t>((nb + 1) * a.n_rows));
-    kern::column_splits(a.n_rows, a.n_cols, nb, a.row_ptr.get(), a.col_idx.get(), tbl.get(), cs_);
-    it = splits_.emplace(key, std::move(tbl)).first;
+  auto it = colblocks_.find(key);
+  if (it == colblocks_.end()) {
+    std::vector<DeviceCsr> blocks;
+    for (int b = 0; b < nb; ++b) {
+      const BlockRange cr = block_range(a.n_cols, nb, b);
+      blocks.push_back(extract_block_device(a, 0, a.n_rows, cr.begin, cr.end, cs_));
+    }
+    it = colblocks_.emplace(key, std::move(blocks)).first;
   }
-  const int64_t* split = it->second.get();
   const int slot = prof_begin();
-  for (int b = 0; b < nb; ++b)
-    kern::spmm_segments(a.n_rows, split + b * a.n_rows, split + (b + 1) * a.n_rows, a.col_idx.get(),
-                        a.vals.get(), h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld,
-                        acc || b > 0, cs_, a.nnz / nb);
+  for (int b = 0; b < nb; ++b) {
+    const DeviceCsr& blk = it->second[static_cast<size_t>(b)];
+    const BlockRange cr = block_range(a.n_cols, nb, b);
+    kern::spmm_csr(blk.n_rows, blk.row_ptr.get(), blk.col_idx.get(), blk.vals.get(), h.p + cr.begin * h.ld,
+                   h.ld, static_cast<int>(h.cols), out.p, out.ld, acc || b > 0, cs_, blk.nnz);
+  }
   if (slot >= 0) {
     const double f = static_cast<double>(h.cols), r = static_cast<double>(a.n_rows);
     const double bytes = 8.0 * (r + 1) + 8.0 * a.nnz + 4.0 * f * h.rows + 4.0 * f * r * (acc ? 2 : 1);
@@ -285,7 +309,7 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const ke
 double Trainer::l2_panel_bytes() {
   static const double v = [] {
     const char* e = std::getenv("CAGNET_L2_PANEL_MB");
-    return (e ? std::atof(e) : 96.0) * 1048576.0;
+    return (e ? std::atof(e) : 48.0) * 1048576.0;
   }();
   return v > 0 ? v : 1e30;
 }

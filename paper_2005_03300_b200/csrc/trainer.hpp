@@ -167,6 +167,7 @@ class Trainer {
                 const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi = nullptr);
   // True when spmm(a, h, ...) is a single kernel pass (no L2 column blocking).
   bool spmm_single_pass(const DeviceCsr& a, const Mat& h) const;
+  int spmm_passes(const DeviceCsr& a, const Mat& h) const;
   // C (+)= A · W[r0:r0+k, c0:c0+n]
   void gemm_aw(const Mat& a, int l, int64_t r0, int64_t c0, Mat c, bool acc, int epi,
                Mat aux_out);
@@ -218,8 +219,9 @@ class Trainer {
   std::vector<DeviceCsr> a_parts_, at_parts_;
   DevBuf<double> loss_partial_;
   DevBuf<float> stage_;  // host-input staging for step_host
-  // Column-block split tables of the local CSR parts, keyed by (row_ptr, blocks).
-  std::map<std::pair<const void*, int>, DevBuf<int64_t>> splits_;
+  // Column blocks of the local CSR parts for L2-blocked SpMM passes, keyed by
+  // (row_ptr, blocks).
+  std::map<std::pair<const void*, int>, std::vector<DeviceCsr>> colblocks_;
   static double l2_panel_bytes();
   DevBuf<double> losses_dev_;
   DevBuf<int> loss_slot_;  // device-side write index into losses_dev_

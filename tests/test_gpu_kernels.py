@@ -171,6 +171,9 @@ TM_CASES = [
     (16, 41, 30000, 1, 0),     # Hᵀ·S, m < 128 (OOB-filled tile), BN = 48
     (300, 24, 12345, 1, 0),    # ragged K
     (16, 16, 100, 1, 0),       # K smaller than one k-block per split
+    (3000, 256, 16, 0, 0),     # N > 64: column tiles (Protein's 256 classes)
+    (3000, 16, 256, 0, 1),     # S·Wᵀ with K = 256
+    (16, 200, 30000, 1, 0),    # Hᵀ·S with N > 64 (ragged last column tile)
 ]
 
 
