@@ -47,9 +47,11 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;
-constexpr int kConv = 128;                // converter threads (warps 2-5)
-constexpr int kEpi = 128;                 // epilogue threads (warps 6-9)
-constexpr int kThreads = 64 + kConv + kEpi;
+constexpr int kConv = 128;                // converter threads per group
+constexpr int kConvGroups = 2;            // groups take alternate k-blocks (warps 2-5, 6-9)
+constexpr int kEpi = 128;                 // epilogue threads (warps 10-13)
+constexpr int kEpiWarp0 = 2 + kConvGroups * kConv / 32;
+constexpr int kThreads = 64 + kConvGroups * kConv + kEpi;
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr int kMaxStages = 8;
 constexpr int kMaxTmemStages = 8;         // A (hi + lo) stages in TMEM (upper bound)
@@ -182,6 +184,16 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
       "}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 32 lanes x 32 bit, 16 consecutive columns per thread.
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
 }
 
@@ -386,9 +398,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < kEpiWarp0) {
     // ---------------- converters ----------------
-    const int ct = tid - 64;       // 0..127
+    // kConvGroups groups of 4 warps convert alternate k-blocks, so one group's
+    // TMEM-store / proxy-fence latency overlaps the other group's work.
+    const int grp = (warp - 2) / 4;
+    const int ct = (tid - 64) % kConv;  // 0..127 within the group
     const int lane_q = warp & 3;   // TMEM lane quarter of this warp
     const int row = lane_q * 32 + (tid & 31);  // tile row = TMEM lane
     const uint32_t lane_bits = static_cast<uint32_t>(lane_q * 32) << 16;
@@ -397,63 +412,64 @@ __global__ void __launch_bounds__(kThreads, 1)
       int m_tile, split, nkb;
       tile_of(t, m_tile, split, nkb);
       for (int kb = 0; kb < nkb; ++kb, ++g) {
+        if (static_cast<int>(g % kConvGroups) != grp) continue;
         const int s = static_cast<int>(g % ns);
         const int ts = static_cast<int>(g % kTmemStages);
         tc::mbar_wait(&full[s], static_cast<uint32_t>((g / ns) & 1));
         if (ct == 0) trace_at(p, 1, g);
         const char* at = a_ring + s * A_TILE;
-        uint32_t hi[BK], lo[BK];
         const int64_t kg = (static_cast<int64_t>(split) * (p.k_chunk / BK) + kb) * BK;
         const int kval = static_cast<int>(p.k - kg < BK ? p.k - kg : BK);
-        if (p.a_bulk) {
-          // Dense rows of stride a_ld; bytes past the copied extent are stale.
-          const int lda = static_cast<int>(p.a_ld);
-          const float* af = reinterpret_cast<const float*>(at);
-          if (AMODE == 0) {
-            const bool live = static_cast<int64_t>(m_tile) * BM + row < p.m;
-#pragma unroll
-            for (int kk = 0; kk < BK; ++kk) {
-              const float x = (live && kk < kval) ? af[row * lda + kk] : 0.f;
-              const float h = tc::to_tf32(x);
-              hi[kk] = __float_as_uint(h);
-              lo[kk] = __float_as_uint(x - h);
-            }
-          } else {
-            const bool live = row < p.m;
-#pragma unroll
-            for (int kk = 0; kk < BK; ++kk) {
-              const float x = (live && kk < kval) ? af[kk * lda + row] : 0.f;
-              const float h = tc::to_tf32(x);
-              hi[kk] = __float_as_uint(h);
-              lo[kk] = __float_as_uint(x - h);
-            }
-          }
-        } else if (AMODE == 0) {
-#pragma unroll
-          for (int c = 0; c < BK / 4; ++c) {
-            const float4 v = *reinterpret_cast<const float4*>(
-                at + row * 128 + ((c ^ (row & 7)) << 4));
-            const float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float h = tc::to_tf32(x[j]);
-              hi[4 * c + j] = __float_as_uint(h);
-              lo[4 * c + j] = __float_as_uint(x[j] - h);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int kk = 0; kk < BK; ++kk) {
-            const float x = *reinterpret_cast<const float*>(at + kk * (BM * 4) + row * 4);
-            const float h = tc::to_tf32(x);
-            hi[kk] = __float_as_uint(h);
-            lo[kk] = __float_as_uint(x - h);
-          }
-        }
         // The TMEM stage (and the streamed-B slot) was consumed by MMA g - stages.
         if (g >= kTmemStages)
           tc::mbar_wait(&tempty[ts], static_cast<uint32_t>(((g / kTmemStages) - 1) & 1));
         tc::tc_fence_after();
+        const uint32_t a_hi = tmem + lane_bits + ts * 2 * BK;
+        // Two halves of 16 k-columns keep the register footprint at 32 + 32.
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint32_t hi[BK / 2], lo[BK / 2];
+          if (p.a_bulk) {
+            // Dense rows of stride a_ld; bytes past the copied extent are stale.
+            const int lda = static_cast<int>(p.a_ld);
+            const float* af = reinterpret_cast<const float*>(at);
+            const bool live = AMODE == 0 ? static_cast<int64_t>(m_tile) * BM + row < p.m : row < p.m;
+#pragma unroll
+            for (int i = 0; i < BK / 2; ++i) {
+              const int kk = half * (BK / 2) + i;
+              const float x = (live && kk < kval) ? (AMODE == 0 ? af[row * lda + kk] : af[kk * lda + row]) : 0.f;
+              const float h = tc::to_tf32(x);
+              hi[i] = __float_as_uint(h);
+              lo[i] = __float_as_uint(x - h);
+            }
+          } else if (AMODE == 0) {
+#pragma unroll
+            for (int c = 0; c < BK / 8; ++c) {
+              const int cc = half * (BK / 8) + c;
+              const float4 v = *reinterpret_cast<const float4*>(at + row * 128 + ((cc ^ (row & 7)) << 4));
+              const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float h = tc::to_tf32(x[j]);
+                hi[4 * c + j] = __float_as_uint(h);
+                lo[4 * c + j] = __float_as_uint(x[j] - h);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < BK / 2; ++i) {
+              const int kk = half * (BK / 2) + i;
+              const float x = *reinterpret_cast<const float*>(at + kk * (BM * 4) + row * 4);
+              const float h = tc::to_tf32(x);
+              hi[i] = __float_as_uint(h);
+              lo[i] = __float_as_uint(x - h);
+            }
+          }
+          if (!(p.dbg & 1)) {
+            tmem_st16(a_hi + half * (BK / 2), hi);
+            tmem_st16(a_hi + BK + half * (BK / 2), lo);
+          }
+        }
         if (BSTREAM) {
           // Raw S k-block [32 k][BN j] → K-major [B_hi; B_lo] rows j / BN + j.
           const char* st = s_ring + s * K::S_TILE;
@@ -472,14 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc::fence_proxy_async_smem();
         }
-        const uint32_t a_hi = tmem + lane_bits + ts * 2 * BK;
-        if (!(p.dbg & 1)) {
-          tmem_st32(a_hi, hi);
-          tmem_st32(a_hi + BK, lo);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        } else if (hi[0] == 0x7fffffffu && lo[0] == 1u) {
-          ep[0] = 1.f;  // keep the conversion live
-        }
+        if (!(p.dbg & 1)) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc::tc_fence_before();
         __syncwarp();
         if ((tid & 31) == 0) {
@@ -491,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------- epilogue ----------------
-    const int et = tid - 64 - kConv;  // 0..127
+    const int et = tid - 64 - kConvGroups * kConv;  // 0..127
     const bool leader = et == 0;
     const int lane_q = warp & 3;
     const int row = lane_q * 32 + (tid & 31);

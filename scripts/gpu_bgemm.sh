@@ -1,2 +1,3 @@
 cd $GRAFT_REPO_ROOT
-CAGNET_GEMM_TRACE=1 REPS=1 timeout 120 python scripts/bench_gemm.py 232965 16 602 0 0 0 > gpurun_out/trace602.txt 2>&1
+timeout 300 python scripts/bench_gemm.py > gpurun_out/bgemm.txt 2>&1
+timeout 300 python -m pytest tests/test_gpu_kernels.py -q -m gpu -k gemm --timeout 120 -p no:cacheprovider > gpurun_out/pytest_gemm.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gemm.log
