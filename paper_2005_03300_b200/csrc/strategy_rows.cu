@@ -141,10 +141,11 @@ class TrainerRows final : public Trainer {
           gemm_hts(saved_t_[static_cast<size_t>(l)].m, g, y, false);
         else
           CG_CUDA(cudaMemsetAsync(y.p, 0, y.rows * y.ld * sizeof(float), cs_));
+        // Y is only read by the SGD step: its all-reduce runs on the comm
+        // stream behind the remaining backward compute (joined before SGD).
         ms_after_cs();
         comm_->all_reduce(grid_.world(), y.p, static_cast<size_t>(y.rows * y.cols), ncclFloat32,
                           Category::Reduce, words(y), ms_);
-        cs_after_ms();
         if (l >= 2) {
           Mat gp = g_[static_cast<size_t>(l - 2)].m;
           Mat u = view(acc_, g.rows, dims_[static_cast<size_t>(l - 1)]);
@@ -195,12 +196,12 @@ class TrainerRows final : public Trainer {
       ms_after_cs();
       comm_->all_reduce(grid_.world(), y.p, static_cast<size_t>(y.rows * y.cols), ncclFloat32,
                         Category::Reduce, words(y), ms_);
-      cs_after_ms();
       if (l >= 2 && !fused) {
         const Mat& zp = z_[static_cast<size_t>(l - 2)].m;
         gemm_swt(s, l - 1, 0, 0, g_[static_cast<size_t>(l - 2)].m, false, kern::EPI_RELU_PRIME, &zp);
       }
     }
+    cs_after_ms();  // the Y all-reduces
     sgd_all();
   }
 

@@ -486,10 +486,11 @@ void Trainer::sgd_all() {
 }
 
 void Trainer::loss_all_reduce(double* partial_dev) {
+  // Off the critical path: the loss is reduced and appended on the comm
+  // stream while the backward pass runs (joined at the end of the epoch).
   ms_after_cs();
   comm_->all_reduce(grid_.world(), partial_dev, 1, ncclFloat64, Category::Reduce, 1, ms_);
-  cs_after_ms();
-  kern::push_loss(losses_dev_.get(), loss_slot_.get(), partial_dev, cs_);
+  kern::push_loss(losses_dev_.get(), loss_slot_.get(), partial_dev, ms_);
   ++epochs_done_;
 }
 

@@ -61,10 +61,20 @@ def launches(path, out_md):
     lines = ["| kernel | launches | total ms | share |", "|---|---|---|---|"]
     for k, (c, ns) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         lines.append(f"| `{k}` | {c} | {ns / 1e6:.3f} | {100 * ns / total:.1f}% |")
+    # Training-step kernels only (drops the one-time dataset generation:
+    # ER rows, radix sorts, scans, transpose, features, normalisation).
+    setup = ("er_rows", "Radix", "Scan", "transpose_gather", "jump_states", "features_kernel",
+             "norm_", "block_fill", "block_count", "iota_", "fill_ones", "keys_to_row_ptr")
+    step = {k: v for k, v in agg.items() if not any(t in k for t in setup)}
+    stot = sum(v[1] for v in step.values()) or 1.0
+    slines = ["| kernel | launches | total ms | share of step kernels |", "|---|---|---|---|"]
+    for k, (c, ns) in sorted(step.items(), key=lambda kv: -kv[1][1]):
+        slines.append(f"| `{k}` | {c} | {ns / 1e6:.3f} | {100 * ns / stot:.1f}% |")
     open(out_md, "w").write(
         f"# ncu launch list ({os.path.basename(path)})\n\n`ncu --metrics gpu__time_duration.sum "
         f"--clock-control none` over the bench command; cold-cache, serialised per launch, so "
-        f"compare shares, not absolutes.\n\n" + "\n".join(lines) + "\n")
+        f"compare shares, not absolutes.\n\n## Training-step kernels\n\n" + "\n".join(slines) +
+        "\n\n## All launches (including one-time dataset generation)\n\n" + "\n".join(lines) + "\n")
 
 
 def report(rep, out_md, traffic, name):
