@@ -67,6 +67,9 @@ class Strategy:
     # 2D / 3D: sparse tiles broadcast once in distribute() and kept resident
     # (False: the reference's per-stage sparse broadcasts and ledger).
     resident_sparse: bool = True
+    # 1D: stage panels exchanged through NVLink peer memory (CUDA IPC) instead
+    # of an NCCL all-gather (same ledger; falls back when peers are unreachable).
+    p2p: bool = True
 
     @property
     def kind_id(self) -> int:
@@ -340,6 +343,7 @@ class Trainer:
         check(lib.cagnet_trainer_set_option(self.h, b"graph", int(strat.graph)))
         check(lib.cagnet_trainer_set_option(self.h, b"resident_sparse",
                                             int(strat.resident_sparse)))
+        check(lib.cagnet_trainer_set_option(self.h, b"p2p", int(strat.p2p)))
 
     # lifecycle -------------------------------------------------------------
     def distribute(self):

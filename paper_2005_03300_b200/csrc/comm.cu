@@ -135,6 +135,12 @@ void Comm::bcast_all(const Group& g, void* buf, size_t slice_count, ncclDataType
   if (slice_count)
     CG_NCCL(ncclAllGather(base + static_cast<size_t>(member) * slice_count * esize, buf, slice_count,
                           t, comm_for(g), s));
+  meter_bcast_all(g, cat, words);
+}
+
+void Comm::meter_bcast_all(const Group& g, Category cat, const std::vector<uint64_t>& words) {
+  const int member = g.index_of(rank_);
+  if (g.size() == 1) return;
   CommCounter& c = ctr(cat);
   for (int q = 0; q < g.size(); ++q) {
     const uint64_t w = words.at(static_cast<size_t>(q));

@@ -75,6 +75,10 @@ class Comm {
   void bcast_all(const Group& g, void* buf, size_t slice_count, ncclDataType_t t, Category cat,
                  const std::vector<uint64_t>& words, cudaStream_t s);
 
+  // Meters g.size() broadcasts (roots in member order, payloads words[q])
+  // for data moved outside NCCL (the NVLink peer-memory panel exchange).
+  void meter_bcast_all(const Group& g, Category cat, const std::vector<uint64_t>& words);
+
   // Fuse the collectives issued in between into one NCCL launch.
   void group_start() {
     if (ranks_ > 1) CG_NCCL(ncclGroupStart());

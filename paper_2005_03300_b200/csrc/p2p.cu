@@ -1,0 +1,267 @@
+// NVLink peer-memory panel exchange (see p2p.hpp).
+#include <unistd.h>
+
+#include <cstring>
+
+#include "p2p.hpp"
+
+namespace cagnet {
+namespace {
+
+constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;  // 20 s, then trap
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t now_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ void spin_until_geq(const uint64_t* p, uint64_t target) {
+  if (ld_acquire_sys(p) >= target) return;
+  const uint64_t t0 = now_ns();
+  while (ld_acquire_sys(p) < target) {
+    if (now_ns() - t0 > kSpinLimitNs) __trap();
+    __nanosleep(128);
+  }
+}
+
+// Flag block of every rank (uint64): ready[P] | consumed[P] | ctr | arrivals.
+//   ready[q]    = last stage rank q published into this rank's buffers
+//   consumed[q] = last stage whose buffer rank q finished reading
+//   ctr         = stages completed by this rank (advanced by consumed())
+struct Flags {
+  int P;
+  __device__ uint64_t* ready(uint64_t* f) const { return f; }
+  __device__ uint64_t* consumed(uint64_t* f) const { return f + P; }
+  __device__ uint64_t* ctr(uint64_t* f) const { return f + 2 * P; }
+  __device__ uint64_t* arrivals(uint64_t* f) const { return f + 2 * P + 1; }
+};
+
+__global__ void publish_kernel(float* const* bufs, uint64_t* const* flags, int rank, int P,
+                               const float* __restrict__ src, int64_t ld_src, uint32_t rows,
+                               uint32_t c4, int64_t slot_floats, int64_t ld_dst) {
+  const Flags F{P};
+  uint64_t* my = flags[rank];
+  const uint64_t s = *F.ctr(my) + 1;
+  const uint32_t total = rows * c4;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const uint32_t r = e / c4, c = e - r * c4;
+    const float4 v = *reinterpret_cast<const float4*>(src + r * ld_src + 4 * c);
+    const int64_t off = rank * slot_floats + r * ld_dst + 4 * c;
+    for (int q = 0; q < P; ++q) *reinterpret_cast<float4*>(bufs[q] + off) = v;
+  }
+  // Grid completion: every block fences its stores system-wide and arrives;
+  // the last block raises ready[rank] in every rank's flags (self included).
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long prev =
+        atomicAdd(reinterpret_cast<unsigned long long*>(F.arrivals(my)), 1ull);
+    if (prev == gridDim.x - 1) {
+      *F.arrivals(my) = 0;
+      __threadfence_system();
+      for (int q = 0; q < P; ++q) st_release_sys(F.ready(flags[q]) + rank, s);
+    }
+  }
+}
+
+// Buffer parity s & 1 last held stage s - 2: every peer must be done with it
+// before this rank overwrites its slot there (one spinning block only, so the
+// copy kernel never holds SMs while waiting).
+__global__ void wait_free_kernel(uint64_t* const* flags, int rank, int P) {
+  const Flags F{P};
+  uint64_t* my = flags[rank];
+  const uint64_t s = *F.ctr(my) + 1;
+  const int q = threadIdx.x;
+  if (s > 2 && q < P && q != rank) spin_until_geq(F.consumed(my) + q, s - 2);
+}
+
+__global__ void wait_ready_kernel(uint64_t* const* flags, int rank, int P) {
+  const Flags F{P};
+  uint64_t* my = flags[rank];
+  const uint64_t s = *F.ctr(my) + 1;
+  const int q = threadIdx.x;
+  if (q < P && q != rank) spin_until_geq(F.ready(my) + q, s);
+  __threadfence_system();
+}
+
+__global__ void consumed_kernel(uint64_t* const* flags, int rank, int P) {
+  const Flags F{P};
+  uint64_t* my = flags[rank];
+  const uint64_t s = *F.ctr(my) + 1;
+  for (int q = 0; q < P; ++q)
+    if (q != rank) st_release_sys(F.consumed(flags[q]) + rank, s);
+  *F.ctr(my) = s;
+}
+
+struct PeerInfo {
+  cudaIpcMemHandle_t h[3];
+  uint64_t ptr[3];
+  uint64_t pid;
+  int32_t device;
+  int32_t ok;
+};
+
+}  // namespace
+
+PeerPanels::~PeerPanels() {
+  if (ranks_ <= 1) return;
+  cudaSetDevice(device_);
+  cudaDeviceSynchronize();
+  for (void* p : opened_) cudaIpcCloseMemHandle(p);
+  for (float* b : base_)
+    if (b) cudaFree(b);
+  if (flags_) cudaFree(flags_);
+}
+
+bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes, cudaStream_t s) {
+  rank_ = rank;
+  ranks_ = ranks;
+  device_ = device;
+  if (ranks <= 1) return false;
+  const int P = ranks;
+  // Allocate first so every rank can advertise handles; freed again on fallback.
+  CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&base_[0]), bytes));
+  CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&base_[1]), bytes));
+  CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&flags_), (2 * P + 2) * sizeof(uint64_t)));
+  CG_CUDA(cudaMemset(flags_, 0, (2 * P + 2) * sizeof(uint64_t)));
+  CG_CUDA(cudaMemset(base_[0], 0, bytes));
+  CG_CUDA(cudaMemset(base_[1], 0, bytes));
+
+  PeerInfo mine{};
+  void* ptrs[3] = {base_[0], base_[1], flags_};
+  mine.ok = 1;
+  for (int i = 0; i < 3; ++i) {
+    mine.ptr[i] = reinterpret_cast<uint64_t>(ptrs[i]);
+    if (cudaIpcGetMemHandle(&mine.h[i], ptrs[i]) != cudaSuccess) {
+      cudaGetLastError();
+      mine.ok = 0;
+    }
+  }
+  mine.pid = static_cast<uint64_t>(getpid());
+  mine.device = device;
+  const size_t words = (sizeof(PeerInfo) + 7) / 8;
+  DevBuf<uint64_t> dsend(words), drecv(words * P);
+  std::vector<uint64_t> hsend(words, 0), hrecv(words * P, 0);
+  std::memcpy(hsend.data(), &mine, sizeof(PeerInfo));
+  CG_CUDA(cudaMemcpy(dsend.get(), hsend.data(), words * 8, cudaMemcpyHostToDevice));
+  comm.setup_all_gather(dsend.get(), drecv.get(), words, ncclUint64, s);
+  CG_CUDA(cudaStreamSynchronize(s));
+  CG_CUDA(cudaMemcpy(hrecv.data(), drecv.get(), words * P * 8, cudaMemcpyDeviceToHost));
+  std::vector<PeerInfo> all(static_cast<size_t>(P));
+  for (int q = 0; q < P; ++q) std::memcpy(&all[q], hrecv.data() + q * words, sizeof(PeerInfo));
+
+  // Map every peer; agree on the outcome (all ranks take the same path).
+  bool ok = true;
+  same_process_ = true;
+  for (int q = 0; q < P; ++q) {
+    ok = ok && all[q].ok;
+    if (all[q].pid != mine.pid) same_process_ = false;
+  }
+  for (int b = 0; b < 2; ++b) peer_buf_[b].assign(static_cast<size_t>(P), nullptr);
+  peer_flags_.assign(static_cast<size_t>(P), nullptr);
+  for (int q = 0; q < P && ok; ++q) {
+    if (q == rank) {
+      peer_buf_[0][q] = base_[0];
+      peer_buf_[1][q] = base_[1];
+      peer_flags_[q] = flags_;
+      continue;
+    }
+    if (same_process_) {
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, device, all[q].device);
+      if (!can) {
+        ok = false;
+        break;
+      }
+      const cudaError_t e = cudaDeviceEnablePeerAccess(all[q].device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        ok = false;
+        break;
+      }
+      cudaGetLastError();
+      peer_buf_[0][q] = reinterpret_cast<float*>(all[q].ptr[0]);
+      peer_buf_[1][q] = reinterpret_cast<float*>(all[q].ptr[1]);
+      peer_flags_[q] = reinterpret_cast<uint64_t*>(all[q].ptr[2]);
+    } else {
+      void* p[3] = {nullptr, nullptr, nullptr};
+      for (int i = 0; i < 3 && ok; ++i) {
+        if (cudaIpcOpenMemHandle(&p[i], all[q].h[i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          cudaGetLastError();
+          ok = false;
+        } else {
+          opened_.push_back(p[i]);
+        }
+      }
+      if (!ok) break;
+      peer_buf_[0][q] = static_cast<float*>(p[0]);
+      peer_buf_[1][q] = static_cast<float*>(p[1]);
+      peer_flags_[q] = static_cast<uint64_t*>(p[2]);
+    }
+  }
+  // Agreement: all-gather the per-rank verdicts.
+  DevBuf<int32_t> vs(1), va(static_cast<size_t>(P));
+  const int32_t v = ok ? 1 : 0;
+  CG_CUDA(cudaMemcpy(vs.get(), &v, sizeof(v), cudaMemcpyHostToDevice));
+  comm.setup_all_gather(vs.get(), va.get(), 1, ncclInt32, s);
+  CG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int32_t> verdicts(static_cast<size_t>(P));
+  CG_CUDA(cudaMemcpy(verdicts.data(), va.get(), P * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  for (int32_t x : verdicts) ok = ok && x;
+  if (!ok) {
+    for (void* p : opened_) cudaIpcCloseMemHandle(p);
+    opened_.clear();
+    for (float*& b : base_) {
+      cudaFree(b);
+      b = nullptr;
+    }
+    cudaFree(flags_);
+    flags_ = nullptr;
+    return false;
+  }
+  for (int b = 0; b < 2; ++b) {
+    d_bufs_[b].resize(static_cast<size_t>(P));
+    CG_CUDA(cudaMemcpy(d_bufs_[b].get(), peer_buf_[b].data(), P * sizeof(float*), cudaMemcpyHostToDevice));
+  }
+  d_flags_.resize(static_cast<size_t>(P));
+  CG_CUDA(cudaMemcpy(d_flags_.get(), peer_flags_.data(), P * sizeof(uint64_t*), cudaMemcpyHostToDevice));
+  return true;
+}
+
+void PeerPanels::publish(int b, const float* src, int64_t ld_src, int64_t rows, int64_t cols,
+                         int64_t slot_floats, int64_t ld_dst, cudaStream_t s) {
+  require(ld_src % 4 == 0 && ld_dst % 4 == 0 && slot_floats % 4 == 0 &&
+              reinterpret_cast<uintptr_t>(src) % 16 == 0,
+          "PeerPanels::publish: rows must be 16 B aligned");
+  const int64_t c4 = (cols + 3) / 4;
+  require(c4 * 4 <= ld_src && c4 * 4 <= ld_dst, "PeerPanels::publish: padded width exceeds ld");
+  const int64_t total = rows * c4;
+  int blocks = static_cast<int>(ceil_div64(total > 0 ? total : 1, 256));
+  const int cap = 2 * num_sms(device_);
+  if (blocks > cap) blocks = cap;
+  wait_free_kernel<<<1, 32 * ((ranks_ + 31) / 32), 0, s>>>(d_flags_.get(), rank_, ranks_);
+  CG_LAUNCH_CHECK();
+  publish_kernel<<<blocks, 256, 0, s>>>(d_bufs_[b].get(), d_flags_.get(), rank_, ranks_, src, ld_src,
+                                        static_cast<uint32_t>(rows), static_cast<uint32_t>(c4),
+                                        slot_floats, ld_dst);
+  CG_LAUNCH_CHECK();
+}
+
+void PeerPanels::wait_ready(cudaStream_t s) {
+  wait_ready_kernel<<<1, 32 * ((ranks_ + 31) / 32), 0, s>>>(d_flags_.get(), rank_, ranks_);
+  CG_LAUNCH_CHECK();
+}
+
+void PeerPanels::consumed(cudaStream_t s) {
+  consumed_kernel<<<1, 1, 0, s>>>(d_flags_.get(), rank_, ranks_);
+  CG_LAUNCH_CHECK();
+}
+
+}  // namespace cagnet

@@ -1,0 +1,71 @@
+// NVLink peer-memory panel exchange for the 1D propagation stages.
+//
+// The 1D strategy's stage broadcasts (dist_1d.cpp:46-56: every rank roots the
+// panel of its vertex block) are an all-gather of an n x f panel whose f is
+// 16 after narrow-first reassociation: ~15 MB for Reddit, which NCCL moves in
+// ~58 us on 4 B200s (busbw ~200 GB/s at this size, measured by
+// scripts/nccl_micro.py).  Here every rank instead *pushes* its own panel
+// rows straight into every peer's panel buffer over NVLink (CUDA IPC mapped
+// peer memory, one copy kernel writing P slots), then raises a per-peer
+// ready flag in the peer's memory; consumers spin on their local flags before
+// the SpMM.  Double-buffered slots plus per-peer "consumed" flags (written
+// by the consumer into the producer's memory after its SpMM) make buffer
+// reuse safe across stages.  Flags carry a device-side stage sequence number,
+// so the exchange works unchanged inside a replayed CUDA graph.
+//
+// All waits are bounded (~20 s of spinning, then __trap()), so a broken peer
+// aborts the kernel instead of hanging the GPU.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "comm.hpp"
+#include "common.cuh"
+
+namespace cagnet {
+
+class PeerPanels {
+ public:
+  PeerPanels() = default;
+  ~PeerPanels();
+  PeerPanels(const PeerPanels&) = delete;
+  PeerPanels& operator=(const PeerPanels&) = delete;
+
+  // Collective over the world communicator: allocates 2 x `bytes` of panel
+  // buffer plus flags on this rank, exchanges IPC handles (or raw pointers
+  // when all ranks share a process) and maps every peer's buffers.  Returns
+  // false (nothing allocated) when some pair of GPUs lacks peer access; the
+  // caller then keeps the NCCL path.  Every rank must call it.
+  bool init(Comm& comm, int rank, int ranks, int device, size_t bytes, cudaStream_t s);
+  bool ready() const { return ranks_ > 1 && base_[0] != nullptr; }
+
+  // Buffer b (stage parity) of this rank: P slots of slot_floats each.
+  float* buffer(int b) const { return base_[b]; }
+
+  // Publishes rows x cols (ld_src) of `src` into slot `rank` of buffer b on
+  // every rank (self included) at leading dimension ld_dst, after all peers
+  // released buffer b from two stages ago; raises the ready flags.
+  void publish(int b, const float* src, int64_t ld_src, int64_t rows, int64_t cols,
+               int64_t slot_floats, int64_t ld_dst, cudaStream_t s);
+  // Waits until every peer published the current stage.
+  void wait_ready(cudaStream_t s);
+  // Marks the current stage's buffer as consumed on every peer and advances
+  // the local stage counter.
+  void consumed(cudaStream_t s);
+
+ private:
+  int rank_ = 0, ranks_ = 1, device_ = 0;
+  bool same_process_ = false;
+  float* base_[2] = {nullptr, nullptr};  // own allocations
+  uint64_t* flags_ = nullptr;            // own: ready[P] | consumed[P] | ctr | arrivals
+  std::vector<float*> peer_buf_[2];      // [b][q] (q == rank: own)
+  std::vector<uint64_t*> peer_flags_;    // [q]
+  DevBuf<float*> d_bufs_[2];             // device copies of peer_buf_
+  DevBuf<uint64_t*> d_flags_;            // device copy of peer_flags_
+  std::vector<void*> opened_;            // IPC mappings to close
+};
+
+}  // namespace cagnet

@@ -8,6 +8,7 @@
 #include <algorithm>
 
 #include "kernels.cuh"
+#include "p2p.hpp"
 #include "trainer.hpp"
 
 namespace cagnet {
@@ -48,6 +49,11 @@ class TrainerRows final : public Trainer {
       at_chunk_ = extract_block_device(data_.adj_t, rows.begin, rows.end, c_lo_, c_hi_, cs_);
       // Rows for whole padded slots (the 1D all-gather writes P equal slots).
       gbuf_.alloc(std::max(c_hi_ - c_lo_, ceil_div64(data_.n, blocks()) * blocks()), kCoalesceMaxF);
+      if (one_d() && p2p_enabled_) {
+        const size_t bytes = static_cast<size_t>(ceil_div64(data_.n, blocks()) * blocks()) *
+                             kCoalesceMaxF * sizeof(float);
+        p2p_ok_ = p2p_.init(*comm_, rank_, grid_.ranks(), device_, bytes, cs_);
+      }
     }
     CG_CUDA(cudaDeviceSynchronize());
   }
@@ -249,6 +255,22 @@ class TrainerRows final : public Trainer {
         const BlockRange r = block_range(data_.n, blocks(), own);
         kern::copy2d(g.p + (r.begin - c_lo_) * g.ld, g.ld, mine.p, mine.ld, mine.rows, mine.cols, ms_);
       }
+      if (one_d() && p2p_ok_) {
+        // NVLink peer-memory exchange: push this rank's panel into every
+        // rank's buffer, wait for the peers' panels, SpMM, release.
+        const int64_t step = ceil_div64(data_.n, blocks());
+        const int b = static_cast<int>(p2p_stage_++ & 1);
+        Mat pg{p2p_.buffer(b), c_hi_ - c_lo_, mine.cols, mine.ld};
+        std::vector<uint64_t> words;
+        for (int q = 0; q < blocks(); ++q)
+          words.push_back(static_cast<uint64_t>(block_range(data_.n, blocks(), q).size() * mine.cols));
+        comm_->meter_bcast_all(grp, Category::DBcast, words);
+        p2p_.publish(b, mine.p, mine.ld, mine.rows, mine.cols, step * mine.ld, mine.ld, cs_);
+        p2p_.wait_ready(cs_);
+        spmm(blk, pg, out, false, epi);
+        p2p_.consumed(cs_);
+        return;
+      }
       if (one_d()) {
         // 1D: every rank roots one stage, so the P broadcasts are an
         // all-gather of the panel slots (ceil-rule blocks = equal padded slots).
@@ -324,6 +346,9 @@ class TrainerRows final : public Trainer {
   int64_t c_lo_ = 0, c_hi_ = 0;
   DeviceCsr a_chunk_, at_chunk_;  // block row restricted to this column's stage columns
   OwnedMat gbuf_;                 // stage panels side by side
+  PeerPanels p2p_;                // NVLink peer-memory panel exchange (1D)
+  bool p2p_ok_ = false;
+  uint64_t p2p_stage_ = 0;        // host parity of the double-buffered panels
   std::vector<OwnedMat> saved_t_;  // T = Aᵀ H of widening layers (narrow-first backward)
   std::vector<bool> saved_valid_;
 };

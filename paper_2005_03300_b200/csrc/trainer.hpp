@@ -137,6 +137,10 @@ class Trainer {
   // distribute() instead of re-broadcasting them every SpMM stage.  Set before
   // distribute(); off reproduces the reference's per-stage SBcast ledger.
   void set_resident_sparse(bool on) { resident_sparse_ = on; }
+  // 1D: exchange the stage panels through NVLink peer memory instead of an
+  // NCCL all-gather (set before distribute(); falls back to NCCL when the
+  // GPUs lack peer access).
+  void set_p2p(bool on) { p2p_enabled_ = on; }
   void reset_profile() {
     collect_profile();
     profile_.clear();
@@ -195,6 +199,7 @@ class Trainer {
   bool reassociate_ = false;
   int fuse_ = 1;
   bool resident_sparse_ = true;
+  bool p2p_enabled_ = true;
   std::vector<ProfRec> recs_;
   size_t recs_used_ = 0;
   std::vector<ProfEntry> profile_;
