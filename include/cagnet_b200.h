@@ -177,6 +177,19 @@ CAGNET_API int cagnet_dataset_make(int device, int64_t n, const int64_t* raw_row
                         const int64_t* labels, const uint8_t* mask, int64_t num_classes,
                         cagnet_dataset_t* out);
 /* info = {n, nnz, num_features, num_classes, train_count} */
+/* load_dataset (dataset.hpp:96-97, dataset.cpp:293-307): edge list ("u v" per
+ * line, '#' comments, optional "% n <count>" header), features CSV (one row of
+ * doubles per vertex) and labels ("vertex,label" per line); from_edge_list
+ * (both directions when undirected), normalisation and transpose on `device`.
+ * I/O and format errors return CAGNET_ERUNTIME with the reference's message. */
+CAGNET_API int cagnet_dataset_load(int device, const char* edges_path, const char* features_path,
+                        const char* labels_path, int undirected, cagnet_dataset_t* out);
+/* permute_random (dataset.hpp:70-77, dataset.cpp:120-144): relabels vertices
+ * by the seeded Fisher-Yates permutation; position i of the result holds the
+ * data of original vertex perm[i] (perm_out: n entries, or NULL); adjacency
+ * values are moved, never recomputed (bit-exact with the reference). */
+CAGNET_API int cagnet_dataset_permute_random(cagnet_dataset_t d, uint64_t seed, int64_t* perm_out,
+                                  cagnet_dataset_t* out);
 CAGNET_API int cagnet_dataset_info(cagnet_dataset_t d, int64_t* info);
 /* which: 0 = adj, 1 = adj_t.  Borrowed handle, owned by the dataset. */
 CAGNET_API int cagnet_dataset_csr(cagnet_dataset_t d, int which, cagnet_csr_t* out);

@@ -251,6 +251,8 @@ class Ref:
         L.ref_dataset_generate.argtypes = [C.c_uint64, C.c_double] + [C.c_uint64] * 5
         L.ref_dataset_make.restype = vp
         L.ref_dataset_make.argtypes = [C.c_uint64, _i64p, _i64p, _f64p, C.c_uint64, _i64p, C.c_uint64]
+        L.ref_dataset_load.restype = vp
+        L.ref_dataset_load.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int]
         L.ref_dataset_permute.restype = vp
         L.ref_dataset_permute.argtypes = [vp, C.c_uint64, _i64p]
         for fn in ("n", "nnz", "features_cols", "classes"):
@@ -303,6 +305,17 @@ class Ref:
         return RefDataset(self, self._check(self.lib.ref_dataset_generate(n, degree, f, classes,
                                                                           sg, sf, sl)))
 
+    def dataset_make(self, raw: CSR, features, labels, classes):
+        """make_dataset (dataset.cpp:76-90) from a raw CSR."""
+        x = np.ascontiguousarray(features, np.float64)
+        y = np.ascontiguousarray(labels, np.int64)
+        return RefDataset(self, self._check(self.lib.ref_dataset_make(
+            raw.n_rows, raw.row_ptr, raw.col_idx, x, x.shape[1], y, classes)))
+
+    def load_dataset(self, edges, features, labels, undirected):
+        return RefDataset(self, self._check(self.lib.ref_dataset_load(
+            edges.encode(), features.encode(), labels.encode(), int(undirected))))
+
     def model(self, dims, seed, lr):
         d = np.asarray(dims, np.uint64)
         return RefModel(self, self._check(self.lib.ref_model_glorot(d, len(d), seed, lr)), dims)
@@ -346,6 +359,12 @@ class RefDataset:
         out = np.zeros(self.n, np.int64)
         self.ref.lib.ref_dataset_labels(self.h, out)
         return out
+
+    def permute(self, seed):
+        """The reference's permute_random (dataset.cpp:120-144): (dataset, perm)."""
+        perm = np.zeros(max(self.n, 1), np.int64)
+        h = self.ref._check(self.ref.lib.ref_dataset_permute(self.h, seed, perm))
+        return RefDataset(self.ref, h), perm[:self.n]
 
     def __del__(self):
         try:

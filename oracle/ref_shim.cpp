@@ -107,6 +107,14 @@ void* ref_dataset_make(uint64_t n, const int64_t* row_ptr, const int64_t* col_id
   return d;
 }
 
+// load_dataset (dataset.cpp:293-307) from the reference's text formats.
+void* ref_dataset_load(const char* edges, const char* features, const char* labels, int undirected) {
+  GraphDataset* d = nullptr;
+  if (guarded([&] { d = new GraphDataset(load_dataset(edges, features, labels, undirected != 0)); }))
+    return nullptr;
+  return d;
+}
+
 void* ref_dataset_permute(void* data, uint64_t seed, int64_t* perm_out) {
   GraphDataset* d = nullptr;
   if (guarded([&] {

@@ -30,7 +30,9 @@ from .api import (  # noqa: F401
     init_glorot,
     make_dataset,
     make_grid,
+    load_dataset,
     make_trainer,
+    permute_random,
     run_distributed,
     transpose,
 )

@@ -250,6 +250,24 @@ def generate_dataset(n, degree, num_features, num_classes, seed_graph=1, seed_fe
     return GraphDataset(out, device)
 
 
+def load_dataset(edges_path, features_path, labels_path, undirected=False,
+                 device=0) -> GraphDataset:
+    """load_dataset (dataset.hpp:96-97): the reference's text formats."""
+    out = C.c_void_p()
+    check(lib.cagnet_dataset_load(device, str(edges_path).encode(), str(features_path).encode(),
+                                  str(labels_path).encode(), int(bool(undirected)), C.byref(out)))
+    return GraphDataset(out, device)
+
+
+def permute_random(data: GraphDataset, seed: int):
+    """permute_random (dataset.hpp:70-77): (permuted dataset, perm) with row i
+    of the result = original vertex perm[i]; built on the dataset's GPU."""
+    perm = np.zeros(max(data.n, 1), np.int64)
+    out = C.c_void_p()
+    check(lib.cagnet_dataset_permute_random(data.h, seed, perm.ctypes.data, C.byref(out)))
+    return GraphDataset(out, data.device), perm[:data.n]
+
+
 def make_dataset(raw_row_ptr, raw_col_idx, features, labels, num_classes, train_mask=None,
                  device=0) -> GraphDataset:
     """make_dataset (dataset.cpp:76-90) from a raw host CSR (canonical: sorted,

@@ -357,6 +357,31 @@ int cagnet_dataset_make(int device, int64_t n, const int64_t* raw_row_ptr, const
   });
 }
 
+int cagnet_dataset_load(int device, const char* edges_path, const char* features_path,
+                        const char* labels_path, int undirected, cagnet_dataset_t* out) {
+  return guarded([&] {
+    cagnet::require(edges_path && features_path && labels_path, "load_dataset: null path");
+    set_device(device);
+    auto d = std::make_unique<cagnet_dataset_s>();
+    d->data = cagnet::dataset_load(edges_path, features_path, labels_path, undirected != 0);
+    wrap_dataset(d.get());
+    *out = d.release();
+  });
+}
+
+int cagnet_dataset_permute_random(cagnet_dataset_t d, uint64_t seed, int64_t* perm_out,
+                                  cagnet_dataset_t* out) {
+  return guarded([&] {
+    set_device(d->data->device);
+    auto p = std::make_unique<cagnet_dataset_s>();
+    std::vector<int64_t> perm;
+    p->data = cagnet::dataset_permute(*d->data, seed, &perm);
+    if (perm_out && !perm.empty()) std::memcpy(perm_out, perm.data(), perm.size() * sizeof(int64_t));
+    wrap_dataset(p.get());
+    *out = p.release();
+  });
+}
+
 int cagnet_dataset_info(cagnet_dataset_t d, int64_t* info) {
   return guarded([&] {
     info[0] = d->data->n;

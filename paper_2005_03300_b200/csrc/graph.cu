@@ -12,6 +12,7 @@
 // next_double() < p:  (x >> 11) < ceil(p * 2^53).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -456,6 +457,76 @@ DeviceCsr transpose_device(const DeviceCsr& a, cudaStream_t s) {
   CG_LAUNCH_CHECK();
   CG_CUDA(cudaStreamSynchronize(s));
   return t;
+}
+
+__global__ void permuted_len_kernel(int64_t n, const int64_t* __restrict__ rp,
+                                    const int64_t* __restrict__ perm, int64_t* __restrict__ len) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) len[i] = rp[perm[i] + 1] - rp[perm[i]];
+}
+
+// Warp per new row i: the entries of old row perm[i] with columns relabelled
+// by inv, in old order (the segmented sort below orders them).
+__global__ void permuted_fill_kernel(int64_t n, const int64_t* __restrict__ rp,
+                                     const int32_t* __restrict__ ci, const float* __restrict__ v,
+                                     const int64_t* __restrict__ perm, const int64_t* __restrict__ inv,
+                                     const int64_t* __restrict__ new_rp, int32_t* __restrict__ keys,
+                                     float* __restrict__ vals) {
+  const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int64_t r = perm[i], b = rp[r], e = rp[r + 1], o = new_rp[i];
+  for (int64_t k = b + lane; k < e; k += 32) {
+    keys[o + (k - b)] = static_cast<int32_t>(inv[ci[k]]);
+    vals[o + (k - b)] = v[k];
+  }
+}
+
+DeviceCsr permute_csr_device(const DeviceCsr& a, const int64_t* perm, const int64_t* inv,
+                             cudaStream_t s) {
+  require(a.n_rows == a.n_cols, "permute_random: square adjacency required");
+  require(a.nnz < (1LL << 31), "permute_random: nnz must fit the segmented sort");
+  DeviceCsr out;
+  out.device = current_device();
+  out.n_rows = a.n_rows;
+  out.n_cols = a.n_cols;
+  out.nnz = a.nnz;
+  const int64_t n = a.n_rows;
+  out.row_ptr.resize(static_cast<size_t>(n + 1));
+  out.col_idx.resize(static_cast<size_t>(std::max<int64_t>(a.nnz, 1)));
+  out.vals.resize(static_cast<size_t>(std::max<int64_t>(a.nnz, 1)));
+  CG_CUDA(cudaMemsetAsync(out.row_ptr.get(), 0, sizeof(int64_t), s));
+  if (n == 0) return out;
+  DevBuf<int64_t> len(static_cast<size_t>(n));
+  permuted_len_kernel<<<static_cast<unsigned>(ceil_div64(n, 256)), 256, 0, s>>>(n, a.row_ptr.get(), perm, len.get());
+  CG_LAUNCH_CHECK();
+  size_t temp = 0;
+  CG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, temp, len.get(), out.row_ptr.get() + 1, n, s));
+  {
+    DevBuf<char> tmp(temp);
+    CG_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), temp, len.get(), out.row_ptr.get() + 1, n, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+  }
+  if (a.nnz == 0) return out;
+  DevBuf<int32_t> keys(static_cast<size_t>(a.nnz));
+  DevBuf<float> vals(static_cast<size_t>(a.nnz));
+  permuted_fill_kernel<<<static_cast<unsigned>(ceil_div64(n * 32, 256)), 256, 0, s>>>(
+      n, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), perm, inv, out.row_ptr.get(), keys.get(),
+      vals.get());
+  CG_LAUNCH_CHECK();
+  temp = 0;
+  CG_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, temp, keys.get(), out.col_idx.get(), vals.get(),
+                                              out.vals.get(), static_cast<int>(a.nnz), static_cast<int>(n),
+                                              out.row_ptr.get(), out.row_ptr.get() + 1, s));
+  {
+    DevBuf<char> tmp(temp);
+    CG_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.get(), temp, keys.get(), out.col_idx.get(),
+                                                vals.get(), out.vals.get(), static_cast<int>(a.nnz),
+                                                static_cast<int>(n), out.row_ptr.get(),
+                                                out.row_ptr.get() + 1, s));
+    CG_CUDA(cudaStreamSynchronize(s));
+  }
+  return out;
 }
 
 DeviceCsr extract_block_device(const DeviceCsr& a, int64_t r0, int64_t r1, int64_t c0,

@@ -27,6 +27,11 @@ DeviceCsr er_skip_generate_device(int64_t n, double degree, uint64_t seed, cudaS
 DeviceCsr normalize_device(const DeviceCsr& raw, DevBuf<int32_t>* degree_out, cudaStream_t s);
 // csr.cpp:118-138 (values moved, columns sorted).
 DeviceCsr transpose_device(const DeviceCsr& a, cudaStream_t s);
+// permute_csr, dataset.cpp:49-72: out[i][j] = in[perm[i]][perm[j]] — values
+// moved (never recomputed), columns re-sorted per row.  perm / inv are device
+// arrays of n = rows = cols entries.
+DeviceCsr permute_csr_device(const DeviceCsr& a, const int64_t* perm, const int64_t* inv,
+                             cudaStream_t s);
 // csr.cpp:140-162.
 DeviceCsr extract_block_device(const DeviceCsr& a, int64_t r0, int64_t r1, int64_t c0,
                                int64_t c1, cudaStream_t s);

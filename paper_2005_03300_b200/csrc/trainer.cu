@@ -71,6 +71,73 @@ std::unique_ptr<DeviceDataset> dataset_generate(int64_t n, double degree, int64_
   return d;
 }
 
+namespace {
+// out[i, :] = in[perm[i], :] for features (ld), labels and mask.
+__global__ void permute_rows_kernel(int64_t n, int64_t ldf, const int64_t* __restrict__ perm,
+                                    const float* __restrict__ fin, float* __restrict__ fout,
+                                    const int32_t* __restrict__ lin, int32_t* __restrict__ lout,
+                                    const uint8_t* __restrict__ min, uint8_t* __restrict__ mout) {
+  const int64_t i = blockIdx.x;
+  if (i >= n) return;
+  const int64_t r = perm[i];
+  for (int64_t j = threadIdx.x; j < ldf; j += blockDim.x) fout[i * ldf + j] = fin[r * ldf + j];
+  if (threadIdx.x == 0) {
+    lout[i] = lin[r];
+    mout[i] = min[r];
+  }
+}
+}  // namespace
+
+std::unique_ptr<DeviceDataset> dataset_permute(const DeviceDataset& d, uint64_t seed,
+                                               std::vector<int64_t>* perm_out) {
+  CG_CUDA(cudaSetDevice(d.device));
+  const int64_t n = d.n;
+  std::vector<int64_t> perm(static_cast<size_t>(n)), inv(static_cast<size_t>(n));
+  {
+    Xoshiro rng(seed);  // rng.hpp:73-82, Fisher-Yates
+    for (int64_t i = 0; i < n; ++i) perm[static_cast<size_t>(i)] = i;
+    for (int64_t i = n; i > 1; --i) {
+      const int64_t j = static_cast<int64_t>(rng.bounded(static_cast<uint64_t>(i)));
+      std::swap(perm[static_cast<size_t>(i - 1)], perm[static_cast<size_t>(j)]);
+    }
+  }
+  for (int64_t i = 0; i < n; ++i) inv[static_cast<size_t>(perm[static_cast<size_t>(i)])] = i;
+  auto out = std::make_unique<DeviceDataset>();
+  out->device = d.device;
+  out->n = n;
+  out->f = d.f;
+  out->num_classes = d.num_classes;
+  out->train_count = d.train_count;
+  out->ldf = d.ldf;
+  cudaStream_t s;
+  CG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  try {
+    DevBuf<int64_t> dp(static_cast<size_t>(std::max<int64_t>(n, 1))), di(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    if (n) {
+      CG_CUDA(cudaMemcpyAsync(dp.get(), perm.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+      CG_CUDA(cudaMemcpyAsync(di.get(), inv.data(), n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    }
+    out->adj = permute_csr_device(d.adj, dp.get(), di.get(), s);
+    out->adj_t = permute_csr_device(d.adj_t, dp.get(), di.get(), s);
+    out->features.resize(static_cast<size_t>(std::max<int64_t>(n * d.ldf, 1)));
+    out->labels.resize(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    out->mask.resize(static_cast<size_t>(std::max<int64_t>(n, 1)));
+    if (n) {
+      permute_rows_kernel<<<static_cast<unsigned>(n), 128, 0, s>>>(
+          n, d.ldf, dp.get(), d.features.get(), out->features.get(), d.labels.get(), out->labels.get(),
+          d.mask.get(), out->mask.get());
+      CG_LAUNCH_CHECK();
+    }
+    CG_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    cudaStreamDestroy(s);
+    throw;
+  }
+  CG_CUDA(cudaStreamDestroy(s));
+  if (perm_out) *perm_out = std::move(perm);
+  return out;
+}
+
 std::unique_ptr<DeviceDataset> dataset_make(int64_t n, const int64_t* raw_rp,
                                             const int64_t* raw_ci, const double* features,
                                             int64_t f, const int64_t* labels,

@@ -36,6 +36,17 @@ struct DeviceDataset {
 std::unique_ptr<DeviceDataset> dataset_generate(int64_t n, double degree, int64_t f,
                                                 int64_t classes, uint64_t sg, uint64_t sf,
                                                 uint64_t sl, int generator);
+// permute_random (dataset.cpp:120-144) on the GPU: perm from the reference's
+// seeded Fisher-Yates (rng.hpp:73-82) on the host, then both CSR
+// orientations, features, labels and mask permuted on the device; perm_out
+// (n entries) receives perm.
+std::unique_ptr<DeviceDataset> dataset_permute(const DeviceDataset& d, uint64_t seed,
+                                               std::vector<int64_t>* perm_out);
+// load_dataset (dataset.cpp:293-307): the reference's text formats parsed on
+// the host (io.cu), then make_dataset on the current device.
+std::unique_ptr<DeviceDataset> dataset_load(const std::string& edges_path,
+                                            const std::string& features_path,
+                                            const std::string& labels_path, bool undirected);
 // make_dataset (dataset.cpp:76-90) from host arrays.
 std::unique_ptr<DeviceDataset> dataset_make(int64_t n, const int64_t* raw_rp,
                                             const int64_t* raw_ci, const double* features,

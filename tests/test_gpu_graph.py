@@ -143,3 +143,101 @@ def test_skip_generator_properties(cg):
         assert np.all(np.diff(cols) > 0) and i in cols
     d2 = cg.generate_dataset(n, deg, 4, 3, 1, 2, 3, generator="skip")
     assert np.array_equal(d2.adj.download()[1], ci)
+
+
+@pytest.mark.parametrize("n,d,seed", [(200, 6.0, 77), (1000, 20.0, 5), (1, 0.0, 3)])
+def test_permute_random_bitwise(cg, ref, n, d, seed):
+    """permute_random on the GPU against the reference's own permute_random
+    (dataset.cpp:120-144): same perm, both orientations bit-exact (values
+    moved, so (float) of the reference's), features / labels moved."""
+    g = cg.generate_dataset(n, d, 5, 3, 1, 2, 3)
+    rd = ref.dataset(n, d, 5, 3, 1, 2, 3)
+    gp, perm = cg.permute_random(g, seed)
+    rp_ds, rperm = rd.permute(seed)
+    assert np.array_equal(perm, rperm)
+    for which in (0, 1):
+        a = gp.csr(which).download()
+        b = rp_ds.csr(which)
+        assert np.array_equal(a[0], b.row_ptr)
+        assert np.array_equal(a[1], b.col_idx)
+        assert np.array_equal(a[2], b.vals.astype(np.float32))
+    assert np.array_equal(gp.features(), rp_ds.features().astype(np.float32))
+    assert np.array_equal(gp.labels(), rp_ds.labels())
+    # A permuted dataset trains like any other (smoke: finite losses).
+    model = cg.init_glorot([5, 4, 3], 4, 0.5)
+    t = cg.make_trainer(gp, model, cg.Strategy("1d", 1))
+    t.distribute()
+    assert np.all(np.isfinite(t.run_epochs(2)))
+
+
+def _write_text_dataset(tmp_path, n, edges, feats, labels, header=True):
+    e = tmp_path / "edges.txt"
+    with open(e, "w") as fh:
+        fh.write("# an edge list\n")
+        if header:
+            fh.write(f"% n {n}\n")
+        for u, v in edges:
+            fh.write(f"{u} {v}  # edge\n")
+        fh.write("\n")
+    f = tmp_path / "features.csv"
+    with open(f, "w") as fh:
+        for row in feats:
+            fh.write(",".join(f"{x:.17g}" for x in row) + "\n")
+    lab = tmp_path / "labels.csv"
+    with open(lab, "w") as fh:
+        fh.write("# vertex,label\n")
+        for i, y in enumerate(labels):
+            fh.write(f"{i},{y}\n")
+    return str(e), str(f), str(lab)
+
+
+@pytest.mark.parametrize("undirected", [False, True])
+def test_load_dataset_text_formats(cg, ref, tmp_path, undirected):
+    """load_dataset (dataset.cpp:293-307) against the reference's own loader:
+    edge list with comments / header / duplicates, features CSV, labels."""
+    rng = np.random.default_rng(5)
+    n = 40
+    edges = [(int(u), int(v)) for u, v in rng.integers(0, n, size=(150, 2))]
+    edges += edges[:10]  # duplicates collapse (from_pairs sort + unique)
+    feats = rng.standard_normal((n, 7))
+    labels = rng.integers(0, 4, size=n)
+    paths = _write_text_dataset(tmp_path, n, edges, feats, labels)
+    g = cg.load_dataset(*paths, undirected=undirected)
+    # Expected: the reference's make_dataset on from_edge_list of the same
+    # pairs (the reference's own text loader misparses "% n" headers once numpy
+    # is loaded in the process — iostream state — so the parse is pinned by the
+    # error-path test and the C restatement of from_edge_list instead).
+    import oracle
+    raw = oracle.Oracle().from_edge_list(n, np.array([e[0] for e in edges]),
+                                         np.array([e[1] for e in edges]), undirected)
+    r = ref.dataset_make(raw, feats, labels, int(labels.max()) + 1)
+    assert (g.n, g.nnz, g.num_features, g.num_classes) == (r.n, r.nnz, r.f, r.num_classes)
+    for which in (0, 1):
+        a, b = g.csr(which).download(), r.csr(which)
+        assert np.array_equal(a[0], b.row_ptr) and np.array_equal(a[1], b.col_idx)
+        assert np.array_equal(a[2], b.vals.astype(np.float32))
+    assert np.array_equal(g.features(), r.features().astype(np.float32))
+    assert np.array_equal(g.labels(), r.labels())
+
+
+def test_load_dataset_errors(cg, tmp_path):
+    n = 5
+    paths = _write_text_dataset(tmp_path, n, [(0, 1), (1, 2)], np.ones((n, 2)), [0, 1, 0, 1, 0])
+    with pytest.raises(cg.CagnetError, match="cannot open"):
+        cg.load_dataset(str(tmp_path / "missing.txt"), paths[1], paths[2])
+    bad = tmp_path / "bad_edges.txt"
+    bad.write_text("% m 5\n0 1\n")
+    with pytest.raises(cg.CagnetError, match="bad header at line 1"):
+        cg.load_dataset(str(bad), paths[1], paths[2])
+    out = tmp_path / "out_of_range.txt"
+    out.write_text("% n 3\n0 4\n")
+    with pytest.raises(cg.CagnetError, match="outside declared n=3"):
+        cg.load_dataset(str(out), paths[1], paths[2])
+    rag = tmp_path / "ragged.csv"
+    rag.write_text("1,2\n3\n1,2\n1,2\n1,2\n")
+    with pytest.raises(cg.CagnetError, match="ragged row at line 2"):
+        cg.load_dataset(paths[0], str(rag), paths[2])
+    lab = tmp_path / "labels_missing.csv"
+    lab.write_text("0,1\n1,0\n")
+    with pytest.raises(cg.CagnetError, match="no label for vertex 2"):
+        cg.load_dataset(paths[0], paths[1], str(lab))
