@@ -451,7 +451,7 @@ class Trainer:
 
     def last_epoch_ms(self) -> float:
         ms = np.zeros(8)
-        check(lib.cagnet_trainer_stats(self.h, ms, None))
+        check(lib.cagnet_trainer_stats(self.h, ms, np.zeros(4, np.uint64)))
         return float(ms[7])
 
     def set_timing(self, on: bool = True):
@@ -510,6 +510,7 @@ class DistOutcome:
     g_final: list
     model: GnnModel
     ledger: list  # per rank
+    epoch_ms: float = 0.0  # last epoch, device time, max over ranks (GPU extension)
 
 
 def assemble_tiles(trainers, n, width, pick) -> np.ndarray:
@@ -589,5 +590,7 @@ def run_distributed(data_factory, model: GnnModel, strat: Strategy, epochs: int,
     w_final = [_verified(trainers, lambda t, i=i: t.weight(i), "weight").astype(np.float64)
                for i in range(L - 1)]
     ledgers = [t.ledger() for t in trainers]
+    epoch_ms = max(t.last_epoch_ms() for t in trainers)
     return DistOutcome(np.asarray(out_losses), h_final, y_final, g_final,
-                       GnnModel(list(model.layer_dims), w_final, model.learning_rate), ledgers)
+                       GnnModel(list(model.layer_dims), w_final, model.learning_rate), ledgers,
+                       epoch_ms)
