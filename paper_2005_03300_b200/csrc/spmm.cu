@@ -440,6 +440,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) spmm_nzpar_kernel(const SpmmArg
     acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
   }
   if constexpr (EPI) {
+    if (ACC && row < a.n_rows && vec_ok) {
+      // Final pass of a split propagation: fold in the earlier passes' partial.
+      const float4 old = load_vec(a.T + row * a.ldt, vec, f);
+      acc.x = old.x + acc.x;
+      acc.y = old.y + acc.y;
+      acc.z = old.z + acc.z;
+      acc.w = old.w + acc.w;
+    }
     spmm_row_epilogue<LV, TEAM>(a, row, lane, vec, q, vec_ok, acc);
     return;
   }
@@ -462,7 +470,14 @@ void launch_nzpar_v(const SpmmArgs& a, bool acc, bool epi, cudaStream_t s) {
   const unsigned g = static_cast<unsigned>(ceil_div64(a.n_rows, rows_per_block));
   const bool tail = (a.f % 4) != 0;
   const bool full = !tail && (a.f / 4) == LV;
-  if (epi) {
+  if (epi && acc) {
+    if (tail)
+      spmm_nzpar_kernel<LV, QPR, U, true, true, NT, 0, false, true><<<g, NT, 0, s>>>(a);
+    else if (full)
+      spmm_nzpar_kernel<LV, QPR, U, true, false, NT, 0, true, true><<<g, NT, 0, s>>>(a);
+    else
+      spmm_nzpar_kernel<LV, QPR, U, true, false, NT, 0, false, true><<<g, NT, 0, s>>>(a);
+  } else if (epi) {
     if (tail)
       spmm_nzpar_kernel<LV, QPR, U, false, true, NT, 0, false, true><<<g, NT, 0, s>>>(a);
     else if (full)
@@ -501,7 +516,7 @@ int spmm_tune() {
 
 template <int LV, int QPR>
 void launch_nzpar(const SpmmArgs& a, bool acc, bool epi, cudaStream_t s) {
-  if (epi) return launch_nzpar_v<LV, QPR, 4, 128, 0>(a, false, true, s);
+  if (epi) return launch_nzpar_v<LV, QPR, 4, 128, 0>(a, acc, true, s);
   switch (spmm_tune()) {
     case 1: return launch_nzpar_v<LV, QPR, 4, kThreads, 0>(a, acc, false, s);
     case 2: return launch_nzpar_v<LV, QPR, 4, 128, 1>(a, acc, false, s);
@@ -587,10 +602,12 @@ void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_
                        (reinterpret_cast<uintptr_t>(H) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(T) % 16 == 0);
   if (epi) {
-    require(!accumulate && aligned && f <= kSpmmEpiMaxF && epi->fo <= kSpmmEpiMaxFo,
+    require(aligned && f <= kSpmmEpiMaxF && epi->fo <= kSpmmEpiMaxFo,
             "spmm: fused epilogue needs a final f <= 32 SpMM on 16 B-aligned rows");
+    require(!accumulate || epi->W == nullptr,
+            "spmm: an accumulating fused epilogue cannot change the row width");
     SpmmArgs a{n_rows, seg_begin, seg_end, col_idx, vals, H, ldh, f, T, ldt, mean, *epi};
-    dispatch<4>(a, false, true, stream);
+    dispatch<4>(a, accumulate, true, stream);
     return;
   }
   // Column chunks of at most 32 lanes * 8 vectors keep accumulators in registers.

@@ -338,8 +338,8 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const ke
   // from an L2-resident slice (SURVEY §7 hard parts).
   const int nb = spmm_passes(a, h);
   if (epi) {
-    if (acc || nb > 1) throw std::logic_error("spmm: fused epilogue needs one final pass");
-    spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, false, epi);
+    if (nb > 1) throw std::logic_error("spmm: fused epilogue needs one pass");
+    spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, acc, epi);
     return;
   }
   if (nb <= 1 || a.nnz == 0 || out.rows != a.n_rows || out.cols != h.cols) {
