@@ -379,7 +379,7 @@ __device__ __forceinline__ void spmm_row_epilogue(const SpmmArgs& a, int64_t row
 // partial sums are folded with xor shuffles at the end (deterministic order).
 template <int LV, int QPR, int U, bool ACC, bool TAIL, int NT = kThreads, int HINT = 0,
           bool FULLV = false, bool EPI = false>
-__global__ void __launch_bounds__(NT, 1024 / NT) spmm_nzpar_kernel(const SpmmArgs a) {
+__global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArgs a) {
   constexpr int TEAM = LV * QPR;
   constexpr int RPW = 32 / TEAM;
   const int lane = threadIdx.x & 31;

@@ -1,12 +1,18 @@
-# One GPU pass: gpu tests, smoke, bench (1 GPU), ncu launch list, ncu --set full of top kernels.
+# One GPU pass: gpu tests, smoke, bench (1 GPU), ncu launch list, ncu --set full of the top kernels.
+# ncu reports stay in /tmp on the box; their summaries come back in gpurun_out/.
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-nvidia-smi > gpurun_out/nvsmi.txt 2>&1
-timeout 900 python -m pytest tests -m gpu -q --timeout 240 -p no:cacheprovider -rf > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
-timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; echo "rc=$?" >> gpurun_out/bench.log
-timeout 600 python bench.py --steps 5 --warmup 3 --reference-order --no-alt --no-cpu-baseline > gpurun_out/bench_reforder.log 2>&1
-CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-alt"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:spmm -s 2 -c 1 -o gpurun_out/prof_spmm $CMD > gpurun_out/ncu_full1.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemm -s 2 -c 1 -o gpurun_out/prof_gemm $CMD > gpurun_out/ncu_full2.log 2>&1
+R=${ROUND_TAG:-r01_s4}
+O=gpurun_out/$R
+mkdir -p $O/prof
+nvidia-smi > $O/nvsmi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q --timeout 240 -p no:cacheprovider -rf > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
+timeout 600 python bench.py --steps 5 --warmup 3 > $O/bench.log 2>&1; echo "rc=$?" >> $O/bench.log
+[ -n "$SKIP_NCU" ] && exit 0
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-alt"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file $O/launches.csv $CMD > $O/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm -s 6 -c 1 -o /tmp/prof_spmm16 $CMD > $O/ncu_f1.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tm -s 7 -c 3 -o /tmp/prof_gemm_tm $CMD > $O/ncu_f2.log 2>&1
+CAGNET_PROF_DIR=$O/prof python scripts/summarize_ncu.py $R $O/launches.csv /tmp/prof_spmm16.ncu-rep=spmm_f16 /tmp/prof_gemm_tm.ncu-rep > $O/summ.log 2>&1
+for r in /tmp/prof_*.ncu-rep; do ncu -i $r --page raw --csv > $O/prof/$(basename $r .ncu-rep)_raw.csv 2>/dev/null; done
+ls -la /tmp/*.ncu-rep >> $O/summ.log
