@@ -101,7 +101,11 @@ struct SpmmArgs {
   SpmmEpi epi;          // fused row epilogue (EPI kernels only)
 };
 
-// VEC = 4: 16-byte vectors (requires 16 B aligned rows); VEC = 1: scalars.
+// VEC = 4: 16-byte vectors (requires 16 B aligned rows, ld a multiple of 4); VEC = 1: scalars.
+// With VEC = 4 a row's last vector is always gathered whole, even when f is not a
+// multiple of 4: the floats past f lie inside the row's padded leading dimension, only
+// feed accumulator lanes that are never stored (stores and the accumulate read are
+// masked to f), so a ragged width costs no scalar loads.
 template <int VEC, int LPR, int VPL, bool ACC, bool TAIL>
 __global__ void __launch_bounds__(kThreads, VPL == 1 ? 4 : 1) spmm_rows_kernel(const SpmmArgs a) {
   using V = typename VecT<VEC>::T;
@@ -169,8 +173,7 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? 4 : 1) spmm_rows_kernel(c
             zero_vec(hv[i]);
             if (vec < nvec) {
               if constexpr (VEC == 4)
-                hv[i] = TAIL ? load_vec(hrow, vec, f)
-                             : __ldg(reinterpret_cast<const float4*>(hrow) + vec);
+                hv[i] = __ldg(reinterpret_cast<const float4*>(hrow) + vec);
               else
                 hv[i] = __ldg(hrow + vec);
             }
@@ -217,8 +220,7 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? 4 : 1) spmm_rows_kernel(c
             // dead slots read nothing and contribute w = 0 times 0.
             if constexpr (VEC == 4)
               hv[tb][i] = (live && vec < nvec)
-                              ? (TAIL ? load_vec(hrow, vec, f)
-                                      : __ldg(reinterpret_cast<const float4*>(hrow) + vec))
+                              ? __ldg(reinterpret_cast<const float4*>(hrow) + vec)
                               : zero;
             else
               hv[tb][i] = (live && vec < nvec) ? __ldg(hrow + vec) : zero;
@@ -253,21 +255,11 @@ __global__ void __launch_bounds__(kThreads, VPL == 1 ? 4 : 1) spmm_rows_kernel(c
 template <int VEC, int LPR, int VPL>
 void launch_one(const SpmmArgs& a, bool acc, cudaStream_t s) {
   constexpr int rows_per_block = (kThreads / 32) * (32 / LPR);
-  const int64_t blocks = ceil_div64(a.n_rows, rows_per_block);
-  const unsigned g = static_cast<unsigned>(blocks);
-  // The scalar-tail path is only compiled in when f is not a multiple of 4.
-  const bool tail = VEC == 4 && (a.f % 4) != 0;
-  if (acc) {
-    if (tail)
-      spmm_rows_kernel<VEC, LPR, VPL, true, true><<<g, kThreads, 0, s>>>(a);
-    else
-      spmm_rows_kernel<VEC, LPR, VPL, true, false><<<g, kThreads, 0, s>>>(a);
-  } else {
-    if (tail)
-      spmm_rows_kernel<VEC, LPR, VPL, false, true><<<g, kThreads, 0, s>>>(a);
-    else
-      spmm_rows_kernel<VEC, LPR, VPL, false, false><<<g, kThreads, 0, s>>>(a);
-  }
+  const unsigned g = static_cast<unsigned>(ceil_div64(a.n_rows, rows_per_block));
+  if (acc)
+    spmm_rows_kernel<VEC, LPR, VPL, true, false><<<g, kThreads, 0, s>>>(a);
+  else
+    spmm_rows_kernel<VEC, LPR, VPL, false, false><<<g, kThreads, 0, s>>>(a);
   CG_LAUNCH_CHECK();
 }
 
@@ -409,7 +401,6 @@ __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArg
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   auto gather = [&](int c) -> float4 {
     if (!vec_ok) return make_float4(0.f, 0.f, 0.f, 0.f);
-    if (TAIL) return load_vec(a.H + static_cast<int64_t>(c) * a.ldh, vec, f);
     const float4* src = reinterpret_cast<const float4*>(
         hbase + static_cast<uint64_t>(static_cast<uint32_t>(c)) * ldh_bytes);
     if (HINT) return ldg_policy(src, pol);
@@ -468,33 +459,25 @@ template <int LV, int QPR, int U, int NT, int HINT>
 void launch_nzpar_v(const SpmmArgs& a, bool acc, bool epi, cudaStream_t s) {
   constexpr int rows_per_block = (NT / 32) * (32 / (LV * QPR));
   const unsigned g = static_cast<unsigned>(ceil_div64(a.n_rows, rows_per_block));
-  const bool tail = (a.f % 4) != 0;
-  const bool full = !tail && (a.f / 4) == LV;
+  // Full vectors: every lane of the LV-wide row team owns a live float4.
+  const bool full = (a.f + 3) / 4 == LV;
   if (epi && acc) {
-    if (tail)
-      spmm_nzpar_kernel<LV, QPR, U, true, true, NT, 0, false, true><<<g, NT, 0, s>>>(a);
-    else if (full)
+    if (full)
       spmm_nzpar_kernel<LV, QPR, U, true, false, NT, 0, true, true><<<g, NT, 0, s>>>(a);
     else
       spmm_nzpar_kernel<LV, QPR, U, true, false, NT, 0, false, true><<<g, NT, 0, s>>>(a);
   } else if (epi) {
-    if (tail)
-      spmm_nzpar_kernel<LV, QPR, U, false, true, NT, 0, false, true><<<g, NT, 0, s>>>(a);
-    else if (full)
+    if (full)
       spmm_nzpar_kernel<LV, QPR, U, false, false, NT, 0, true, true><<<g, NT, 0, s>>>(a);
     else
       spmm_nzpar_kernel<LV, QPR, U, false, false, NT, 0, false, true><<<g, NT, 0, s>>>(a);
   } else if (acc) {
-    if (tail)
-      spmm_nzpar_kernel<LV, QPR, U, true, true, NT, 0><<<g, NT, 0, s>>>(a);
-    else if (full)
+    if (full)
       spmm_nzpar_kernel<LV, QPR, U, true, false, NT, HINT, true><<<g, NT, 0, s>>>(a);
     else
       spmm_nzpar_kernel<LV, QPR, U, true, false, NT, HINT><<<g, NT, 0, s>>>(a);
   } else {
-    if (tail)
-      spmm_nzpar_kernel<LV, QPR, U, false, true, NT, 0><<<g, NT, 0, s>>>(a);
-    else if (full)
+    if (full)
       spmm_nzpar_kernel<LV, QPR, U, false, false, NT, HINT, true><<<g, NT, 0, s>>>(a);
     else
       spmm_nzpar_kernel<LV, QPR, U, false, false, NT, HINT><<<g, NT, 0, s>>>(a);

@@ -59,6 +59,20 @@ def test_spmm_matches_oracle(cg, orc, torch, f, acc):
         torch.cuda.synchronize()
         got = T.cpu().numpy()[:, :f]
         assert rel(got, want) < 1e-6, (f, ld)
+    # Ragged width in a padded layout: the vector path gathers the last vector of
+    # every row whole, so junk (NaN) in H's padding must not reach the valid
+    # columns, and T's padding columns must stay untouched.
+    ld = ((f + 3) // 4) * 4 + 4
+    H = padded(torch, h, ld)
+    H[:, f:] = float("nan")
+    T = padded(torch, t0, ld)
+    T[:, f:] = 7.0
+    cg.check(cg.lib.cagnet_spmm_csr_f32(n, n, a.nnz, rp, ci, v, H.data_ptr(), ld, f,
+                                        T.data_ptr(), ld, acc, stream(torch)))
+    torch.cuda.synchronize()
+    got = T.cpu().numpy()
+    assert rel(got[:, :f], want) < 1e-6, (f, "junk padding")
+    assert (got[:, f:] == 7.0).all(), "spmm wrote into the padding columns"
 
 
 # Fused SpMM row epilogue (the GCN layer's next dense step): raw copy, dense
