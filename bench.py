@@ -60,6 +60,8 @@ def parse():
     p.add_argument("--reference-order", action="store_true",
                    help="propagate as the reference does, (A^T H) W, instead of the default "
                         "narrow-first A^T (H W) on 1D/1.5D (same product)")
+    p.add_argument("--overlap", action="store_true",
+                   help="1D peer-memory stages: own-block SpMM overlapped with the pushes")
     p.add_argument("--no-alt", action="store_true",
                    help="skip timing the other propagation order")
     p.add_argument("--fuse", type=int, default=1,
@@ -238,7 +240,7 @@ def run_ours(args, cfg):
     kind = args.strategy
     repl = args.repl or (2 if kind == "1.5d" else 1)
     strat = cg.Strategy(kind, N, repl, args.block, reassociate=not args.reference_order,
-                        fuse=args.fuse)
+                        fuse=args.fuse, overlap=args.overlap)
 
     # NCCL bootstrap for the library's own communicators.
     nid = None

@@ -251,8 +251,12 @@ CAGNET_API int cagnet_trainer_ledger(cagnet_trainer_t t, uint64_t* out20);
 /* Enable/disable per-category CUDA-event timing (adds event records; default off). */
 CAGNET_API int cagnet_trainer_set_timing(cagnet_trainer_t t, int on);
 /* Trainer options: "reassociate" (1 = narrow-first propagation Aᵀ(H W) when
- * f_out < f_in, block-row strategies; same product, f_out-wide panels),
- * "timing" (per-launch CUDA-event profile). */
+ * f_out < f_in, Tᵀ G backward when f_out > f_in; same products, narrower panels),
+ * "timing" (per-launch CUDA-event profile), "fuse" (SpMM row epilogues: 0/1/2),
+ * "graph" (CUDA-graph epochs), "resident_sparse" (2D/3D tiles kept in HBM),
+ * "p2p" (1D stage panels through NVLink peer memory), "overlap" (1D peer-memory
+ * stages: own vertex block SpMM while the pushes fly).  Set before distribute()
+ * for resident_sparse / p2p / overlap. */
 CAGNET_API int cagnet_trainer_set_option(cagnet_trainer_t t, const char* name, int64_t value);
 /* Per-launch CUDA-event profile, aggregated by kernel name (e.g. "spmm_f602"):
  * out4 = {launches, total_ms, algorithmic_bytes, flops} (SURVEY §8(d) byte model). */

@@ -305,6 +305,25 @@ __global__ void block_fill_kernel(int64_t rows, int64_t c0, const int64_t* __res
   }
 }
 
+__global__ void rotate_rows_kernel(int64_t rows, int32_t c0, int32_t c1, const int64_t* __restrict__ rp,
+                                   const int32_t* __restrict__ ci, const float* __restrict__ v,
+                                   int32_t* __restrict__ oci, float* __restrict__ ov,
+                                   int64_t* __restrict__ mid) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (r >= rows) return;
+  const int64_t b = rp[r], e = rp[r + 1], len = e - b;
+  const int64_t lo = lower_bound_i32(ci, b, e, c0);
+  const int64_t hi = lower_bound_i32(ci, lo, e, c1);
+  if (lane == 0) mid[r] = b + (hi - lo);
+  for (int64_t t = lane; t < len; t += 32) {
+    int64_t src = lo + t;
+    if (src >= e) src -= len;
+    oci[b + t] = ci[src];
+    ov[b + t] = v[src];
+  }
+}
+
 // ---- features ----------------------------------------------------------------------
 constexpr int64_t kFeatChunk = 4096;
 
@@ -562,6 +581,22 @@ DeviceCsr extract_block_device(const DeviceCsr& a, int64_t r0, int64_t r1, int64
   CG_LAUNCH_CHECK();
   CG_CUDA(cudaStreamSynchronize(s));
   return b;
+}
+
+RotatedCsr rotate_rows_device(const DeviceCsr& a, int64_t c0, int64_t c1, cudaStream_t s) {
+  require(0 <= c0 && c0 <= c1 && c1 <= a.n_cols, "rotate_rows: column range outside the matrix");
+  RotatedCsr o;
+  o.col_idx.resize(static_cast<size_t>(std::max<int64_t>(a.nnz, 1)));
+  o.vals.resize(static_cast<size_t>(std::max<int64_t>(a.nnz, 1)));
+  o.mid.resize(static_cast<size_t>(std::max<int64_t>(a.n_rows, 1)));
+  if (a.n_rows > 0) {
+    rotate_rows_kernel<<<static_cast<unsigned>(ceil_div64(a.n_rows * 32, 256)), 256, 0, s>>>(
+        a.n_rows, static_cast<int32_t>(c0), static_cast<int32_t>(c1), a.row_ptr.get(), a.col_idx.get(),
+        a.vals.get(), o.col_idx.get(), o.vals.get(), o.mid.get());
+    CG_LAUNCH_CHECK();
+  }
+  CG_CUDA(cudaStreamSynchronize(s));
+  return o;
 }
 
 DeviceCsr upload_csr(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,

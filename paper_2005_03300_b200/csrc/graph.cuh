@@ -35,6 +35,16 @@ DeviceCsr permute_csr_device(const DeviceCsr& a, const int64_t* perm, const int6
 // csr.cpp:140-162.
 DeviceCsr extract_block_device(const DeviceCsr& a, int64_t r0, int64_t r1, int64_t c0,
                                int64_t c1, cudaStream_t s);
+// Rotated copy for the overlapped 1D stage (strategy_rows.cu): row r keeps its
+// nonzeros but starts at the first column >= c0, so the columns in [c0, c1)
+// (this rank's own vertex block) come first, then [c1, n), then [0, c0); the
+// out CSR shares a's row_ptr, and mid[r] ends the [c0, c1) group.
+struct RotatedCsr {
+  DevBuf<int32_t> col_idx;
+  DevBuf<float> vals;
+  DevBuf<int64_t> mid;
+};
+RotatedCsr rotate_rows_device(const DeviceCsr& a, int64_t c0, int64_t c1, cudaStream_t s);
 // Host arrays (int64 indices; fp64 values or NULL = unit) → device.
 DeviceCsr upload_csr(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
                      const int64_t* col_idx, const double* vals, cudaStream_t s);

@@ -39,26 +39,31 @@ __device__ void spin_until_geq(const uint64_t* p, uint64_t target) {
 struct Flags {
   int P;
   __device__ uint64_t* ready(uint64_t* f) const { return f; }
-  __device__ uint64_t* consumed(uint64_t* f) const { return f + P; }
-  __device__ uint64_t* ctr(uint64_t* f) const { return f + 2 * P; }
-  __device__ uint64_t* arrivals(uint64_t* f) const { return f + 2 * P + 1; }
+  __device__ uint64_t* pub_ctr(uint64_t* f) const { return f + P; }
+  __device__ uint64_t* wait_ctr(uint64_t* f) const { return f + P + 1; }
+  __device__ uint64_t* arrivals(uint64_t* f) const { return f + P + 2; }
 };
 
+// Copies the panel into slot `rank` of every destination buffer; the last CTA
+// to finish raises ready[rank] = s on every peer (s = this rank's publish count).
 __global__ void publish_kernel(float* const* bufs, uint64_t* const* flags, int rank, int P,
-                               const float* __restrict__ src, int64_t ld_src, uint32_t rows,
-                               uint32_t c4, int64_t slot_floats, int64_t ld_dst) {
+                               bool skip_self, const float* __restrict__ src, int64_t ld_src,
+                               uint32_t rows, uint32_t c4, int64_t slot_floats, int64_t ld_dst) {
   const Flags F{P};
   uint64_t* my = flags[rank];
-  const uint64_t s = *F.ctr(my) + 1;
+  const uint64_t s = *F.pub_ctr(my) + 1;
   const uint32_t total = rows * c4;
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const uint32_t r = e / c4, c = e - r * c4;
     const float4 v = *reinterpret_cast<const float4*>(src + r * ld_src + 4 * c);
     const int64_t off = rank * slot_floats + r * ld_dst + 4 * c;
-    for (int q = 0; q < P; ++q) *reinterpret_cast<float4*>(bufs[q] + off) = v;
+#pragma unroll 4
+    for (int d = 1; d <= P; ++d) {
+      const int q = (rank + d) % P;  // peers first, self last
+      if (q == rank && skip_self) continue;
+      *reinterpret_cast<float4*>(bufs[q] + off) = v;
+    }
   }
-  // Grid completion: every block fences its stores system-wide and arrives;
-  // the last block raises ready[rank] in every rank's flags (self included).
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -66,39 +71,23 @@ __global__ void publish_kernel(float* const* bufs, uint64_t* const* flags, int r
         atomicAdd(reinterpret_cast<unsigned long long*>(F.arrivals(my)), 1ull);
     if (prev == gridDim.x - 1) {
       *F.arrivals(my) = 0;
+      *F.pub_ctr(my) = s;
       __threadfence_system();
-      for (int q = 0; q < P; ++q) st_release_sys(F.ready(flags[q]) + rank, s);
+      for (int q = 0; q < P; ++q)
+        if (q != rank) st_release_sys(F.ready(flags[q]) + rank, s);
     }
   }
-}
-
-// Buffer parity s & 1 last held stage s - 2: every peer must be done with it
-// before this rank overwrites its slot there (one spinning block only, so the
-// copy kernel never holds SMs while waiting).
-__global__ void wait_free_kernel(uint64_t* const* flags, int rank, int P) {
-  const Flags F{P};
-  uint64_t* my = flags[rank];
-  const uint64_t s = *F.ctr(my) + 1;
-  const int q = threadIdx.x;
-  if (s > 2 && q < P && q != rank) spin_until_geq(F.consumed(my) + q, s - 2);
 }
 
 __global__ void wait_ready_kernel(uint64_t* const* flags, int rank, int P) {
   const Flags F{P};
   uint64_t* my = flags[rank];
-  const uint64_t s = *F.ctr(my) + 1;
-  const int q = threadIdx.x;
-  if (q < P && q != rank) spin_until_geq(F.ready(my) + q, s);
+  const uint64_t s = *F.wait_ctr(my) + 1;
+  for (int q = threadIdx.x; q < P; q += blockDim.x)
+    if (q != rank) spin_until_geq(F.ready(my) + q, s);
   __threadfence_system();
-}
-
-__global__ void consumed_kernel(uint64_t* const* flags, int rank, int P) {
-  const Flags F{P};
-  uint64_t* my = flags[rank];
-  const uint64_t s = *F.ctr(my) + 1;
-  for (int q = 0; q < P; ++q)
-    if (q != rank) st_release_sys(F.consumed(flags[q]) + rank, s);
-  *F.ctr(my) = s;
+  __syncthreads();
+  if (threadIdx.x == 0) *F.wait_ctr(my) = s;
 }
 
 struct PeerInfo {
@@ -130,8 +119,8 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
   // Allocate first so every rank can advertise handles; freed again on fallback.
   CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&base_[0]), bytes));
   CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&base_[1]), bytes));
-  CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&flags_), (2 * P + 2) * sizeof(uint64_t)));
-  CG_CUDA(cudaMemset(flags_, 0, (2 * P + 2) * sizeof(uint64_t)));
+  CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&flags_), (P + 3) * sizeof(uint64_t)));
+  CG_CUDA(cudaMemset(flags_, 0, (P + 3) * sizeof(uint64_t)));
   CG_CUDA(cudaMemset(base_[0], 0, bytes));
   CG_CUDA(cudaMemset(base_[1], 0, bytes));
 
@@ -236,7 +225,7 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
 }
 
 void PeerPanels::publish(int b, const float* src, int64_t ld_src, int64_t rows, int64_t cols,
-                         int64_t slot_floats, int64_t ld_dst, cudaStream_t s) {
+                         int64_t slot_floats, int64_t ld_dst, bool skip_self, cudaStream_t s) {
   require(ld_src % 4 == 0 && ld_dst % 4 == 0 && slot_floats % 4 == 0 &&
               reinterpret_cast<uintptr_t>(src) % 16 == 0,
           "PeerPanels::publish: rows must be 16 B aligned");
@@ -246,21 +235,14 @@ void PeerPanels::publish(int b, const float* src, int64_t ld_src, int64_t rows, 
   int blocks = static_cast<int>(ceil_div64(total > 0 ? total : 1, 256));
   const int cap = 2 * num_sms(device_);
   if (blocks > cap) blocks = cap;
-  wait_free_kernel<<<1, 32 * ((ranks_ + 31) / 32), 0, s>>>(d_flags_.get(), rank_, ranks_);
-  CG_LAUNCH_CHECK();
-  publish_kernel<<<blocks, 256, 0, s>>>(d_bufs_[b].get(), d_flags_.get(), rank_, ranks_, src, ld_src,
-                                        static_cast<uint32_t>(rows), static_cast<uint32_t>(c4),
+  publish_kernel<<<blocks, 256, 0, s>>>(d_bufs_[b].get(), d_flags_.get(), rank_, ranks_, skip_self, src,
+                                        ld_src, static_cast<uint32_t>(rows), static_cast<uint32_t>(c4),
                                         slot_floats, ld_dst);
   CG_LAUNCH_CHECK();
 }
 
 void PeerPanels::wait_ready(cudaStream_t s) {
   wait_ready_kernel<<<1, 32 * ((ranks_ + 31) / 32), 0, s>>>(d_flags_.get(), rank_, ranks_);
-  CG_LAUNCH_CHECK();
-}
-
-void PeerPanels::consumed(cudaStream_t s) {
-  consumed_kernel<<<1, 1, 0, s>>>(d_flags_.get(), rank_, ranks_);
   CG_LAUNCH_CHECK();
 }
 

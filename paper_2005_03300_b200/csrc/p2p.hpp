@@ -8,10 +8,16 @@
 // rows straight into every peer's panel buffer over NVLink (CUDA IPC mapped
 // peer memory, one copy kernel writing P slots), then raises a per-peer
 // ready flag in the peer's memory; consumers spin on their local flags before
-// the SpMM.  Double-buffered slots plus per-peer "consumed" flags (written
-// by the consumer into the producer's memory after its SpMM) make buffer
-// reuse safe across stages.  Flags carry a device-side stage sequence number,
-// so the exchange works unchanged inside a replayed CUDA graph.
+// the SpMM.  Flags carry a device-side stage sequence number, so the exchange
+// works unchanged inside a replayed CUDA graph.
+//
+// Buffer reuse needs no "consumed" flags: slots are double-buffered and every
+// rank waits for all peers' ready flags at every stage, on the stream that
+// also runs its SpMMs, and publishes stage s only after that stream passed
+// its wait for stage s-1.  A peer's ready(s-1) is raised only after the
+// peer's SpMM of stage s-2 — the last reader of the buffer that stage s
+// overwrites — has finished (stream order on the peer), so when a rank
+// publishes stage s nobody still reads that buffer.
 //
 // All waits are bounded (~20 s of spinning, then __trap()), so a broken peer
 // aborts the kernel instead of hanging the GPU.
@@ -46,21 +52,21 @@ class PeerPanels {
   float* buffer(int b) const { return base_[b]; }
 
   // Publishes rows x cols (ld_src) of `src` into slot `rank` of buffer b on
-  // every rank (self included) at leading dimension ld_dst, after all peers
-  // released buffer b from two stages ago; raises the ready flags.
+  // every peer (and on this rank too unless skip_self) at leading dimension
+  // ld_dst, then raises this stage's ready flag on every peer.  The stream
+  // must already be ordered after this rank's wait_ready() of the previous
+  // stage (see above).
   void publish(int b, const float* src, int64_t ld_src, int64_t rows, int64_t cols,
-               int64_t slot_floats, int64_t ld_dst, cudaStream_t s);
-  // Waits until every peer published the current stage.
+               int64_t slot_floats, int64_t ld_dst, bool skip_self, cudaStream_t s);
+  // Waits until every peer published the current stage, then advances the
+  // local stage counter.
   void wait_ready(cudaStream_t s);
-  // Marks the current stage's buffer as consumed on every peer and advances
-  // the local stage counter.
-  void consumed(cudaStream_t s);
 
  private:
   int rank_ = 0, ranks_ = 1, device_ = 0;
   bool same_process_ = false;
   float* base_[2] = {nullptr, nullptr};  // own allocations
-  uint64_t* flags_ = nullptr;            // own: ready[P] | consumed[P] | ctr | arrivals
+  uint64_t* flags_ = nullptr;            // own: ready[P] | pub_ctr | wait_ctr | arrivals
   std::vector<float*> peer_buf_[2];      // [b][q] (q == rank: own)
   std::vector<uint64_t*> peer_flags_;    // [q]
   DevBuf<float*> d_bufs_[2];             // device copies of peer_buf_

@@ -53,6 +53,13 @@ class TrainerRows final : public Trainer {
         const size_t bytes = static_cast<size_t>(ceil_div64(data_.n, blocks()) * blocks()) *
                              kCoalesceMaxF * sizeof(float);
         p2p_ok_ = p2p_.init(*comm_, rank_, grid_.ranks(), device_, bytes, cs_);
+        overlap_ok_ = p2p_ok_ && overlap_enabled_;
+        if (overlap_ok_) {
+          // Own vertex block first in every row (columns relative to c_lo_).
+          own_ = block_range(data_.n, blocks(), rank_);
+          a_rot_ = rotate_rows_device(a_chunk_, own_.begin - c_lo_, own_.end - c_lo_, cs_);
+          at_rot_ = rotate_rows_device(at_chunk_, own_.begin - c_lo_, own_.end - c_lo_, cs_);
+        }
       }
     }
     CG_CUDA(cudaDeviceSynchronize());
@@ -249,9 +256,38 @@ class TrainerRows final : public Trainer {
       // into adjacent slots and one SpMM consumes them all.
       const DeviceCsr& blk = &parts == &a_parts_ ? a_chunk_ : at_chunk_;
       Mat g{gbuf_.m.p, c_hi_ - c_lo_, mine.cols, mine.ld};
+      if (one_d() && p2p_ok_ && overlap_ok_ && spmm_single_pass(blk, Mat{nullptr, c_hi_ - c_lo_, mine.cols, mine.ld}) &&
+          !(epi && epi->W)) {
+        // Peer-memory stage with overlap: the pushes to the peers run on the
+        // comm stream while this stream SpMMs the own vertex block straight
+        // from the local panel (rows rotated so those columns come first),
+        // then the remaining columns from the filled buffer, accumulating,
+        // with the fused row epilogue on that last pass.
+        const int64_t step = ceil_div64(data_.n, blocks());
+        const int b = static_cast<int>(p2p_stage_++ & 1);
+        Mat pg{p2p_.buffer(b), c_hi_ - c_lo_, mine.cols, mine.ld};
+        std::vector<uint64_t> words;
+        for (int q = 0; q < blocks(); ++q)
+          words.push_back(static_cast<uint64_t>(block_range(data_.n, blocks(), q).size() * mine.cols));
+        comm_->meter_bcast_all(grp, Category::DBcast, words);
+        const RotatedCsr& rot = &parts == &a_parts_ ? a_rot_ : at_rot_;
+        const double own_share = static_cast<double>(own_.size()) / static_cast<double>(std::max<int64_t>(blk.n_cols, 1));
+        const int64_t own_nnz = static_cast<int64_t>(own_share * static_cast<double>(blk.nnz));
+        ms_after_cs();
+        p2p_.publish(b, mine.p, mine.ld, mine.rows, mine.cols, step * mine.ld, mine.ld, /*skip_self=*/true, ms_);
+        // Column c of the block row is row c - own.begin of the local panel.
+        const Mat own_panel{mine.p - (own_.begin - c_lo_) * mine.ld, mine.rows, mine.cols, mine.ld};
+        spmm_seg(blk.n_rows, own_nnz, blk.row_ptr.get(), rot.mid.get(), rot.col_idx.get(), rot.vals.get(),
+                 own_panel, out, false, nullptr, "spmm_own");
+        p2p_.wait_ready(cs_);
+        cs_after_ms();  // own pushes done before anything overwrites `mine`
+        spmm_seg(blk.n_rows, blk.nnz - own_nnz, rot.mid.get(), blk.row_ptr.get() + 1, rot.col_idx.get(),
+                 rot.vals.get(), pg, out, true, epi, "spmm");
+        return;
+      }
       ms_after_cs();
       const int own = one_d() ? rank_ : grid_.row_of(rank_);
-      if (own >= chunk_begin(j) && own < chunk_end(j)) {
+      if (own >= chunk_begin(j) && own < chunk_end(j) && !(one_d() && p2p_ok_)) {
         const BlockRange r = block_range(data_.n, blocks(), own);
         kern::copy2d(g.p + (r.begin - c_lo_) * g.ld, g.ld, mine.p, mine.ld, mine.rows, mine.cols, ms_);
       }
@@ -265,10 +301,9 @@ class TrainerRows final : public Trainer {
         for (int q = 0; q < blocks(); ++q)
           words.push_back(static_cast<uint64_t>(block_range(data_.n, blocks(), q).size() * mine.cols));
         comm_->meter_bcast_all(grp, Category::DBcast, words);
-        p2p_.publish(b, mine.p, mine.ld, mine.rows, mine.cols, step * mine.ld, mine.ld, cs_);
+        p2p_.publish(b, mine.p, mine.ld, mine.rows, mine.cols, step * mine.ld, mine.ld, /*skip_self=*/false, cs_);
         p2p_.wait_ready(cs_);
         spmm(blk, pg, out, false, epi);
-        p2p_.consumed(cs_);
         return;
       }
       if (one_d()) {
@@ -348,6 +383,9 @@ class TrainerRows final : public Trainer {
   OwnedMat gbuf_;                 // stage panels side by side
   PeerPanels p2p_;                // NVLink peer-memory panel exchange (1D)
   bool p2p_ok_ = false;
+  bool overlap_ok_ = false;       // own-block SpMM overlaps the peer pushes
+  BlockRange own_{0, 0};          // this rank's vertex block (1D)
+  RotatedCsr a_rot_, at_rot_;     // chunk CSRs with the own block first per row
   uint64_t p2p_stage_ = 0;        // host parity of the double-buffered panels
   std::vector<OwnedMat> saved_t_;  // T = Aᵀ H of widening layers (narrow-first backward)
   std::vector<bool> saved_valid_;

@@ -152,6 +152,15 @@ class TrainerSumma final : public Trainer {
       Mat part{partial_.m.p, blockrow.size(), prevc.size(), padded_ld(prevc.size())};
       propagate(at_parts_[0], /*transpose=*/true, h, chunks(prevc.size()), part);
       Mat t = fiber_reduce_scatter(part, i);
+      // A widening layer keeps its T tile for the narrow-first backward
+      // (Y = Tᵀ G instead of Hᵀ (A G), see backward_and_step).
+      if (saved_t_.size() < static_cast<size_t>(num_layers())) saved_t_.resize(static_cast<size_t>(num_layers()));
+      OwnedMat& keep = saved_t_[static_cast<size_t>(l)];
+      keep_t_valid(l, reassociate_ && wcur > wprev);
+      if (reassociate_ && wcur > wprev) {
+        if (keep.m.p == nullptr) keep.alloc(t.rows, t.cols);
+        kern::copy2d(keep.m.p, keep.m.ld, t.p, t.ld, t.rows, t.cols, cs_);
+      }
       // Phase 2: Z = sum_q T[i, q] * W[F_q, F_j] (+ ReLU into H_l).
       row_gemm(t, l, wprev, mycur, z, !last, h_[static_cast<size_t>(l)].m);
     }
@@ -191,6 +200,11 @@ class TrainerSumma final : public Trainer {
       const BlockRange mycur = tile_cols(rank_, wcur);
       const BlockRange myprev = tile_cols(rank_, wprev);
       const Mat& g = g_[static_cast<size_t>(l - 1)].m;
+
+      if (reassociate_ && t_valid(l)) {
+        narrow_backward(l, g);
+        continue;
+      }
 
       // S = A * G with the same split as the forward propagation.
       Mat part{partial_.m.p, blockrow.size(), mycur.size(), padded_ld(mycur.size())};
@@ -312,6 +326,88 @@ class TrainerSumma final : public Trainer {
     return Mat{utile_.m.p, rows, block_range(fout, side(), j).size(), ld};
   }
 
+  // Narrow-first backward of a widening layer (wcur > wprev), the SUMMA form of
+  // the 1D one (strategy_rows.cu):
+  //   Y = Hᵀ (A G) = (Aᵀ H)ᵀ G = Tᵀ G with the T tile kept by the forward pass:
+  //     the G tiles of the row group are swept like the reference's S panels
+  //     (dist_2d.cpp:150-170) and the Y strips meet in the column (+fiber)
+  //     all-reduce and the row all-gather;
+  //   G_prev = (A (G Wᵀ)) ⊙ relu′(Z_prev): every rank multiplies its G tile by
+  //     its W column slab for all f_prev columns, the row group reduce-scatters
+  //     the f_prev column blocks, and the SUMMA propagation moves f_prev / √P
+  //     wide panels instead of f_cur / √P wide ones.
+  void narrow_backward(int l, const Mat& g) {
+    const int i = grid_.row_of(rank_), j = grid_.col_of(rank_), k = grid_.layer_of(rank_);
+    const int64_t wcur = dims_[static_cast<size_t>(l)], wprev = dims_[static_cast<size_t>(l - 1)];
+    const BlockRange blockrow = block_range(data_.n, side(), i);
+    const BlockRange mycur = tile_cols(rank_, wcur);
+    const BlockRange myprev = tile_cols(rank_, wprev);
+    const Mat& t = saved_t_[static_cast<size_t>(l)].m;
+    Mat y = Y_[static_cast<size_t>(l - 1)].m;
+    const int64_t step_p = ceil_div64(wprev, side());
+    float* yslot = y.p + static_cast<int64_t>(j) * step_p * y.ld;
+    ms_after_cs();
+    for (int q = 0; q < side(); ++q) {
+      const BlockRange fq = block_range(wcur, side(), q);
+      const int groot = grid_.rank_at(i, q, k);
+      const int b = next_buffer();
+      Mat gpanel = dense_panel(grid_.row_group(rank_), groot, g, g.rows, fq.size(), {BlockRange{0, fq.size()}}, b)[0];
+      Mat strip{strip_.m.p, myprev.size(), fq.size(), fq.size() > 0 ? fq.size() : 1};
+      gemm_hts(t, gpanel, strip, false);
+      ms_after_cs();
+      comm_->all_reduce(grid_.col_group(rank_), strip.p, static_cast<size_t>(strip.rows * strip.cols),
+                        ncclFloat32, Category::Reduce, words(strip), ms_);
+      if (grid_.has_fiber_groups())
+        comm_->all_reduce(grid_.fiber_group(rank_), strip.p, static_cast<size_t>(strip.rows * strip.cols),
+                          ncclFloat32, Category::Reduce, words(strip), ms_);
+      cs_after_ms();
+      kern::copy2d(yslot + fq.begin, y.ld, strip.p, strip.ld, strip.rows, strip.cols, cs_);
+      release_buffer(b);
+    }
+    std::vector<uint64_t> slot_words;
+    for (int q = 0; q < side(); ++q)
+      slot_words.push_back(static_cast<uint64_t>(block_range(wprev, side(), q).size() * wcur));
+    ms_after_cs();
+    comm_->all_gather(grid_.row_group(rank_), yslot, y.p, static_cast<size_t>(step_p * wcur),
+                      ncclFloat32, Category::AllGather, slot_words, ms_);
+    cs_after_ms();
+    if (l < 2) return;
+    // U tile = sum_q G[rows, F_q(cur)] W[F_j(prev), F_q(cur)]ᵀ over the row group.
+    const int64_t rows = g.rows;
+    const int64_t wslot = ceil_div64(wprev, side());
+    const int64_t ld = padded_ld(wslot);
+    Mat full{pfull_.m.p, rows, wprev, padded_ld(wprev)};
+    gemm_swt(g, l - 1, 0, mycur.begin, full, false, kern::EPI_NONE, nullptr);
+    Mat u = full;
+    if (side() > 1) {
+      std::vector<uint64_t> red_words;
+      for (int q = 0; q < side(); ++q) {
+        const BlockRange oq = block_range(wprev, side(), q);
+        red_words.push_back(static_cast<uint64_t>(rows * oq.size()));
+        if (oq.size() > 0)
+          kern::copy2d(redbuf_.m.p + q * rows * ld, ld, full.p + oq.begin, full.ld, rows, oq.size(), cs_);
+      }
+      ms_after_cs();
+      comm_->reduce_scatter(grid_.row_group(rank_), redbuf_.m.p, utile_.m.p, static_cast<size_t>(rows * ld),
+                            ncclFloat32, Category::Reduce, red_words, ms_);
+      cs_after_ms();
+      u = Mat{utile_.m.p, rows, myprev.size(), ld};
+    }
+    Mat part{partial_.m.p, blockrow.size(), myprev.size(), padded_ld(myprev.size())};
+    propagate(a_parts_[0], /*transpose=*/false, u, {BlockRange{0, myprev.size()}}, part);
+    Mat st = fiber_reduce_scatter(part, i);
+    Mat gprev = g_[static_cast<size_t>(l - 2)].m;
+    const Mat& zp = z_[static_cast<size_t>(l - 2)].m;
+    kern::copy2d(gprev.p, gprev.ld, st.p, st.ld, st.rows, st.cols, cs_);
+    kern::mask_relu_prime(gprev.p, gprev.ld, zp.p, zp.ld, gprev.rows, gprev.cols, cs_);
+  }
+
+  void keep_t_valid(int l, bool v) {
+    if (t_valid_.size() < static_cast<size_t>(num_layers())) t_valid_.assign(static_cast<size_t>(num_layers()), false);
+    t_valid_[static_cast<size_t>(l)] = v;
+  }
+  bool t_valid(int l) const { return static_cast<size_t>(l) < t_valid_.size() && t_valid_[static_cast<size_t>(l)]; }
+
   // Double-buffered panel slots: a slot is reused only after the compute
   // stream finished with its previous contents.
   int next_buffer() {
@@ -428,6 +524,8 @@ class TrainerSumma final : public Trainer {
   std::vector<SparsePanel> resident_[2];  // [A, Aᵀ][q]: row-group tiles kept in HBM
   OwnedMat dpanel_[2];
   OwnedMat partial_, tslice_, strip_, gather_, utile_, pfull_, redbuf_;
+  std::vector<OwnedMat> saved_t_;  // T = Aᵀ H tiles of widening layers (narrow-first backward)
+  std::vector<bool> t_valid_;
   uint64_t slot_ = 0;
 };
 

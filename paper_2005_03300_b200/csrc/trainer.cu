@@ -220,7 +220,15 @@ Trainer::Trainer(const DeviceDataset& data, std::vector<int64_t> dims, const dou
   require(rank >= 0 && rank < grid_.ranks(), "trainer: rank outside the grid");
   CG_CUDA(cudaSetDevice(device_));
   CG_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
-  CG_CUDA(cudaStreamCreateWithFlags(&ms_, cudaStreamNonBlocking));
+  // The comm stream runs at the highest priority: its NCCL / peer-push
+  // kernels then get SM slots as soon as CTAs of a running SpMM retire
+  // instead of queueing behind the SpMM's whole grid (measured: SUMMA stage
+  // broadcasts otherwise start only after the previous stage's SpMM ends).
+  {
+    int lo = 0, hi = 0;
+    CG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CG_CUDA(cudaStreamCreateWithPriority(&ms_, cudaStreamNonBlocking, hi));
+  }
   CG_CUDA(cudaEventCreateWithFlags(&ev_cs_, cudaEventDisableTiming));
   CG_CUDA(cudaEventCreateWithFlags(&ev_ms_, cudaEventDisableTiming));
   for (int i = 0; i < 2; ++i) {
@@ -400,6 +408,21 @@ void Trainer::spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32
                (epi->mask ? 4.0 * r * fo : 0.0) + (epi->relu_out ? 4.0 * r * fo : 0.0);
     }
     prof_end(slot, "spmm", h.cols, bytes, 2.0 * nnz * f + (epi && epi->W ? 2.0 * r * f * width : 0.0));
+  }
+}
+
+void Trainer::spmm_seg(int64_t rows, int64_t nnz, const int64_t* seg_b, const int64_t* seg_e,
+                       const int32_t* ci, const float* v, const Mat& h, Mat out, bool acc,
+                       const kern::SpmmEpi* epi, const char* kind) {
+  if (out.rows != rows || out.cols != h.cols) throw std::invalid_argument("spmm: accumulator shape mismatch");
+  const int slot = prof_begin();
+  kern::spmm_segments(rows, seg_b, seg_e, ci, v, h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld, acc, cs_,
+                      nnz, epi);
+  if (slot >= 0) {
+    const double f = static_cast<double>(h.cols), r = static_cast<double>(rows);
+    double bytes = 16.0 * r + 8.0 * nnz + 4.0 * f * h.rows + 4.0 * f * r * (acc ? 2 : 1);
+    if (epi) bytes += (epi->mask ? 4.0 * r * f : 0.0) + (epi->relu_out ? 4.0 * r * f : 0.0);
+    prof_end(slot, kind, h.cols, bytes, 2.0 * nnz * f);
   }
 }
 

@@ -152,6 +152,10 @@ class Trainer {
   // NCCL all-gather (set before distribute(); falls back to NCCL when the
   // GPUs lack peer access).
   void set_p2p(bool on) { p2p_enabled_ = on; }
+  // 1D peer-memory stages: SpMM the rank's own vertex block from its local
+  // panel while the pushes to the peers are in flight, then the remaining
+  // columns (set before distribute(); off = one SpMM after the exchange).
+  void set_overlap(bool on) { overlap_enabled_ = on; }
   void reset_profile() {
     collect_profile();
     profile_.clear();
@@ -178,6 +182,11 @@ class Trainer {
   // next dense step runs in the SpMM's row epilogue (kern::SpmmEpi).
   void spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc,
             const kern::SpmmEpi* epi = nullptr);
+  // out (+)= A·h over row segments [seg_b[r], seg_e[r]) of (ci, v); h.p may be
+  // offset so that column index c addresses row c of the view (no shape check
+  // on h.rows).  `kind` labels the profile entry.
+  void spmm_seg(int64_t rows, int64_t nnz, const int64_t* seg_b, const int64_t* seg_e, const int32_t* ci,
+                const float* v, const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi, const char* kind);
   void spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32_t* ci, const float* v,
                 const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi = nullptr);
   // True when spmm(a, h, ...) is a single kernel pass (no L2 column blocking).
@@ -211,6 +220,7 @@ class Trainer {
   int fuse_ = 1;
   bool resident_sparse_ = true;
   bool p2p_enabled_ = true;
+  bool overlap_enabled_ = false;
   std::vector<ProfRec> recs_;
   size_t recs_used_ = 0;
   std::vector<ProfEntry> profile_;

@@ -1,0 +1,22 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/mq2
+run() { # name nproc args...
+  name=$1; np=$2; shift 2
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $np --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 400)) bench.py --gpus $np "$@" > gpurun_out/mq2/$name.log 2>&1; echo "rc=$?" >> gpurun_out/mq2/$name.log
+  python - gpurun_out/mq2/$name.log <<'PY'
+import json,sys
+l=[x for x in open(sys.argv[1]) if x.startswith('{')]
+if not l: print(sys.argv[1], "NO JSON", open(sys.argv[1]).read()[-800:]); sys.exit()
+d=json.loads(l[-1]); print(sys.argv[1], d["value"], "eager", d.get("eager_ms_per_step"), "e2e", d["e2e"]["value"], {k:(v["launches"],v["ms_per_launch"]) for k,v in d["kernels"].items()})
+PY
+}
+run 1d_n2 2 --steps 10 --warmup 3 --no-alt
+run 1d_n2_noov 2 --steps 10 --warmup 3 --no-alt --no-overlap
+run 1d_n4 4 --steps 10 --warmup 3 --no-alt
+run 1d_n4_noov 4 --steps 10 --warmup 3 --no-alt --no-overlap
+run 2d_n4 4 --strategy 2d --steps 10 --warmup 3 --no-alt
+run 15d_n4 4 --strategy 1.5d --steps 10 --warmup 3 --no-alt
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 400)) scripts/timeline.py --gpus 4 > gpurun_out/mq2/tl_4.log 2>&1
+mv gpurun_out/timeline_1d_n4_r0.txt gpurun_out/mq2/tl_1d_n4_ov_r0.txt 2>/dev/null
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 400)) scripts/timeline.py --gpus 4 --no-overlap > gpurun_out/mq2/tl_4n.log 2>&1
+mv gpurun_out/timeline_1d_n4_r0.txt gpurun_out/mq2/tl_1d_n4_noov_r0.txt 2>/dev/null

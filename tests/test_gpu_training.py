@@ -178,16 +178,39 @@ DIST = {  # name -> (kind, P, repl, block, n, dims)   (tests/golden/make_golden.
 @pytest.mark.multigpu
 @pytest.mark.parametrize("kind,P,repl", [("1d", 2, 1), ("1.5d", 4, 2), ("1d", 4, 1), ("2d", 4, 1),
                                         ("3d", 8, 1)])
-def test_distributed_reassociated(cg, orc, need_gpus, kind, P, repl):
+@pytest.mark.parametrize("dims", [[24, 8, 6], [24, 6, 8, 10]])
+def test_distributed_reassociated(cg, orc, need_gpus, kind, P, repl, dims):
     """Narrow-first propagation on every strategy (2D/3D: row-group GEMM
-    first, then SUMMA propagation of the f_out-wide U tiles)."""
+    first, then SUMMA propagation of the f_out-wide U tiles); the second dims
+    have widening layers (Y = Tᵀ G, G_prev = A (G Wᵀ) ⊙ relu′), one of them
+    in the middle of the network."""
     need_gpus(P)
-    dims = [24, 8, 6]
     model = cg.init_glorot(dims, 5, 0.5)
-    out = cg.run_distributed(lambda dev: cg.generate_dataset(50, 6.0, 24, 6, 2, 3, 4, device=dev),
+    out = cg.run_distributed(lambda dev: cg.generate_dataset(50, 6.0, 24, dims[-1], 2, 3, 4, device=dev),
                              model, cg.Strategy(kind, P, repl, reassociate=True), 3)
-    od = orc.generate_dataset(50, 6.0, 24, 6, 2, 3, 4)
+    od = orc.generate_dataset(50, 6.0, 24, dims[-1], 2, 3, 4)
     losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.5, 3)
+    res = dict(losses=out.losses, h_final=out.h_final, y=out.y_final, g=out.g_final,
+               w=out.model.weights)
+    assert max_rel_error(res, losses, h, y, g, w) < TOL
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("p2p,overlap", [(True, True), (True, False), (False, False)])
+def test_1d_exchange_paths(cg, orc, need_gpus, P, p2p, overlap):
+    """1D stage exchanges: NVLink peer-memory pushes with the own-block SpMM
+    overlapped, peer memory without overlap, and the NCCL all-gather — same
+    numbers as the serial oracle over graph-replayed epochs (the flag protocol
+    runs inside the replays)."""
+    need_gpus(P)
+    dims = [24, 8, 8, 6]
+    model = cg.init_glorot(dims, 5, 0.5)
+    strat = cg.Strategy("1d", P, 1, reassociate=True, p2p=p2p, overlap=overlap)
+    out = cg.run_distributed(lambda dev: cg.generate_dataset(300, 12.0, 24, 6, 2, 3, 4, device=dev),
+                             model, strat, 5)
+    od = orc.generate_dataset(300, 12.0, 24, 6, 2, 3, 4)
+    losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.5, 5)
     res = dict(losses=out.losses, h_final=out.h_final, y=out.y_final, g=out.g_final,
                w=out.model.weights)
     assert max_rel_error(res, losses, h, y, g, w) < TOL
