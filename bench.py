@@ -275,6 +275,7 @@ def run_ours(args, cfg):
     # (kernels + NCCL collectives); the warm-up above ran the eager epoch and
     # the capture.
     launches0 = cg.kernel_launches()
+    ledger0 = trainer.ledger()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         barrier()
@@ -284,6 +285,10 @@ def run_ours(args, cfg):
         end.record(stream)
         barrier()
     launches = cg.kernel_launches() - launches0
+    ledger1 = trainer.ledger()
+    # NVLink words received per rank per epoch (reference ledger conventions).
+    recv_words = sum(ledger1[c]["words_received"] - ledger0[c]["words_received"]
+                     for c in ledger1) / max(args.steps, 1)
     losses = trainer.losses()
     ms_total = start.elapsed_time(end)
 
@@ -377,6 +382,31 @@ def run_ours(args, cfg):
                 "share_of_step": round(dom["ms"] / max(ms_prof_total, 1e-9), 4),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
 
+    # ---- epoch roofline (north star): the slower of this rank's kernel bytes at
+    # HBM bandwidth and its received block bytes at NVLink bandwidth, max over ranks.
+    hbm_bytes = sum(v["bytes"] for v in prof.values()) / max(args.steps, 1)
+    link_bytes = recv_words * 4.0
+    rb = torch.tensor([hbm_bytes, link_bytes], dtype=torch.float64, device="cuda")
+    if pg:
+        pg.all_reduce(rb, op=pg.ReduceOp.MAX)
+    hbm_bytes, link_bytes = float(rb[0].item()), float(rb[1].item())
+    link_peak, link_meas = 900.0, 470.0
+    t_hbm = hbm_bytes / (peak * 1e9) * 1e3
+    t_link = link_bytes / (link_peak * 1e9) * 1e3
+    epoch_roof = {
+        "hbm_bytes_per_rank": round(hbm_bytes), "link_bytes_per_rank": round(link_bytes),
+        "t_hbm_ms": round(t_hbm, 4), "t_link_ms": round(t_link, 4),
+        "bound": "hbm" if t_hbm >= t_link else "nvlink",
+        "floor_ms": round(max(t_hbm, t_link), 4),
+        "frac": round(max(t_hbm, t_link) / max(ms_step, 1e-9), 4),
+        "link_peak_gbs": link_peak,
+        "t_link_measured_ms": round(link_bytes / (link_meas * 1e9) * 1e3, 4),
+        "link_measured_gbs": link_meas,
+        "source": "hbm: algorithmic bytes of every profiled kernel per epoch (SURVEY 8d byte "
+                  "model); link: ledger words_received x 4 B per epoch; NVLink 5 nominal "
+                  "900 GB/s per direction, measured all-to-all push ingress ~470 GB/s "
+                  "(profiles/r01_s4_micro_push_4gpu.txt)"}
+
     if rank != 0:
         if pg:
             pg.destroy_process_group()
@@ -415,6 +445,7 @@ def run_ours(args, cfg):
         "gpu_launches": int(launches),
         "eager_ms_per_step": round(eager_ms_step, 4),
         "roofline": roof,
+        "epoch_roofline": epoch_roof,
         "cpu_baseline": cpu,
         "clocks": clk,
         "kernels": {k: {"launches": v["launches"], "ms_per_launch": round(v["ms"] / v["launches"], 4),
