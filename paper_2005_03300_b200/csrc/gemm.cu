@@ -345,6 +345,7 @@ int pick_mode(const float* base, int64_t s_mn, int64_t s_k) {
 
 void gemm_tf32x3(const GemmDesc& d, cudaStream_t stream) {
   if (d.m <= 0 || d.n <= 0) return;
+  if (gemm_small_try(d, stream)) return;
   if (gemm_tm_enabled() && gemm_tm_try(d, stream)) return;
   if (gemm_tma_enabled() && gemm_tma_try(d, stream)) return;
   Params p{};

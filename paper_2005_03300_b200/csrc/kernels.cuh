@@ -77,6 +77,10 @@ bool gemm_tma_try(const GemmDesc& d, cudaStream_t stream);
 // M-contiguous A with B streamed and split-K (Hᵀ·S); N <= 64.  Returns false
 // (nothing launched) when the shape or layout does not apply.
 bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream);
+// CUDA-core kernels (gemm_small.cu) for narrow x narrow shapes: K, N <= 32
+// with many rows (H·W, S·Wᵀ of 16-wide layers) and M, N <= 32 with a long K
+// (Hᵀ·S); returns false (nothing launched) otherwise.
+bool gemm_small_try(const GemmDesc& d, cudaStream_t stream);
 
 // ---- K3: fused elementwise ----------------------------------------------------
 // log_softmax_rows + nll_tile (dense.cpp:94-136) over full rows of Z; writes

@@ -148,6 +148,13 @@ GEMM_CASES = [
     (130, 200, 70, 0, 0),      # ragged tiles, n > 128
     (5, 3, 2, 1, 1),
     (64, 16, 0, 0, 0),         # k = 0
+    (5000, 16, 16, 0, 0),      # H·W, 16-wide layer
+    (5000, 21, 13, 0, 1),      # S·Wᵀ, ragged
+    (12, 16, 9000, 1, 0),      # Hᵀ·S reduction
+    # >= 1 M rows: the CUDA-core narrow x narrow kernels (gemm_small.cu), unaligned ld
+    (1000003, 16, 16, 0, 0),
+    (1000003, 21, 13, 0, 1),
+    (12, 16, 1000003, 1, 0),
 ]
 
 
@@ -188,6 +195,18 @@ TM_CASES = [
     (3000, 256, 16, 0, 0),     # N > 64: column tiles (Protein's 256 classes)
     (3000, 16, 256, 0, 1),     # S·Wᵀ with K = 256
     (16, 200, 30000, 1, 0),    # Hᵀ·S with N > 64 (ragged last column tile)
+    (40000, 16, 16, 0, 0),     # H·W (16 -> 16)
+    (30000, 24, 16, 0, 1),     # S·Wᵀ (16 -> 24)
+    (16, 16, 70000, 1, 0),     # Hᵀ·S, the 16-wide weight gradient
+    # >= 1 M rows: the CUDA-core narrow x narrow kernels (gemm_small.cu)
+    (1000003, 16, 16, 0, 0),   # H·W (16 -> 16), Amazon / Protein hidden layers
+    (1000003, 24, 16, 0, 1),   # S·Wᵀ (16 -> 24)
+    (1000003, 16, 24, 0, 1),
+    (1000003, 40, 32, 0, 0),   # two column groups per lane, ragged
+    (16, 16, 1000003, 1, 0),   # Hᵀ·S, cp.async-staged reduction
+    (8, 24, 1000003, 1, 0),
+    (32, 32, 1000003, 1, 0),
+    (3, 5, 1000003, 1, 0),     # tiny tile
 ]
 
 
@@ -279,3 +298,29 @@ def test_logsoftmax_nll(cg, orc, torch, cols, c0, c1):
     assert rel(L.cpu().numpy(), logp[:, c0:c1]) < 1e-6
     assert rel(G.cpu().numpy(), g) < 1e-5
     assert abs(loss_dev.item() - loss) / max(1.0, abs(loss)) < 1e-6
+
+
+@pytest.mark.parametrize("acc", [0, 1])
+def test_gemm_small_epilogues(cg, orc, torch, acc):
+    """Fused epilogues on the CUDA-core narrow kernels: relu(Z) side output
+    (EPI_RELU) and ⊙ relu′(aux) (EPI_RELU_PRIME), with and without accumulate."""
+    rng = np.random.default_rng(11 + acc)
+    m, k, n = 1000003, 16, 16
+    a, w = rng.standard_normal((m, k)), rng.standard_normal((k, n))
+    c0 = rng.standard_normal((m, n)) if acc else np.zeros((m, n))
+    z = c0 + orc.gemm(a, w)
+    A, W = padded(torch, a, 16), dev(torch, w.astype(np.float32))
+    Z, H = padded(torch, c0, 16), torch.zeros((m, 16), device="cuda")
+    cg.check(cg.lib.cagnet_gemm_f32(0, 0, m, n, k, A.data_ptr(), 16, W.data_ptr(), n, Z.data_ptr(), 16,
+                                    acc, 1, None, 0, H.data_ptr(), 16, stream(torch)))
+    torch.cuda.synchronize()
+    assert rel(Z.cpu().numpy(), z) < 2e-6
+    assert rel(H.cpu().numpy(), np.maximum(z, 0)) < 2e-6
+    aux = rng.standard_normal((m, n))
+    want = (c0 + orc.gemm(a, w)) * (aux > 0)
+    G = padded(torch, c0, 16)
+    AUX = padded(torch, aux, 16)
+    cg.check(cg.lib.cagnet_gemm_f32(0, 0, m, n, k, A.data_ptr(), 16, W.data_ptr(), n, G.data_ptr(), 16,
+                                    acc, 2, AUX.data_ptr(), 16, None, 0, stream(torch)))
+    torch.cuda.synchronize()
+    assert rel(G.cpu().numpy(), want) < 2e-6
