@@ -16,3 +16,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm
 CAGNET_PROF_DIR=$O/prof python scripts/summarize_ncu.py $R $O/launches.csv /tmp/prof_spmm16.ncu-rep=spmm_f16 /tmp/prof_gemm_tm.ncu-rep > $O/summ.log 2>&1
 for r in /tmp/prof_*.ncu-rep; do ncu -i $r --page raw --csv > $O/prof/$(basename $r .ncu-rep)_raw.csv 2>/dev/null; done
 ls -la /tmp/*.ncu-rep >> $O/summ.log
+( time timeout 900 python bench.py --impl reference > $O/bench_ref.log 2>&1 ) 2> $O/bench_ref_time.txt
