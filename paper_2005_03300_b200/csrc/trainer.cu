@@ -628,7 +628,9 @@ void Trainer::epoch() {
     }
     cudaGraph_t g = nullptr;
     CG_CUDA(cudaStreamEndCapture(cs_, &g));
-    CG_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
+    // Per-node priorities: kernels captured from the high-priority comm stream
+    // (NCCL, peer pushes) keep their priority inside the replayed graph.
+    CG_CUDA(cudaGraphInstantiate(&graph_exec_, g, cudaGraphInstantiateFlagUseNodePriority));
     CG_CUDA(cudaGraphDestroy(g));
     comm_->snapshot(ledger_after_);  // the capture metered this epoch once
     graph_kernels_ = launch_counter().load() - k0;
