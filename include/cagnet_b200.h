@@ -255,7 +255,8 @@ CAGNET_API int cagnet_trainer_set_timing(cagnet_trainer_t t, int on);
  * "timing" (per-launch CUDA-event profile), "fuse" (SpMM row epilogues: 0/1/2),
  * "graph" (CUDA-graph epochs), "resident_sparse" (2D/3D tiles kept in HBM),
  * "p2p" (1D stage panels through NVLink peer memory), "overlap" (1D peer-memory
- * stages: own vertex block SpMM while the pushes fly).  Set before distribute()
+ * stages: own vertex block SpMM while the pushes fly), "pipeline" (1D peer-memory
+ * stages with >= 32 MB slots: per-destination pushes, per-block SpMMs as slots land).  Set before distribute()
  * for resident_sparse / p2p / overlap. */
 CAGNET_API int cagnet_trainer_set_option(cagnet_trainer_t t, const char* name, int64_t value);
 /* Per-launch CUDA-event profile, aggregated by kernel name (e.g. "spmm_f602"):

@@ -75,6 +75,11 @@ class Strategy:
     # second pass costs more SpMM time (Reddit P=4: 0.074 + 0.128 ms vs
     # 0.161 ms in one pass) than the ~25 us push it hides.
     overlap: bool = False
+    # 1D peer-memory stages whose per-peer slot is >= 32 MB (Amazon / Protein):
+    # per-destination pushes, each peer's column block SpMM'd as its slot lands.
+    # Off by default: P SpMM passes cost more than the transfer they hide
+    # (Amazon P = 4: 4 x 0.55 ms vs 1.34 ms in one pass).
+    pipeline: bool = False
 
     @property
     def kind_id(self) -> int:
@@ -368,6 +373,7 @@ class Trainer:
                                             int(strat.resident_sparse)))
         check(lib.cagnet_trainer_set_option(self.h, b"p2p", int(strat.p2p)))
         check(lib.cagnet_trainer_set_option(self.h, b"overlap", int(strat.overlap)))
+        check(lib.cagnet_trainer_set_option(self.h, b"pipeline", int(strat.pipeline)))
 
     # lifecycle -------------------------------------------------------------
     def distribute(self):

@@ -647,6 +647,8 @@ int cagnet_trainer_set_option(cagnet_trainer_t t, const char* name, int64_t valu
       t->t->set_p2p(value != 0);
     else if (n == "overlap")
       t->t->set_overlap(value != 0);
+    else if (n == "pipeline")
+      t->t->set_pipeline(value != 0);
     else if (n == "resident_sparse")
       t->t->set_resident_sparse(value != 0);
     else if (n == "graph")

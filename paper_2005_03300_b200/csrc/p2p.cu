@@ -79,6 +79,42 @@ __global__ void publish_kernel(float* const* bufs, uint64_t* const* flags, int r
   }
 }
 
+// One destination of a pipelined stage: the last CTA raises ready[rank] on q
+// (and, for the stage's last destination, advances the publish count).
+__global__ void publish_one_kernel(float* const* bufs, uint64_t* const* flags, int rank, int P, int q,
+                                   bool last, const float* __restrict__ src, int64_t ld_src, uint32_t rows,
+                                   uint32_t c4, int64_t slot_floats, int64_t ld_dst) {
+  const Flags F{P};
+  uint64_t* my = flags[rank];
+  const uint64_t s = *F.pub_ctr(my) + 1;
+  const uint32_t total = rows * c4;
+  float* dst = bufs[q] + rank * slot_floats;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const uint32_t r = e / c4, c = e - r * c4;
+    *reinterpret_cast<float4*>(dst + r * ld_dst + 4 * c) = *reinterpret_cast<const float4*>(src + r * ld_src + 4 * c);
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long prev =
+        atomicAdd(reinterpret_cast<unsigned long long*>(F.arrivals(my)), 1ull);
+    if (prev == gridDim.x - 1) {
+      *F.arrivals(my) = 0;
+      if (last) *F.pub_ctr(my) = s;
+      __threadfence_system();
+      st_release_sys(F.ready(flags[q]) + rank, s);
+    }
+  }
+}
+
+__global__ void wait_slot_kernel(uint64_t* const* flags, int rank, int P, int q) {
+  const Flags F{P};
+  uint64_t* my = flags[rank];
+  const uint64_t s = *F.wait_ctr(my) + 1;
+  if (threadIdx.x == 0) spin_until_geq(F.ready(my) + q, s);
+  __threadfence_system();
+}
+
 __global__ void wait_ready_kernel(uint64_t* const* flags, int rank, int P) {
   const Flags F{P};
   uint64_t* my = flags[rank];
@@ -238,6 +274,29 @@ void PeerPanels::publish(int b, const float* src, int64_t ld_src, int64_t rows, 
   publish_kernel<<<blocks, 256, 0, s>>>(d_bufs_[b].get(), d_flags_.get(), rank_, ranks_, skip_self, src,
                                         ld_src, static_cast<uint32_t>(rows), static_cast<uint32_t>(c4),
                                         slot_floats, ld_dst);
+  CG_LAUNCH_CHECK();
+}
+
+void PeerPanels::publish_to(int b, int dest, const float* src, int64_t ld_src, int64_t rows, int64_t cols,
+                            int64_t slot_floats, int64_t ld_dst, bool last, cudaStream_t s) {
+  require(ld_src % 4 == 0 && ld_dst % 4 == 0 && slot_floats % 4 == 0 &&
+              reinterpret_cast<uintptr_t>(src) % 16 == 0,
+          "PeerPanels::publish_to: rows must be 16 B aligned");
+  require(dest >= 0 && dest < ranks_ && dest != rank_, "PeerPanels::publish_to: bad destination");
+  const int64_t c4 = (cols + 3) / 4;
+  require(c4 * 4 <= ld_src && c4 * 4 <= ld_dst, "PeerPanels::publish_to: padded width exceeds ld");
+  const int64_t total = rows * c4;
+  int blocks = static_cast<int>(ceil_div64(total > 0 ? total : 1, 256));
+  const int cap = 2 * num_sms(device_);
+  if (blocks > cap) blocks = cap;
+  publish_one_kernel<<<blocks, 256, 0, s>>>(d_bufs_[b].get(), d_flags_.get(), rank_, ranks_, dest, last, src,
+                                            ld_src, static_cast<uint32_t>(rows), static_cast<uint32_t>(c4),
+                                            slot_floats, ld_dst);
+  CG_LAUNCH_CHECK();
+}
+
+void PeerPanels::wait_slot(int q, cudaStream_t s) {
+  wait_slot_kernel<<<1, 32, 0, s>>>(d_flags_.get(), rank_, ranks_, q);
   CG_LAUNCH_CHECK();
 }
 

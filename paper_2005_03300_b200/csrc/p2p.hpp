@@ -62,6 +62,15 @@ class PeerPanels {
   // local stage counter.
   void wait_ready(cudaStream_t s);
 
+  // Pipelined form of publish(): one destination per call, in the caller's
+  // order, each raising that destination's ready flag when its copy is done;
+  // `last` closes the stage (advances the publish count).  Every stage must
+  // still end with wait_ready() on the SpMM stream.
+  void publish_to(int b, int dest, const float* src, int64_t ld_src, int64_t rows, int64_t cols,
+                  int64_t slot_floats, int64_t ld_dst, bool last, cudaStream_t s);
+  // Waits until peer q published the current stage (no counter change).
+  void wait_slot(int q, cudaStream_t s);
+
  private:
   int rank_ = 0, ranks_ = 1, device_ = 0;
   bool same_process_ = false;

@@ -6,6 +6,7 @@
 // a row all-reduce.  Broadcast panels are double-buffered on the comm stream
 // so stage q+1's NCCL broadcast overlaps stage q's SpMM.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "p2p.hpp"
@@ -256,6 +257,36 @@ class TrainerRows final : public Trainer {
       // into adjacent slots and one SpMM consumes them all.
       const DeviceCsr& blk = &parts == &a_parts_ ? a_chunk_ : at_chunk_;
       Mat g{gbuf_.m.p, c_hi_ - c_lo_, mine.cols, mine.ld};
+      if (one_d() && p2p_ok_ && pipelined(parts, mine) && !(epi && epi->W)) {
+        // Bandwidth-heavy exchange (Amazon / Protein scale): push the panel to
+        // the peers one destination after another (every rank starts with
+        // rank + 1), SpMM the own vertex block from the local panel meanwhile,
+        // then each peer's column block as its slot lands (rank - 1 first),
+        // accumulating; the fused row epilogue rides on the last block.
+        const int P = blocks();
+        const int64_t step = ceil_div64(data_.n, P);
+        const int b = static_cast<int>(p2p_stage_++ & 1);
+        float* base = p2p_.buffer(b);
+        std::vector<uint64_t> words;
+        for (int q = 0; q < P; ++q)
+          words.push_back(static_cast<uint64_t>(block_range(data_.n, P, q).size() * mine.cols));
+        comm_->meter_bcast_all(grp, Category::DBcast, words);
+        ms_after_cs();
+        for (int d = 1; d < P; ++d)
+          p2p_.publish_to(b, (rank_ + d) % P, mine.p, mine.ld, mine.rows, mine.cols, step * mine.ld, mine.ld,
+                          d + 1 == P, ms_);
+        spmm(parts[static_cast<size_t>(rank_)], mine, out, false, nullptr);
+        for (int d = 1; d < P; ++d) {
+          const int q = (rank_ - d + P) % P;
+          const DeviceCsr& part = parts[static_cast<size_t>(q)];
+          p2p_.wait_slot(q, cs_);
+          const Mat slot{base + q * step * mine.ld, part.n_cols, mine.cols, mine.ld};
+          spmm(part, slot, out, true, d + 1 == P ? epi : nullptr);
+        }
+        p2p_.wait_ready(cs_);
+        cs_after_ms();  // pushes done before anything overwrites `mine`
+        return;
+      }
       if (one_d() && p2p_ok_ && overlap_ok_ && spmm_single_pass(blk, Mat{nullptr, c_hi_ - c_lo_, mine.cols, mine.ld}) &&
           !(epi && epi->W)) {
         // Peer-memory stage with overlap: the pushes to the peers run on the
@@ -367,6 +398,20 @@ class TrainerRows final : public Trainer {
     comm_->all_reduce(grid_.row_group(rank_), m.p, static_cast<size_t>(m.rows * m.ld), ncclFloat32,
                       Category::Reduce, words(m), ms_);
     cs_after_ms();
+  }
+
+  // Pipelined peer-memory stages pay one SpMM pass per column block, so they
+  // are used only when a peer's slot is large enough for the transfer to
+  // matter (>= 32 MB: Amazon / Protein, not Reddit) and every per-block SpMM
+  // is a single pass.
+  bool pipelined(const std::vector<DeviceCsr>& parts, const Mat& mine) const {
+    if (!pipeline_enabled_ || blocks() < 2) return false;
+    const double slot = static_cast<double>(ceil_div64(data_.n, blocks())) * mine.ld * 4.0;
+    const char* e = std::getenv("CAGNET_PIPELINE_MIN_MB");  // tests lower it
+    if (slot < (e ? std::atof(e) : 32.0) * 1048576.0) return false;
+    for (const DeviceCsr& p : parts)
+      if (!spmm_single_pass(p, Mat{nullptr, p.n_cols, mine.cols, mine.ld})) return false;
+    return true;
   }
 
   bool saved_t_ok(int l) const {

@@ -156,6 +156,13 @@ class Trainer {
   // panel while the pushes to the peers are in flight, then the remaining
   // columns (set before distribute(); off = one SpMM after the exchange).
   void set_overlap(bool on) { overlap_enabled_ = on; }
+  // 1D peer-memory stages with large slots (>= 32 MB per peer): per-destination
+  // pushes and per-block SpMMs as slots land (off by default: the per-block
+  // SpMM passes cost more than the transfer they hide).
+  void set_pipeline(bool on) {
+    if (on != pipeline_enabled_) reset_graph();
+    pipeline_enabled_ = on;
+  }
   void reset_profile() {
     collect_profile();
     profile_.clear();
@@ -221,6 +228,7 @@ class Trainer {
   bool resident_sparse_ = true;
   bool p2p_enabled_ = true;
   bool overlap_enabled_ = false;
+  bool pipeline_enabled_ = false;
   std::vector<ProfRec> recs_;
   size_t recs_used_ = 0;
   std::vector<ProfEntry> profile_;

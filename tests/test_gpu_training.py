@@ -197,13 +197,17 @@ def test_distributed_reassociated(cg, orc, need_gpus, kind, P, repl, dims):
 
 @pytest.mark.multigpu
 @pytest.mark.parametrize("P", [2, 4])
-@pytest.mark.parametrize("p2p,overlap", [(True, True), (True, False), (False, False)])
-def test_1d_exchange_paths(cg, orc, need_gpus, P, p2p, overlap):
+@pytest.mark.parametrize("p2p,overlap,pipeline", [(True, True, False), (True, False, False),
+                                                  (True, False, True), (False, False, False)])
+def test_1d_exchange_paths(cg, orc, need_gpus, monkeypatch, P, p2p, overlap, pipeline):
     """1D stage exchanges: NVLink peer-memory pushes with the own-block SpMM
-    overlapped, peer memory without overlap, and the NCCL all-gather — same
-    numbers as the serial oracle over graph-replayed epochs (the flag protocol
-    runs inside the replays)."""
+    overlapped, peer memory in one SpMM after the exchange, the pipelined form
+    (per-destination pushes, per-block SpMMs as slots land; forced here by a
+    zero slot threshold), and the NCCL all-gather — same numbers as the serial
+    oracle over graph-replayed epochs (the flag protocol runs inside the
+    replays)."""
     need_gpus(P)
+    monkeypatch.setenv("CAGNET_PIPELINE_MIN_MB", "0" if pipeline else "1e9")
     dims = [24, 8, 8, 6]
     model = cg.init_glorot(dims, 5, 0.5)
     strat = cg.Strategy("1d", P, 1, reassociate=True, p2p=p2p, overlap=overlap)
