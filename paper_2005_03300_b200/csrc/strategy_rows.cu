@@ -215,9 +215,20 @@ class TrainerRows final : public Trainer {
         gemm_swt(s, l - 1, 0, 0, g_[static_cast<size_t>(l - 2)].m, false, kern::EPI_RELU_PRIME, &zp);
       }
     }
+    // Peer-memory buffers alternate between consecutive exchanges, and the
+    // captured epoch graph repeats its buffer sequence: an odd number of
+    // exchanges per epoch would give the last exchange of one epoch and the
+    // first of the next the same buffer.  A flag-only exchange evens it out.
+    if (p2p_ok_ && (epoch_exchanges_ & 1)) {
+      const int b = next_p2p_buffer();
+      p2p_.publish(b, p2p_.buffer(b), 4, 0, 0, 4, 4, /*skip_self=*/true, cs_);
+      p2p_.wait_ready(cs_);
+    }
     cs_after_ms();  // the Y all-reduces
     sgd_all();
   }
+
+  void begin_epoch() override { epoch_exchanges_ = 0; }
 
  private:
   bool one_d() const { return grid_.kind() == GridKind::Row1D; }
@@ -265,7 +276,7 @@ class TrainerRows final : public Trainer {
         // accumulating; the fused row epilogue rides on the last block.
         const int P = blocks();
         const int64_t step = ceil_div64(data_.n, P);
-        const int b = static_cast<int>(p2p_stage_++ & 1);
+        const int b = next_p2p_buffer();
         float* base = p2p_.buffer(b);
         std::vector<uint64_t> words;
         for (int q = 0; q < P; ++q)
@@ -295,7 +306,7 @@ class TrainerRows final : public Trainer {
         // then the remaining columns from the filled buffer, accumulating,
         // with the fused row epilogue on that last pass.
         const int64_t step = ceil_div64(data_.n, blocks());
-        const int b = static_cast<int>(p2p_stage_++ & 1);
+        const int b = next_p2p_buffer();
         Mat pg{p2p_.buffer(b), c_hi_ - c_lo_, mine.cols, mine.ld};
         std::vector<uint64_t> words;
         for (int q = 0; q < blocks(); ++q)
@@ -326,7 +337,7 @@ class TrainerRows final : public Trainer {
         // NVLink peer-memory exchange: push this rank's panel into every
         // rank's buffer, wait for the peers' panels, SpMM, release.
         const int64_t step = ceil_div64(data_.n, blocks());
-        const int b = static_cast<int>(p2p_stage_++ & 1);
+        const int b = next_p2p_buffer();
         Mat pg{p2p_.buffer(b), c_hi_ - c_lo_, mine.cols, mine.ld};
         std::vector<uint64_t> words;
         for (int q = 0; q < blocks(); ++q)
@@ -432,6 +443,11 @@ class TrainerRows final : public Trainer {
   BlockRange own_{0, 0};          // this rank's vertex block (1D)
   RotatedCsr a_rot_, at_rot_;     // chunk CSRs with the own block first per row
   uint64_t p2p_stage_ = 0;        // host parity of the double-buffered panels
+  int epoch_exchanges_ = 0;       // peer-memory exchanges in the current epoch
+  int next_p2p_buffer() {
+    ++epoch_exchanges_;
+    return static_cast<int>(p2p_stage_++ & 1);
+  }
   std::vector<OwnedMat> saved_t_;  // T = Aᵀ H of widening layers (narrow-first backward)
   std::vector<bool> saved_valid_;
 };

@@ -221,6 +221,25 @@ def test_1d_exchange_paths(cg, orc, need_gpus, monkeypatch, P, p2p, overlap, pip
 
 
 @pytest.mark.multigpu
+@pytest.mark.parametrize("P", [2, 4])
+def test_1d_odd_exchange_count(cg, orc, need_gpus, P):
+    """A widening first layer skips the last backward SpMM, leaving an odd
+    number of peer-memory exchanges per epoch; the trainer evens it out with a
+    flag-only exchange so the replayed epoch graph never reuses the buffer of
+    the exchange before it (many replays, result still matches the oracle)."""
+    need_gpus(P)
+    dims = [8, 16, 4]
+    model = cg.init_glorot(dims, 5, 0.5)
+    out = cg.run_distributed(lambda dev: cg.generate_dataset(400, 12.0, 8, 4, 2, 3, 4, device=dev),
+                             model, cg.Strategy("1d", P, 1, reassociate=True), 12)
+    od = orc.generate_dataset(400, 12.0, 8, 4, 2, 3, 4)
+    losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.5, 12)
+    res = dict(losses=out.losses, h_final=out.h_final, y=out.y_final, g=out.g_final,
+               w=out.model.weights)
+    assert max_rel_error(res, losses, h, y, g, w) < TOL
+
+
+@pytest.mark.multigpu
 @pytest.mark.parametrize("kind,P", [("2d", 4), ("3d", 8)])
 def test_resident_sparse_tiles(cg, need_gpus, kind, P):
     """SUMMA with the sparse tiles kept resident after distribute(): the same
