@@ -36,15 +36,21 @@ constexpr int kSpmmEpiMaxFo = 64;
 // with the nonzeros of each row folded in ascending order (the reference's
 // accumulation order), one fp32 FMA per term.
 // nnz (optional, -1 = unknown) sizes the row teams of the narrow-row kernel.
+// colval (optional): the same nonzeros interleaved as int2 {col, float bits}
+// (interleave_colval), read by the narrow-row kernel in one load per nonzero.
 void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
               const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
-              cudaStream_t stream, int64_t nnz = -1, const SpmmEpi* epi = nullptr);
+              cudaStream_t stream, int64_t nnz = -1, const SpmmEpi* epi = nullptr,
+              const int2* colval = nullptr);
 
 // Same, with row i's nonzeros given as [seg_begin[i], seg_end[i]).
 void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_end,
                    const int32_t* col_idx, const float* vals, const float* H, int64_t ldh, int f,
                    float* T, int64_t ldt, bool accumulate, cudaStream_t stream, int64_t nnz = -1,
-                   const SpmmEpi* epi = nullptr);
+                   const SpmmEpi* epi = nullptr, const int2* colval = nullptr);
+// out[k] = {col_idx[k], bits of vals[k]} for the interleaved nonzero stream.
+void interleave_colval(int64_t nnz, const int32_t* col_idx, const float* vals, int2* out,
+                       cudaStream_t stream);
 // split[b * rows + r] (b = 0..nb) = first nonzero of row r in column block b
 // of the ceiling-rule split of n_cols into nb blocks; split[nb * rows + r] = row end.
 void column_splits(int64_t rows, int64_t n_cols, int nb, const int64_t* row_ptr,

@@ -99,6 +99,9 @@ struct SpmmArgs {
   int64_t ldt;
   double mean_row_nnz;  // host-side hint for the row-team shape
   SpmmEpi epi;          // fused row epilogue (EPI kernels only)
+  // Optional interleaved copy of (col_idx, vals) as int2 {col, float bits}:
+  // one 8 B load per nonzero instead of two 4 B loads (narrow-row kernel).
+  const int2* colval = nullptr;
 };
 
 // VEC = 4: 16-byte vectors (requires 16 B aligned rows, ld a multiple of 4); VEC = 1: scalars.
@@ -369,7 +372,11 @@ __device__ __forceinline__ void spmm_row_epilogue(const SpmmArgs& a, int64_t row
 // row's nonzeros (sub-team q takes q, q+QPR, ...), so every lane streams
 // independent gathers with no shuffles in the loop (U in flight); the QPR
 // partial sums are folded with xor shuffles at the end (deterministic order).
-template <int LV, int QPR, int U, bool ACC, bool TAIL, int NT = kThreads, int HINT = 0,
+// CV: the nonzeros come from the interleaved (col, value) stream a.colval —
+// per warp instruction the 8 sub-teams then read 8 consecutive 8 B entries (one
+// L1 wavefront) instead of 8 columns and 8 values (two), which matters because
+// the kernel is bound by L1 LSU wavefronts (one per gathered row).
+template <int LV, int QPR, int U, bool ACC, bool CV, int NT = kThreads, int HINT = 0,
           bool FULLV = false, bool EPI = false>
 __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArgs a) {
   constexpr int TEAM = LV * QPR;
@@ -389,15 +396,14 @@ __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArg
   const char* __restrict__ hbase = reinterpret_cast<const char*>(a.H) + vec * 16;
   const uint32_t ldh_bytes = static_cast<uint32_t>(a.ldh * 4);
 
-  const int32_t* __restrict__ cp = a.col_idx;
-  const float* __restrict__ vp = a.vals;
-  const int32_t* ce = cp;
+  int64_t nz_b = 0, nz_e = 0;
   if (row < a.n_rows) {
-    const int64_t b = a.seg_begin[row];
-    ce = cp + a.seg_end[row];
-    cp += b + q;
-    vp += b + q;
+    nz_b = a.seg_begin[row];
+    nz_e = a.seg_end[row];
   }
+  const int32_t* __restrict__ cp = a.col_idx + nz_b + q;
+  const float* __restrict__ vp = a.vals + nz_b + q;
+  const int32_t* ce = a.col_idx + nz_e;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   auto gather = [&](int c) -> float4 {
     if (!vec_ok) return make_float4(0.f, 0.f, 0.f, 0.f);
@@ -410,19 +416,40 @@ __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArg
   // gathered H rows out of L2.
   auto ld_c = [&](const int32_t* p) { return HINT ? __ldcs(p) : __ldg(p); };
   auto ld_v = [&](const float* p) { return HINT ? __ldcs(p) : __ldg(p); };
-  for (; cp + (U - 1) * QPR < ce; cp += U * QPR, vp += U * QPR) {
-    float4 h[U];
-    float w[U];
+  if constexpr (CV) {
+    const int2* __restrict__ p = a.colval + nz_b + q;
+    const int2* pe = a.colval + nz_e;
+    for (; p + (U - 1) * QPR < pe; p += U * QPR) {
+      float4 h[U];
+      float w[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int c = ld_c(cp + u * QPR);
-      w[u] = ld_v(vp + u * QPR);
-      h[u] = gather(c);
+      for (int u = 0; u < U; ++u) {
+        const int2 x = __ldg(p + u * QPR);
+        w[u] = __int_as_float(x.y);
+        h[u] = gather(x.x);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) fma_vec(acc, w[u], h[u]);
     }
+    for (; p < pe; p += QPR) {
+      const int2 x = __ldg(p);
+      fma_vec(acc, __int_as_float(x.y), gather(x.x));
+    }
+  } else {
+    for (; cp + (U - 1) * QPR < ce; cp += U * QPR, vp += U * QPR) {
+      float4 h[U];
+      float w[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) fma_vec(acc, w[u], h[u]);
+      for (int u = 0; u < U; ++u) {
+        const int c = ld_c(cp + u * QPR);
+        w[u] = ld_v(vp + u * QPR);
+        h[u] = gather(c);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) fma_vec(acc, w[u], h[u]);
+    }
+    for (; cp < ce; cp += QPR, vp += QPR) fma_vec(acc, ld_v(vp), gather(ld_c(cp)));
   }
-  for (; cp < ce; cp += QPR, vp += QPR) fma_vec(acc, ld_v(vp), gather(ld_c(cp)));
 #pragma unroll
   for (int o = LV; o < TEAM; o <<= 1) {
     acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
@@ -455,40 +482,48 @@ __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArg
   }
 }
 
+template <int LV, int QPR, int U, int NT, int HINT, bool CV>
+void launch_nzpar_cv(const SpmmArgs& a, bool acc, bool epi, unsigned g, bool full, cudaStream_t s) {
+  if (epi && acc) {
+    if (full)
+      spmm_nzpar_kernel<LV, QPR, U, true, CV, NT, 0, true, true><<<g, NT, 0, s>>>(a);
+    else
+      spmm_nzpar_kernel<LV, QPR, U, true, CV, NT, 0, false, true><<<g, NT, 0, s>>>(a);
+  } else if (epi) {
+    if (full)
+      spmm_nzpar_kernel<LV, QPR, U, false, CV, NT, 0, true, true><<<g, NT, 0, s>>>(a);
+    else
+      spmm_nzpar_kernel<LV, QPR, U, false, CV, NT, 0, false, true><<<g, NT, 0, s>>>(a);
+  } else if (acc) {
+    if (full)
+      spmm_nzpar_kernel<LV, QPR, U, true, CV, NT, HINT, true><<<g, NT, 0, s>>>(a);
+    else
+      spmm_nzpar_kernel<LV, QPR, U, true, CV, NT, HINT><<<g, NT, 0, s>>>(a);
+  } else {
+    if (full)
+      spmm_nzpar_kernel<LV, QPR, U, false, CV, NT, HINT, true><<<g, NT, 0, s>>>(a);
+    else
+      spmm_nzpar_kernel<LV, QPR, U, false, CV, NT, HINT><<<g, NT, 0, s>>>(a);
+  }
+}
+
 template <int LV, int QPR, int U, int NT, int HINT>
 void launch_nzpar_v(const SpmmArgs& a, bool acc, bool epi, cudaStream_t s) {
   constexpr int rows_per_block = (NT / 32) * (32 / (LV * QPR));
   const unsigned g = static_cast<unsigned>(ceil_div64(a.n_rows, rows_per_block));
   // Full vectors: every lane of the LV-wide row team owns a live float4.
   const bool full = (a.f + 3) / 4 == LV;
-  if (epi && acc) {
-    if (full)
-      spmm_nzpar_kernel<LV, QPR, U, true, false, NT, 0, true, true><<<g, NT, 0, s>>>(a);
-    else
-      spmm_nzpar_kernel<LV, QPR, U, true, false, NT, 0, false, true><<<g, NT, 0, s>>>(a);
-  } else if (epi) {
-    if (full)
-      spmm_nzpar_kernel<LV, QPR, U, false, false, NT, 0, true, true><<<g, NT, 0, s>>>(a);
-    else
-      spmm_nzpar_kernel<LV, QPR, U, false, false, NT, 0, false, true><<<g, NT, 0, s>>>(a);
-  } else if (acc) {
-    if (full)
-      spmm_nzpar_kernel<LV, QPR, U, true, false, NT, HINT, true><<<g, NT, 0, s>>>(a);
-    else
-      spmm_nzpar_kernel<LV, QPR, U, true, false, NT, HINT><<<g, NT, 0, s>>>(a);
-  } else {
-    if (full)
-      spmm_nzpar_kernel<LV, QPR, U, false, false, NT, HINT, true><<<g, NT, 0, s>>>(a);
-    else
-      spmm_nzpar_kernel<LV, QPR, U, false, false, NT, HINT><<<g, NT, 0, s>>>(a);
-  }
+  if (a.colval)
+    launch_nzpar_cv<LV, QPR, U, NT, HINT, true>(a, acc, epi, g, full, s);
+  else
+    launch_nzpar_cv<LV, QPR, U, NT, HINT, false>(a, acc, epi, g, full, s);
   CG_LAUNCH_CHECK();
 }
 
 // Tuning knob for experiments (CAGNET_SPMM_TUNE=<variant>); 0 = the default
 // (128-thread CTAs, U = 4 gathers in flight per lane, no cache hints — the
 // fastest on the Reddit-shaped graph: 0.548 ms vs 0.565 ms with L2 evict hints
-// and 0.561 ms with 256-thread CTAs at f = 16).
+// (variant 2), 0.561 ms with 256-thread CTAs and no gain from U = 8 at f = 16).
 int spmm_tune() {
   static const int v = [] {
     const char* e = getenv("CAGNET_SPMM_TUNE");
@@ -501,9 +536,7 @@ template <int LV, int QPR>
 void launch_nzpar(const SpmmArgs& a, bool acc, bool epi, cudaStream_t s) {
   if (epi) return launch_nzpar_v<LV, QPR, 4, 128, 0>(a, acc, true, s);
   switch (spmm_tune()) {
-    case 1: return launch_nzpar_v<LV, QPR, 4, kThreads, 0>(a, acc, false, s);
     case 2: return launch_nzpar_v<LV, QPR, 4, 128, 1>(a, acc, false, s);
-    case 3: return launch_nzpar_v<LV, QPR, 8, 128, 0>(a, acc, false, s);
     default: return launch_nzpar_v<LV, QPR, 4, 128, 0>(a, acc, false, s);
   }
 }
@@ -578,7 +611,7 @@ __global__ void column_splits_kernel(int64_t rows, int nb, int64_t step,
 void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_end,
                    const int32_t* col_idx, const float* vals, const float* H, int64_t ldh, int f,
                    float* T, int64_t ldt, bool accumulate, cudaStream_t stream, int64_t nnz,
-                   const SpmmEpi* epi) {
+                   const SpmmEpi* epi, const int2* colval) {
   if (n_rows <= 0 || f <= 0) return;
   const double mean = nnz >= 0 ? static_cast<double>(nnz) / static_cast<double>(n_rows) : 64.0;
   const bool aligned = (ldh % 4 == 0) && (ldt % 4 == 0) &&
@@ -589,7 +622,7 @@ void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_
             "spmm: fused epilogue needs a final f <= 32 SpMM on 16 B-aligned rows");
     require(!accumulate || epi->W == nullptr,
             "spmm: an accumulating fused epilogue cannot change the row width");
-    SpmmArgs a{n_rows, seg_begin, seg_end, col_idx, vals, H, ldh, f, T, ldt, mean, *epi};
+    SpmmArgs a{n_rows, seg_begin, seg_end, col_idx, vals, H, ldh, f, T, ldt, mean, *epi, colval};
     dispatch<4>(a, accumulate, true, stream);
     return;
   }
@@ -597,7 +630,7 @@ void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_
   const int chunk = aligned ? 32 * 8 * 4 : 32 * 8;
   for (int c0 = 0; c0 < f; c0 += chunk) {
     SpmmArgs a{n_rows, seg_begin, seg_end, col_idx, vals, H + c0, ldh, f - c0 < chunk ? f - c0 : chunk,
-               T + c0, ldt, mean, SpmmEpi{}};
+               T + c0, ldt, mean, SpmmEpi{}, colval};
     if (aligned)
       dispatch<4>(a, accumulate, false, stream);
     else
@@ -607,9 +640,26 @@ void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_
 
 void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
               const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
-              cudaStream_t stream, int64_t nnz, const SpmmEpi* epi) {
+              cudaStream_t stream, int64_t nnz, const SpmmEpi* epi, const int2* colval) {
   spmm_segments(n_rows, row_ptr, row_ptr + 1, col_idx, vals, H, ldh, f, T, ldt, accumulate, stream,
-                nnz, epi);
+                nnz, epi, colval);
+}
+
+namespace {
+__global__ void interleave_kernel(int64_t nnz, const int32_t* __restrict__ ci, const float* __restrict__ v,
+                                  int2* __restrict__ out) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[k] = make_int2(ci[k], __float_as_int(v[k]));
+}
+}  // namespace
+
+void interleave_colval(int64_t nnz, const int32_t* col_idx, const float* vals, int2* out, cudaStream_t s) {
+  if (nnz <= 0) return;
+  const int64_t want = ceil_div64(nnz, 256);
+  const unsigned g = static_cast<unsigned>(want < 16LL * 1024 ? want : 16LL * 1024);
+  interleave_kernel<<<g, 256, 0, s>>>(nnz, col_idx, vals, out);
+  CG_LAUNCH_CHECK();
 }
 
 void column_splits(int64_t rows, int64_t n_cols, int nb, const int64_t* row_ptr,

@@ -496,7 +496,7 @@ class TrainerSumma final : public Trainer {
       std::vector<Mat> pieces = dense_panel(col, xroot, mine, xrows, mine.cols, chs, b);
       for (size_t c = 0; c < chs.size(); ++c) {
         Mat dst{out.p + chs[c].begin, out.rows, chs[c].size(), out.ld};
-        spmm_raw(arows, annz, rp, ci, vv, pieces[c], dst, q > 0);
+        spmm_raw(arows, annz, rp, ci, vv, pieces[c], dst, q > 0, nullptr, rp != spanel_[b].row_ptr.get());
       }
       release_buffer(b);
     }

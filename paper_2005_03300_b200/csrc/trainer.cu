@@ -274,7 +274,25 @@ Trainer::~Trainer() {
   if (ms_) cudaStreamDestroy(ms_);
 }
 
+const int2* Trainer::colval(const int32_t* ci, const float* v, int64_t nnz) {
+  static const bool on = [] {
+    const char* e = std::getenv("CAGNET_SPMM_CV");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || nnz <= 0 || ci == nullptr || v == nullptr) return nullptr;
+  const auto key = std::make_pair(static_cast<const void*>(ci), static_cast<const void*>(v));
+  auto it = colval_.find(key);
+  if (it != colval_.end()) return it->second.get();
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  CG_CUDA(cudaStreamIsCapturing(cs_, &st));
+  if (st != cudaStreamCaptureStatusNone) return nullptr;  // no allocation inside a capture
+  DevBuf<int2> buf(static_cast<size_t>(nnz));
+  kern::interleave_colval(nnz, ci, v, buf.get(), cs_);
+  return colval_.emplace(key, std::move(buf)).first->second.get();
+}
+
 void Trainer::init_tiles() {
+  colval_.clear();
   const int L = num_layers();
   const BlockRange rows = tile_rows(rank_);
   h_.clear();
@@ -367,12 +385,18 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const ke
     }
     it = colblocks_.emplace(key, std::move(blocks)).first;
   }
+  std::vector<const int2*> cvs;
+  for (int b = 0; b < nb; ++b) {
+    const DeviceCsr& blk = it->second[static_cast<size_t>(b)];
+    cvs.push_back(colval(blk.col_idx.get(), blk.vals.get(), blk.nnz));
+  }
   const int slot = prof_begin();
   for (int b = 0; b < nb; ++b) {
     const DeviceCsr& blk = it->second[static_cast<size_t>(b)];
     const BlockRange cr = block_range(a.n_cols, nb, b);
     kern::spmm_csr(blk.n_rows, blk.row_ptr.get(), blk.col_idx.get(), blk.vals.get(), h.p + cr.begin * h.ld,
-                   h.ld, static_cast<int>(h.cols), out.p, out.ld, acc || b > 0, cs_, blk.nnz);
+                   h.ld, static_cast<int>(h.cols), out.p, out.ld, acc || b > 0, cs_, blk.nnz, nullptr,
+                   cvs[static_cast<size_t>(b)]);
   }
   if (slot >= 0) {
     const double f = static_cast<double>(h.cols), r = static_cast<double>(a.n_rows);
@@ -390,13 +414,16 @@ double Trainer::l2_panel_bytes() {
 }
 
 void Trainer::spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32_t* ci,
-                       const float* v, const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi) {
+                       const float* v, const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi,
+                       bool stable) {
   const int64_t width = epi && epi->W ? epi->fo : h.cols;
   if (out.rows != rows || out.cols != width)
     throw std::invalid_argument("spmm: accumulator shape mismatch");
+  // nnz here is the length of the (0-based) arrays, so the interleaved copy covers every row.
+  const int2* cv = stable ? colval(ci, v, nnz) : nullptr;
   const int slot = prof_begin();
   kern::spmm_csr(rows, rp, ci, v, h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld, acc, cs_, nnz,
-                 epi);
+                 epi, cv);
   if (slot >= 0) {
     // B = 8(r+1) + 8 nnz + 4 f c + 4 f r (1 + acc); F = 2 nnz f;
     // plus the fused epilogue's extra row traffic (raw copy, relu′ mask, relu).

@@ -194,8 +194,10 @@ class Trainer {
   // on h.rows).  `kind` labels the profile entry.
   void spmm_seg(int64_t rows, int64_t nnz, const int64_t* seg_b, const int64_t* seg_e, const int32_t* ci,
                 const float* v, const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi, const char* kind);
+  // stable = false: the CSR arrays are a scratch buffer whose contents change
+  // between calls (no interleaved copy is cached for them).
   void spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32_t* ci, const float* v,
-                const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi = nullptr);
+                const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi = nullptr, bool stable = true);
   // True when spmm(a, h, ...) is a single kernel pass (no L2 column blocking).
   bool spmm_single_pass(const DeviceCsr& a, const Mat& h) const;
   int spmm_passes(const DeviceCsr& a, const Mat& h) const;
@@ -256,6 +258,11 @@ class Trainer {
   // Column blocks of the local CSR parts for L2-blocked SpMM passes, keyed by
   // (row_ptr, blocks).
   std::map<std::pair<const void*, int>, std::vector<DeviceCsr>> colblocks_;
+  // Interleaved (col, value) copies of the CSR arrays the SpMMs stream, keyed
+  // by the arrays they copy; built on first use outside graph capture
+  // (CAGNET_SPMM_CV=0 disables them).
+  std::map<std::pair<const void*, const void*>, DevBuf<int2>> colval_;
+  const int2* colval(const int32_t* ci, const float* v, int64_t nnz);
   static double l2_panel_bytes();
   DevBuf<double> losses_dev_;
   DevBuf<int> loss_slot_;  // device-side write index into losses_dev_
