@@ -28,6 +28,14 @@ struct SpmmEpi {
   int64_t relu_ld = 0;
   float* raw_out = nullptr;
   int64_t raw_ld = 0;
+  // Direct peer push (no-W epilogues): the final row value — relu(Z) when
+  // push_relu, else the stored (masked) row — also goes to row
+  // push_off + row * push_ld of each of the push_n buffers in push_bufs (a
+  // device array: the next exchange's panel slot of this rank on every rank).
+  float* const* push_bufs = nullptr;
+  int push_n = 0;
+  int64_t push_off = 0, push_ld = 0;
+  bool push_relu = false;
 };
 constexpr int kSpmmEpiMaxF = 32;
 constexpr int kSpmmEpiMaxFo = 64;

@@ -126,9 +126,11 @@ __global__ void wait_ready_kernel(uint64_t* const* flags, int rank, int P) {
   if (threadIdx.x == 0) *F.wait_ctr(my) = s;
 }
 
+constexpr int kAllocs = PeerPanels::kBuffers + 1;  // panel buffers + flags
+
 struct PeerInfo {
-  cudaIpcMemHandle_t h[3];
-  uint64_t ptr[3];
+  cudaIpcMemHandle_t h[kAllocs];
+  uint64_t ptr[kAllocs];
   uint64_t pid;
   int32_t device;
   int32_t ok;
@@ -153,17 +155,19 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
   if (ranks <= 1) return false;
   const int P = ranks;
   // Allocate first so every rank can advertise handles; freed again on fallback.
-  CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&base_[0]), bytes));
-  CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&base_[1]), bytes));
+  for (int b = 0; b < kBuffers; ++b) {
+    CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&base_[b]), bytes));
+    CG_CUDA(cudaMemset(base_[b], 0, bytes));
+  }
   CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&flags_), (P + 3) * sizeof(uint64_t)));
   CG_CUDA(cudaMemset(flags_, 0, (P + 3) * sizeof(uint64_t)));
-  CG_CUDA(cudaMemset(base_[0], 0, bytes));
-  CG_CUDA(cudaMemset(base_[1], 0, bytes));
 
   PeerInfo mine{};
-  void* ptrs[3] = {base_[0], base_[1], flags_};
+  void* ptrs[kAllocs];
+  for (int b = 0; b < kBuffers; ++b) ptrs[b] = base_[b];
+  ptrs[kBuffers] = flags_;
   mine.ok = 1;
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < kAllocs; ++i) {
     mine.ptr[i] = reinterpret_cast<uint64_t>(ptrs[i]);
     if (cudaIpcGetMemHandle(&mine.h[i], ptrs[i]) != cudaSuccess) {
       cudaGetLastError();
@@ -190,12 +194,11 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
     ok = ok && all[q].ok;
     if (all[q].pid != mine.pid) same_process_ = false;
   }
-  for (int b = 0; b < 2; ++b) peer_buf_[b].assign(static_cast<size_t>(P), nullptr);
+  for (int b = 0; b < kBuffers; ++b) peer_buf_[b].assign(static_cast<size_t>(P), nullptr);
   peer_flags_.assign(static_cast<size_t>(P), nullptr);
   for (int q = 0; q < P && ok; ++q) {
     if (q == rank) {
-      peer_buf_[0][q] = base_[0];
-      peer_buf_[1][q] = base_[1];
+      for (int b = 0; b < kBuffers; ++b) peer_buf_[b][q] = base_[b];
       peer_flags_[q] = flags_;
       continue;
     }
@@ -212,12 +215,11 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
         break;
       }
       cudaGetLastError();
-      peer_buf_[0][q] = reinterpret_cast<float*>(all[q].ptr[0]);
-      peer_buf_[1][q] = reinterpret_cast<float*>(all[q].ptr[1]);
-      peer_flags_[q] = reinterpret_cast<uint64_t*>(all[q].ptr[2]);
+      for (int b = 0; b < kBuffers; ++b) peer_buf_[b][q] = reinterpret_cast<float*>(all[q].ptr[b]);
+      peer_flags_[q] = reinterpret_cast<uint64_t*>(all[q].ptr[kBuffers]);
     } else {
-      void* p[3] = {nullptr, nullptr, nullptr};
-      for (int i = 0; i < 3 && ok; ++i) {
+      void* p[kAllocs] = {};
+      for (int i = 0; i < kAllocs && ok; ++i) {
         if (cudaIpcOpenMemHandle(&p[i], all[q].h[i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
           cudaGetLastError();
           ok = false;
@@ -226,9 +228,8 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
         }
       }
       if (!ok) break;
-      peer_buf_[0][q] = static_cast<float*>(p[0]);
-      peer_buf_[1][q] = static_cast<float*>(p[1]);
-      peer_flags_[q] = static_cast<uint64_t*>(p[2]);
+      for (int b = 0; b < kBuffers; ++b) peer_buf_[b][q] = static_cast<float*>(p[b]);
+      peer_flags_[q] = static_cast<uint64_t*>(p[kBuffers]);
     }
   }
   // Agreement: all-gather the per-rank verdicts.
@@ -251,7 +252,7 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
     flags_ = nullptr;
     return false;
   }
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < kBuffers; ++b) {
     d_bufs_[b].resize(static_cast<size_t>(P));
     CG_CUDA(cudaMemcpy(d_bufs_[b].get(), peer_buf_[b].data(), P * sizeof(float*), cudaMemcpyHostToDevice));
   }
@@ -292,6 +293,13 @@ void PeerPanels::publish_to(int b, int dest, const float* src, int64_t ld_src, i
   publish_one_kernel<<<blocks, 256, 0, s>>>(d_bufs_[b].get(), d_flags_.get(), rank_, ranks_, dest, last, src,
                                             ld_src, static_cast<uint32_t>(rows), static_cast<uint32_t>(c4),
                                             slot_floats, ld_dst);
+  CG_LAUNCH_CHECK();
+}
+
+void PeerPanels::signal(cudaStream_t s) {
+  // A copy-free publish: one CTA fences and raises the flags (the rows were
+  // stored by an earlier kernel on this stream, complete at its boundary).
+  publish_kernel<<<1, 32, 0, s>>>(d_bufs_[0].get(), d_flags_.get(), rank_, ranks_, true, nullptr, 0, 0, 0, 0, 0);
   CG_LAUNCH_CHECK();
 }
 

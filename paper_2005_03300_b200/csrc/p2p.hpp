@@ -11,7 +11,9 @@
 // the SpMM.  Flags carry a device-side stage sequence number, so the exchange
 // works unchanged inside a replayed CUDA graph.
 //
-// Buffer reuse needs no "consumed" flags: slots are double-buffered and every
+// (Three buffers rotate because a producer SpMM may push the next exchange's
+// panel directly — strategy_rows.cu, "direct push".)
+// Buffer reuse needs no "consumed" flags: buffers rotate and every
 // rank waits for all peers' ready flags at every stage, on the stream that
 // also runs its SpMMs, and publishes stage s only after that stream passed
 // its wait for stage s-1.  A peer's ready(s-1) is raised only after the
@@ -48,8 +50,17 @@ class PeerPanels {
   bool init(Comm& comm, int rank, int ranks, int device, size_t bytes, cudaStream_t s);
   bool ready() const { return ranks_ > 1 && base_[0] != nullptr; }
 
-  // Buffer b (stage parity) of this rank: P slots of slot_floats each.
+  // Panel buffers rotate over consecutive exchanges; three, so a producer
+  // kernel can push stage s's panel while peers still read stage s-1's and
+  // may be finishing stage s-2's (see strategy_rows.cu).
+  static constexpr int kBuffers = 3;
+  // Buffer b of this rank: P slots of slot_floats each.
   float* buffer(int b) const { return base_[b]; }
+  // Device array of the P ranks' buffer b (for kernels that push directly).
+  float* const* device_buffers(int b) const { return d_bufs_[b].get(); }
+  // Raises this stage's ready flag on every peer without copying: the panel
+  // was already pushed by a producer kernel earlier on the same stream.
+  void signal(cudaStream_t s);
 
   // Publishes rows x cols (ld_src) of `src` into slot `rank` of buffer b on
   // every peer (and on this rank too unless skip_self) at leading dimension
@@ -74,11 +85,11 @@ class PeerPanels {
  private:
   int rank_ = 0, ranks_ = 1, device_ = 0;
   bool same_process_ = false;
-  float* base_[2] = {nullptr, nullptr};  // own allocations
+  float* base_[kBuffers] = {};          // own allocations
   uint64_t* flags_ = nullptr;            // own: ready[P] | pub_ctr | wait_ctr | arrivals
-  std::vector<float*> peer_buf_[2];      // [b][q] (q == rank: own)
+  std::vector<float*> peer_buf_[kBuffers];  // [b][q] (q == rank: own)
   std::vector<uint64_t*> peer_flags_;    // [q]
-  DevBuf<float*> d_bufs_[2];             // device copies of peer_buf_
+  DevBuf<float*> d_bufs_[kBuffers];      // device copies of peer_buf_
   DevBuf<uint64_t*> d_flags_;            // device copy of peer_flags_
   std::vector<void*> opened_;            // IPC mappings to close
 };

@@ -322,9 +322,10 @@ __device__ __forceinline__ void spmm_row_epilogue(const SpmmArgs& a, int64_t row
       z.w = m.w > 0.f ? z.w : z.w * 0.f;
     }
     store_vec(a.T + row * a.ldt, vec, f, z);
-    if (e.relu_out)
-      store_vec(e.relu_out + row * e.relu_ld, vec, f,
-                make_float4(fmaxf(z.x, 0.f), fmaxf(z.y, 0.f), fmaxf(z.z, 0.f), fmaxf(z.w, 0.f)));
+    const float4 rz = make_float4(fmaxf(z.x, 0.f), fmaxf(z.y, 0.f), fmaxf(z.z, 0.f), fmaxf(z.w, 0.f));
+    if (e.relu_out) store_vec(e.relu_out + row * e.relu_ld, vec, f, rz);
+    for (int p = 0; p < e.push_n; ++p)
+      store_vec(e.push_bufs[p] + e.push_off + row * e.push_ld, vec, f, e.push_relu ? rz : z);
     return;
   }
   constexpr int SLOTS = (kSpmmEpiMaxFo + TEAM - 1) / TEAM;
@@ -466,6 +467,8 @@ __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArg
       acc.z = old.z + acc.z;
       acc.w = old.w + acc.w;
     }
+    // Pushed rows become visible to the peers at kernel completion; the flag
+    // kernel that follows on this stream fences before raising their flags.
     spmm_row_epilogue<LV, TEAM>(a, row, lane, vec, q, vec_ok, acc);
     return;
   }

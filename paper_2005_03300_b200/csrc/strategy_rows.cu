@@ -81,11 +81,18 @@ class TrainerRows final : public Trainer {
       Mat u = view(acc_, h.rows, fout);
       gemm_aw(h, l - 1, 0, 0, u, false, kern::EPI_NONE, Mat{});
       if (!last && fusable(at_parts_, u)) {
-        // ReLU in the SpMM's row epilogue: Z and H_l in one pass.
+        // ReLU in the SpMM's row epilogue: Z and H_l in one pass; when the next
+        // layer's exchange moves H_l itself, the epilogue also pushes it
+        // straight into the peers' panel buffers.
         kern::SpmmEpi e;
-        e.relu_out = h_[static_cast<size_t>(l)].m.p;
-        e.relu_ld = h_[static_cast<size_t>(l)].m.ld;
+        const Mat& hl = h_[static_cast<size_t>(l)].m;
+        e.relu_out = hl.p;
+        e.relu_ld = hl.ld;
+        const bool next_takes_h =
+            l + 1 < num_layers() && !(reassociate_ && dims_[static_cast<size_t>(l + 1)] < dims_[static_cast<size_t>(l)]);
+        const bool push = next_takes_h && arm_push(e, hl, /*relu=*/true);
         stages(at_parts_, u, z, &e);
+        if (push) commit_push();
         return;
       }
       stages(at_parts_, u, z);
@@ -169,7 +176,12 @@ class TrainerRows final : public Trainer {
             kern::SpmmEpi e;  // ⊙ relu′(Z_prev) in the SpMM's row epilogue
             e.mask = zp.p;
             e.mask_ld = zp.ld;
+            // The next (lower) layer's exchange moves G_prev itself unless it
+            // is a narrow-first widening layer (G Wᵀ first): push it directly.
+            const bool next_takes_g = l - 1 >= 1 && !(reassociate_ && saved_t_ok(l - 1));
+            const bool push = next_takes_g && arm_push(e, gp, /*relu=*/false);
             stages(a_parts_, u, gp, &e);
+            if (push) commit_push();
             continue;
           }
           stages(a_parts_, u, gp);
@@ -215,13 +227,15 @@ class TrainerRows final : public Trainer {
         gemm_swt(s, l - 1, 0, 0, g_[static_cast<size_t>(l - 2)].m, false, kern::EPI_RELU_PRIME, &zp);
       }
     }
-    // Peer-memory buffers alternate between consecutive exchanges, and the
-    // captured epoch graph repeats its buffer sequence: an odd number of
-    // exchanges per epoch would give the last exchange of one epoch and the
-    // first of the next the same buffer.  A flag-only exchange evens it out.
-    if (p2p_ok_ && (epoch_exchanges_ & 1)) {
-      const int b = next_p2p_buffer();
-      p2p_.publish(b, p2p_.buffer(b), 4, 0, 0, 4, 4, /*skip_self=*/true, cs_);
+    // Peer-memory buffers rotate over consecutive exchanges, and the captured
+    // epoch graph repeats its buffer sequence: unless the exchanges per epoch
+    // are a multiple of the buffer count, the first exchanges of one epoch
+    // would reuse buffers the last ones of the previous epoch still need.
+    // Flag-only exchanges pad the count.
+    settle_pending();
+    while (p2p_ok_ && epoch_exchanges_ % PeerPanels::kBuffers != 0) {
+      next_p2p_buffer();
+      p2p_.signal(cs_);
       p2p_.wait_ready(cs_);
     }
     cs_after_ms();  // the Y all-reduces
@@ -259,6 +273,7 @@ class TrainerRows final : public Trainer {
 
   void stages(const std::vector<DeviceCsr>& parts, const Mat& mine, Mat out,
               const kern::SpmmEpi* epi = nullptr) {
+    if (!(pending_.valid && pending_.src == mine.p)) settle_pending();
     const int j = grid_.col_of(rank_);
     const Group& grp = stage_group();
     const bool comm = grp.size() > 1;
@@ -335,15 +350,25 @@ class TrainerRows final : public Trainer {
       }
       if (one_d() && p2p_ok_) {
         // NVLink peer-memory exchange: push this rank's panel into every
-        // rank's buffer, wait for the peers' panels, SpMM, release.
+        // rank's buffer (unless the producer kernel already did), wait for
+        // the peers' panels, SpMM.
         const int64_t step = ceil_div64(data_.n, blocks());
-        const int b = next_p2p_buffer();
+        const bool pushed = pending_.valid && pending_.src == mine.p && pending_.ld == mine.ld;
+        int b;
+        if (pushed) {
+          b = pending_.buf;
+          pending_.valid = false;
+        } else {
+          settle_pending();
+          b = next_p2p_buffer();
+        }
         Mat pg{p2p_.buffer(b), c_hi_ - c_lo_, mine.cols, mine.ld};
         std::vector<uint64_t> words;
         for (int q = 0; q < blocks(); ++q)
           words.push_back(static_cast<uint64_t>(block_range(data_.n, blocks(), q).size() * mine.cols));
         comm_->meter_bcast_all(grp, Category::DBcast, words);
-        p2p_.publish(b, mine.p, mine.ld, mine.rows, mine.cols, step * mine.ld, mine.ld, /*skip_self=*/false, cs_);
+        if (!pushed)
+          p2p_.publish(b, mine.p, mine.ld, mine.rows, mine.cols, step * mine.ld, mine.ld, /*skip_self=*/false, cs_);
         p2p_.wait_ready(cs_);
         spmm(blk, pg, out, false, epi);
         return;
@@ -442,11 +467,63 @@ class TrainerRows final : public Trainer {
   bool overlap_ok_ = false;       // own-block SpMM overlaps the peer pushes
   BlockRange own_{0, 0};          // this rank's vertex block (1D)
   RotatedCsr a_rot_, at_rot_;     // chunk CSRs with the own block first per row
-  uint64_t p2p_stage_ = 0;        // host parity of the double-buffered panels
+  uint64_t p2p_stage_ = 0;        // exchange count (buffer rotation)
   int epoch_exchanges_ = 0;       // peer-memory exchanges in the current epoch
   int next_p2p_buffer() {
     ++epoch_exchanges_;
-    return static_cast<int>(p2p_stage_++ & 1);
+    return static_cast<int>(p2p_stage_++ % PeerPanels::kBuffers);
+  }
+
+  // Direct push (fused producer + exchange): the SpMM whose row epilogue
+  // produces the next exchange's panel also stores it into every rank's
+  // buffer for that exchange, then p2p_.signal() raises the ready flags; the
+  // consuming stages() call skips its publish.  Safe with three rotating
+  // buffers: the producer runs during exchange s-1 (peers may still read the
+  // buffers of s-1 and s-2) and writes the buffer of s, last read at s-3,
+  // which every peer finished before it published s-1 (stream order).
+  struct PendingPush {
+    bool valid = false;
+    int buf = 0;
+    const float* src = nullptr;
+    int64_t ld = 0;
+  };
+  PendingPush pending_;
+
+  // Called before the producer's own exchange (which takes the next buffer in
+  // the rotation), so the pushed exchange gets the one after it.
+  bool arm_push(kern::SpmmEpi& e, const Mat& panel, bool relu) {
+    if (!(one_d() && p2p_ok_ && chunk_ok_ && !overlap_ok_ && !pipeline_enabled_ &&
+          panel.cols <= kCoalesceMaxF && !pending_.valid))
+      return false;
+    const int b = static_cast<int>((p2p_stage_ + 1) % PeerPanels::kBuffers);
+    e.push_bufs = p2p_.device_buffers(b);
+    e.push_n = grid_.ranks();
+    e.push_off = static_cast<int64_t>(rank_) * ceil_div64(data_.n, blocks()) * panel.ld;
+    e.push_ld = panel.ld;
+    e.push_relu = relu;
+    pending_ = PendingPush{false, b, panel.p, panel.ld};
+    armed_at_ = p2p_stage_;
+    return true;
+  }
+
+  // After the producer's exchange and SpMM: the pushed exchange takes its
+  // buffer in the rotation and its ready flags go up.
+  void commit_push() {
+    if (p2p_stage_ != armed_at_ + 1)
+      throw std::logic_error("direct push: the producer stage did not take exactly one exchange");
+    const int b = next_p2p_buffer();
+    if (b != pending_.buf) throw std::logic_error("direct push: buffer rotation mismatch");
+    p2p_.signal(cs_);
+    pending_.valid = true;
+  }
+  uint64_t armed_at_ = 0;
+
+  // A pushed exchange that no stage consumed still has to be waited for, so
+  // the device-side wait count stays in step with the publish count.
+  void settle_pending() {
+    if (!pending_.valid) return;
+    pending_.valid = false;
+    p2p_.wait_ready(cs_);
   }
   std::vector<OwnedMat> saved_t_;  // T = Aᵀ H of widening layers (narrow-first backward)
   std::vector<bool> saved_valid_;
