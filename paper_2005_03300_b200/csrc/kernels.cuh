@@ -68,6 +68,14 @@ void column_splits(int64_t rows, int64_t n_cols, int nb, const int64_t* row_ptr,
 // op(A) m x k: element (i, p) at A[i * a_sm + p * a_sk]
 // op(B) k x n: element (p, j) at B[p * b_sk + j * b_sn]
 enum Epilogue { EPI_NONE = 0, EPI_RELU = 1, EPI_RELU_PRIME = 2 };
+// Direct peer push of an SpMM's finished rows (see SpmmEpi::push_*).
+struct PushSpec {
+  float* const* bufs = nullptr;
+  int n = 0;
+  int64_t off = 0, ld = 0;
+  bool relu = false;
+};
+
 struct GemmDesc {
   int64_t m = 0, n = 0, k = 0;
   const float* A = nullptr;

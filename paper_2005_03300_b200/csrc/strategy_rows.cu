@@ -90,7 +90,7 @@ class TrainerRows final : public Trainer {
         e.relu_ld = hl.ld;
         const bool next_takes_h =
             l + 1 < num_layers() && !(reassociate_ && dims_[static_cast<size_t>(l + 1)] < dims_[static_cast<size_t>(l)]);
-        const bool push = next_takes_h && arm_push(e, hl, /*relu=*/true);
+        const bool push = next_takes_h && arm_push(e, hl, /*relu=*/true, u);
         stages(at_parts_, u, z, &e);
         if (push) commit_push();
         return;
@@ -179,7 +179,7 @@ class TrainerRows final : public Trainer {
             // The next (lower) layer's exchange moves G_prev itself unless it
             // is a narrow-first widening layer (G Wᵀ first): push it directly.
             const bool next_takes_g = l - 1 >= 1 && !(reassociate_ && saved_t_ok(l - 1));
-            const bool push = next_takes_g && arm_push(e, gp, /*relu=*/false);
+            const bool push = next_takes_g && arm_push(e, gp, /*relu=*/false, u);
             stages(a_parts_, u, gp, &e);
             if (push) commit_push();
             continue;
@@ -475,48 +475,67 @@ class TrainerRows final : public Trainer {
   }
 
   // Direct push (fused producer + exchange): the SpMM whose row epilogue
-  // produces the next exchange's panel also stores it into every rank's
-  // buffer for that exchange, then p2p_.signal() raises the ready flags; the
-  // consuming stages() call skips its publish.  Safe with three rotating
-  // buffers: the producer runs during exchange s-1 (peers may still read the
-  // buffers of s-1 and s-2) and writes the buffer of s, last read at s-3,
-  // which every peer finished before it published s-1 (stream order).
+  // produces the next exchange's panel also stores it into every rank's buffer
+  // for that exchange (GEMM producers do not: their short epilogues issue the
+  // remote row stores from too few threads — a 16 x 16 GEMM went from 9.5 to
+  // 68 us with the push), then p2p_.signal() raises
+  // the ready flags and the consuming stages() call skips its publish.  Safe
+  // with three rotating buffers: the producer runs no earlier than during
+  // exchange s-1 (peers may still read the buffers of s-1 and s-2) and writes
+  // the buffer of s, last read at s-3, which every peer finished before it
+  // published s-1 (stream order).
   struct PendingPush {
     bool valid = false;
     int buf = 0;
     const float* src = nullptr;
     int64_t ld = 0;
   };
-  PendingPush pending_;
+  PendingPush pending_;  // committed: the next exchange of `src` skips its publish
+  PendingPush armed_;    // armed: a producer kernel is about to push `src`
+  uint64_t armed_at_ = 0;
+  int armed_skip_ = 0;
 
-  // Called before the producer's own exchange (which takes the next buffer in
-  // the rotation), so the pushed exchange gets the one after it.
-  bool arm_push(kern::SpmmEpi& e, const Mat& panel, bool relu) {
+  // `skip` = exchanges the producer itself takes before the pushed one (1 for
+  // an SpMM producer whose own exchange still publishes, else 0).
+  bool arm(const Mat& panel, bool relu, int skip, kern::PushSpec* ps) {
     if (!(one_d() && p2p_ok_ && chunk_ok_ && !overlap_ok_ && !pipeline_enabled_ &&
-          panel.cols <= kCoalesceMaxF && !pending_.valid))
+          panel.cols <= kCoalesceMaxF && !armed_.valid))
       return false;
-    const int b = static_cast<int>((p2p_stage_ + 1) % PeerPanels::kBuffers);
-    e.push_bufs = p2p_.device_buffers(b);
-    e.push_n = grid_.ranks();
-    e.push_off = static_cast<int64_t>(rank_) * ceil_div64(data_.n, blocks()) * panel.ld;
-    e.push_ld = panel.ld;
-    e.push_relu = relu;
-    pending_ = PendingPush{false, b, panel.p, panel.ld};
+    const int b = static_cast<int>((p2p_stage_ + static_cast<uint64_t>(skip)) % PeerPanels::kBuffers);
+    ps->bufs = p2p_.device_buffers(b);
+    ps->n = grid_.ranks();
+    ps->off = static_cast<int64_t>(rank_) * ceil_div64(data_.n, blocks()) * panel.ld;
+    ps->ld = panel.ld;
+    ps->relu = relu;
+    armed_ = PendingPush{true, b, panel.p, panel.ld};
     armed_at_ = p2p_stage_;
+    armed_skip_ = skip;
+    return true;
+  }
+  bool arm_push(kern::SpmmEpi& e, const Mat& panel, bool relu, const Mat& producer_in) {
+    const int skip = pending_.valid && pending_.src == producer_in.p ? 0 : 1;
+    kern::PushSpec ps;
+    if (!arm(panel, relu, skip, &ps)) return false;
+    e.push_bufs = ps.bufs;
+    e.push_n = ps.n;
+    e.push_off = ps.off;
+    e.push_ld = ps.ld;
+    e.push_relu = ps.relu;
     return true;
   }
 
-  // After the producer's exchange and SpMM: the pushed exchange takes its
-  // buffer in the rotation and its ready flags go up.
+  // After the producer kernel: the pushed exchange takes its buffer in the
+  // rotation and its ready flags go up.
   void commit_push() {
-    if (p2p_stage_ != armed_at_ + 1)
-      throw std::logic_error("direct push: the producer stage did not take exactly one exchange");
+    settle_pending();  // an earlier push nobody consumed keeps the wait count in step
+    if (p2p_stage_ != armed_at_ + static_cast<uint64_t>(armed_skip_))
+      throw std::logic_error("direct push: unexpected exchanges between producer and push");
     const int b = next_p2p_buffer();
-    if (b != pending_.buf) throw std::logic_error("direct push: buffer rotation mismatch");
+    if (b != armed_.buf) throw std::logic_error("direct push: buffer rotation mismatch");
     p2p_.signal(cs_);
-    pending_.valid = true;
+    pending_ = armed_;
+    armed_.valid = false;
   }
-  uint64_t armed_at_ = 0;
 
   // A pushed exchange that no stage consumed still has to be waited for, so
   // the device-side wait count stays in step with the publish count.

@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/pu4
+timeout 1500 python -m pytest tests/test_gpu_training.py -m "gpu" -q --timeout 300 -p no:cacheprovider -rf -x > gpurun_out/pu4/pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pu4/pytest.log
+tail -2 gpurun_out/pu4/pytest.log
+for np in 2 4; do
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $np --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 400)) bench.py --gpus $np --steps 10 --warmup 3 --no-alt > gpurun_out/pu4/b$np.log 2>&1
+grep "^{" gpurun_out/pu4/b$np.log | cut -c1-140
+done
