@@ -3,7 +3,7 @@
 // rank (i, j) of the (P/c) x c grid owns block row i, walks the propagation
 // stages [chunk_begin(j), chunk_end(j)) (dist_impl.hpp:50-53) broadcasting
 // embedding panels down its column group, and the per-column partials meet in
-// a row all-reduce.  Broadcast panels are double-buffered on the comm stream
+// a row all-reduce.  NCCL broadcast panels are double-buffered on the comm stream
 // so stage q+1's NCCL broadcast overlaps stage q's SpMM.
 #include <algorithm>
 #include <cstdlib>
