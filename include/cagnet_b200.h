@@ -205,6 +205,16 @@ CAGNET_API int cagnet_init_glorot(const int64_t* dims, int ndims, uint64_t seed,
 /* --- training (dist.hpp:43-150) --------------------------------------------- */
 /* NCCL bootstrap: rank 0 creates the id, the launcher broadcasts its 128 bytes. */
 CAGNET_API int cagnet_comm_unique_id(uint8_t* out128);
+/* In-process world (replaces SimRuntime::run's thread-per-rank world,
+ * runtime.cpp:270-285): `ranks` ranks as host threads of this process, all on
+ * `device`, exchanging data through device memory with the same device-flag
+ * protocol as the NVLink peer-memory exchange.  The 128-byte id it writes is
+ * passed to cagnet_trainer_create like an NCCL id (one trainer per rank, each
+ * driven from its own thread).  Used where the GPUs are fewer than the ranks. */
+CAGNET_API int cagnet_comm_local_id(int ranks, int device, uint8_t* out128);
+/* Fails every pending and future wait of a local world (a rank that raised
+ * must release its peers, like the reference's SimError propagation). */
+CAGNET_API int cagnet_comm_local_abort(const uint8_t* id128, const char* why);
 
 /* Creates rank `rank` of Strategy{kind, ranks, repl, block} on the dataset's
  * device.  dims[ndims] are the layer widths; weights are the fp64 Glorot

@@ -20,6 +20,8 @@ from .api import (  # noqa: F401
     block_range,
     block_sizes,
     ceil_div,
+    comm_local_abort,
+    comm_local_id,
     comm_unique_id,
     device_count,
     kernel_launches,

@@ -82,6 +82,8 @@ SIGNATURES = {
     "cagnet_dataset_free": [vp],
     "cagnet_init_glorot": [_i64p, i32, u64, _f64p],
     "cagnet_comm_unique_id": [C.c_char_p],
+    "cagnet_comm_local_id": [i32, i32, C.c_char_p],
+    "cagnet_comm_local_abort": [C.c_char_p, C.c_char_p],
     "cagnet_trainer_create": [vp, _i64p, i32, _f64p, f64, i32, i32, i32, i32, i32, vp,
                               C.POINTER(vp)],
     "cagnet_trainer_distribute": [vp],

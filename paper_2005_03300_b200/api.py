@@ -349,6 +349,18 @@ def comm_unique_id() -> bytes:
     return buf.raw
 
 
+def comm_local_id(ranks: int, device: int = 0) -> bytes:
+    """Id of an in-process world: `ranks` ranks as threads of this process on
+    one GPU (SimRuntime's thread-per-rank model, runtime.cpp:270-285)."""
+    buf = C.create_string_buffer(128)
+    check(lib.cagnet_comm_local_id(ranks, device, buf))
+    return buf.raw
+
+
+def comm_local_abort(nid: bytes, why: str) -> None:
+    lib.cagnet_comm_local_abort(nid, why.encode())
+
+
 class Trainer:
     """One rank of a partitioned trainer (dist.hpp:83-131) on the dataset's GPU."""
 
@@ -553,23 +565,37 @@ def _verified(trainers, get, what):
 
 
 def run_distributed(data_factory, model: GnnModel, strat: Strategy, epochs: int,
-                    devices=None) -> DistOutcome:
+                    devices=None, comm: str = "auto") -> DistOutcome:
     """run_distributed (dist_common.cpp:205-222) in one process: one host
-    thread and one GPU per rank (the reference's thread-per-rank model,
-    runtime.cpp:270-285), NCCL over NVLink between them.  data_factory(device)
-    must build the same dataset on each device."""
+    thread per rank (the reference's thread-per-rank model,
+    runtime.cpp:270-285).  comm = "nccl": one GPU per rank, NCCL and NVLink
+    peer memory between them; "local": every rank on one GPU through the
+    in-process world (device-memory collectives, same flag protocol);
+    "auto": NCCL when there are at least P GPUs, else local.
+    data_factory(device) must build the same dataset on each call."""
     if epochs <= 0:
         raise InvalidArgument(1, "run_epochs: epoch count must be positive")
     P = strat.ranks
     ProcessGrid(strat)  # validates the geometry before any GPU work
+    if comm not in ("auto", "nccl", "local"):
+        raise InvalidArgument(1, f"run_distributed: unknown comm backend {comm!r}")
     if devices is None:
         n_dev = C.c_int()
         check(lib.cagnet_device_count(C.byref(n_dev)))
-        if n_dev.value < P:
+        if comm == "auto":
+            comm = "nccl" if n_dev.value >= P else "local"
+        if comm == "nccl" and n_dev.value < P:
             raise InvalidArgument(1, f"run_distributed: {P} ranks need {P} GPUs, "
                                      f"found {n_dev.value}")
-        devices = list(range(P))
-    nid = comm_unique_id() if P > 1 else None
+        if n_dev.value < 1:
+            raise InvalidArgument(1, "run_distributed: no GPU")
+        devices = list(range(P)) if comm == "nccl" else [0] * P
+    elif comm == "auto":
+        comm = "local" if P > 1 and len(set(devices)) == 1 else "nccl"
+    if comm == "local" and len(set(devices)) != 1:
+        raise InvalidArgument(1, "run_distributed: the local world runs every rank on one GPU")
+    local = comm == "local" and P > 1
+    nid = (comm_local_id(P, devices[0]) if local else comm_unique_id()) if P > 1 else None
     datas = [None] * P
     trainers = [None] * P
     losses = [None] * P
@@ -583,6 +609,8 @@ def run_distributed(data_factory, model: GnnModel, strat: Strategy, epochs: int,
             losses[r] = trainers[r].run_epochs(epochs)
         except Exception as e:  # the lowest-rank exception wins (runtime.cpp:281-284)
             errors.append((r, e))
+            if local:  # release the peers blocked in this rank's collectives
+                comm_local_abort(nid, f"rank {r} raised: {e}")
 
     threads = [threading.Thread(target=body, args=(r,)) for r in range(P)]
     for th in threads:
@@ -590,7 +618,10 @@ def run_distributed(data_factory, model: GnnModel, strat: Strategy, epochs: int,
     for th in threads:
         th.join()
     if errors:
-        raise sorted(errors, key=lambda x: x[0])[0][1]
+        # The lowest-rank original failure wins; peers released by an abort
+        # only report its echo.
+        primary = [x for x in errors if "local world aborted" not in str(x[1])] or errors
+        raise sorted(primary, key=lambda x: x[0])[0][1]
     n = datas[0].n
     L = len(model.layer_dims)
     out_losses = _verified(trainers, lambda t: losses[t.rank], "loss")

@@ -3,6 +3,7 @@
 // codes and records the message per thread.
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -27,6 +28,19 @@ struct cagnet_trainer_s {
 };
 
 namespace {
+
+// Process defaults, applied before the first CUDA call of this process when
+// the library is loaded first (an explicit setting always wins):
+// * a hardware work queue per stream for up to 16 streams of in-process ranks;
+// * module data loaded eagerly: with lazy loading, the first launch of a
+//   kernel may wait for a context-wide synchronisation, which never comes
+//   while a rank sharing the GPU spins in a device-side wait for this rank
+//   (the CUDA programming guide's documented lazy-loading hazard for kernels
+//   that wait on each other; CUDA_MODULE_DATA_LOADING=EAGER is its remedy).
+__attribute__((constructor)) void cagnet_env_defaults() {
+  setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+  setenv("CUDA_MODULE_DATA_LOADING", "EAGER", 0);
+}
 
 thread_local std::string g_error;
 
@@ -471,6 +485,28 @@ int cagnet_comm_unique_id(uint8_t* out128) {
     CG_NCCL(ncclGetUniqueId(&id));
     static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
     std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int cagnet_comm_local_id(int ranks, int device, uint8_t* out128) {
+  return guarded([&] {
+    cagnet::require(out128 != nullptr, "comm_local_id: null output");
+    int n = 0;
+    CG_CUDA(cudaGetDeviceCount(&n));
+    cagnet::require(device >= 0 && device < n, "comm_local_id: device " + std::to_string(device) +
+                                                   " outside [0, " + std::to_string(n) + ")");
+    cagnet::LocalId id;
+    cagnet::LocalWorld::create(ranks, device, &id);
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int cagnet_comm_local_abort(const uint8_t* id128, const char* why) {
+  return guarded([&] {
+    cagnet::require(cagnet::is_local_id(id128), "comm_local_abort: not a local world id");
+    cagnet::LocalId id;
+    std::memcpy(&id, id128, sizeof(id));
+    cagnet::LocalWorld::abort_id(id, why ? why : "aborted by a rank");
   });
 }
 

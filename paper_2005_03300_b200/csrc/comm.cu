@@ -1,11 +1,51 @@
+#include <cstring>
+
 #include "comm.hpp"
 
 namespace cagnet {
+
+namespace {
+size_t dtype_size(ncclDataType_t t) {
+  switch (t) {
+    case ncclInt64: case ncclUint64: case ncclFloat64: return 8;
+    case ncclInt32: case ncclUint32: case ncclFloat32: return 4;
+    case ncclInt8: case ncclUint8: return 1;
+    default: return 2;
+  }
+}
+int local_dtype(ncclDataType_t t) {
+  if (t == ncclFloat32) return 0;
+  if (t == ncclFloat64) return 1;
+  throw std::invalid_argument("local collectives: reductions support f32 and f64 only");
+}
+}  // namespace
 
 Comm::Comm(const ProcessGrid& grid, int rank, const ncclUniqueId* id)
     : rank_(rank), ranks_(grid.ranks()) {
   if (ranks_ == 1) return;
   if (!id) throw std::invalid_argument("Comm: an NCCL unique id is required for P > 1");
+  if (is_local_id(id)) {
+    LocalId lid;
+    std::memcpy(&lid, id, sizeof(lid));
+    if (lid.ranks != ranks_)
+      throw std::invalid_argument("Comm: local world has " + std::to_string(lid.ranks) + " ranks, grid has " +
+                                  std::to_string(ranks_));
+    int dev = 0;
+    CG_CUDA(cudaGetDevice(&dev));
+    if (dev != lid.device)
+      throw std::invalid_argument("Comm: local world lives on device " + std::to_string(lid.device) +
+                                  " but this rank runs on device " + std::to_string(dev));
+    auto w = LocalWorld::attach(lid, rank);
+    // Register every group now: flag arenas are allocated outside any capture.
+    w->group_flags(grid.world());
+    if (grid.kind() != GridKind::Row1D) {
+      w->group_flags(grid.row_group(rank));
+      w->group_flags(grid.col_group(rank));
+    }
+    if (grid.has_fiber_groups()) w->group_flags(grid.fiber_group(rank));
+    local_ = std::make_unique<LocalCollectives>(std::move(w), rank);
+    return;
+  }
   CG_NCCL(ncclCommInitRank(&world_, ranks_, *id, rank));
   comms_[grid.world().id] = world_;
   // Split one communicator per group kind, in the same order on every rank.
@@ -20,6 +60,26 @@ Comm::Comm(const ProcessGrid& grid, int rank, const ncclUniqueId* id)
     split(grid.col_group(rank));
   }
   if (grid.has_fiber_groups()) split(grid.fiber_group(rank));
+}
+
+void Comm::check_async() {
+  if (local_) {
+    local_->world().check();
+    return;
+  }
+  for (auto& kv : comms_) {
+    ncclResult_t async = ncclSuccess;
+    if (kv.second && ncclCommGetAsyncError(kv.second, &async) == ncclSuccess && async != ncclSuccess &&
+        async != ncclInProgress) {
+      const std::string msg = std::string("NCCL asynchronous error on group ") + std::to_string(kv.first) +
+                              ": " + ncclGetErrorString(async);
+      for (auto& c : comms_)
+        if (c.second) ncclCommAbort(c.second);
+      comms_.clear();
+      world_ = nullptr;
+      throw NcclError(msg + " (communicators aborted)");
+    }
+  }
 }
 
 Comm::~Comm() {
@@ -40,7 +100,10 @@ void Comm::bcast(const Group& g, int root_rank, void* buf, size_t count, ncclDat
   (void)g.index_of(rank_);
   const int root = g.index_of(root_rank);
   if (g.size() == 1) return;
-  if (count) CG_NCCL(ncclBroadcast(buf, buf, count, t, root, comm_for(g), s));
+  if (local_)
+    local_->bcast(g, root, buf, count * dtype_size(t), s);
+  else if (count)
+    CG_NCCL(ncclBroadcast(buf, buf, count, t, root, comm_for(g), s));
   CommCounter& c = ctr(cat);
   c.calls += 1;
   c.payload_words += words;
@@ -57,6 +120,10 @@ void Comm::bcast_csr(const Group& g, int root_rank, int64_t* row_ptr, int64_t n_
   (void)g.index_of(rank_);
   const int root = g.index_of(root_rank);
   if (g.size() == 1) return;
+  if (local_) {
+    local_->bcast3(g, root, row_ptr, static_cast<size_t>(n_rows + 1) * 8, col, static_cast<size_t>(nnz) * 4,
+                   vals, static_cast<size_t>(nnz) * 4, s);
+  } else {
   ncclComm_t comm = comm_for(g);
   CG_NCCL(ncclGroupStart());
   CG_NCCL(ncclBroadcast(row_ptr, row_ptr, static_cast<size_t>(n_rows + 1), ncclInt64, root, comm, s));
@@ -65,6 +132,7 @@ void Comm::bcast_csr(const Group& g, int root_rank, int64_t* row_ptr, int64_t n_
     CG_NCCL(ncclBroadcast(vals, vals, static_cast<size_t>(nnz), ncclFloat32, root, comm, s));
   }
   CG_NCCL(ncclGroupEnd());
+  }
   CommCounter& c = ctr(cat);
   const uint64_t words = static_cast<uint64_t>(nnz);
   c.calls += 1;
@@ -81,7 +149,10 @@ void Comm::all_reduce(const Group& g, void* buf, size_t count, ncclDataType_t t,
                       uint64_t words, cudaStream_t s) {
   const int member = g.index_of(rank_);
   if (g.size() == 1) return;
-  if (count) CG_NCCL(ncclAllReduce(buf, buf, count, t, ncclSum, comm_for(g), s));
+  if (local_)
+    local_->all_reduce(g, buf, count, local_dtype(t), s);
+  else if (count)
+    CG_NCCL(ncclAllReduce(buf, buf, count, t, ncclSum, comm_for(g), s));
   const uint64_t gs = g.size(), m = words, r = static_cast<uint64_t>(member);
   auto chunk = [&](uint64_t j) { return m / gs + (j < m % gs ? 1 : 0); };
   CommCounter& c = ctr(cat);
@@ -97,7 +168,9 @@ void Comm::reduce_scatter(const Group& g, const void* send, void* recv, size_t s
                           cudaStream_t s) {
   const int member = g.index_of(rank_);
   if (g.size() == 1) return;
-  if (slice_count)
+  if (local_)
+    local_->reduce_scatter(g, send, recv, slice_count, local_dtype(t), s);
+  else if (slice_count)
     CG_NCCL(ncclReduceScatter(send, recv, slice_count, t, ncclSum, comm_for(g), s));
   uint64_t m = 0;
   for (uint64_t w : slot_words) m += w;
@@ -115,7 +188,10 @@ void Comm::all_gather(const Group& g, const void* send, void* recv, size_t slice
                       cudaStream_t s) {
   const int member = g.index_of(rank_);
   if (g.size() == 1) return;
-  if (slice_count) CG_NCCL(ncclAllGather(send, recv, slice_count, t, comm_for(g), s));
+  if (local_)
+    local_->all_gather(g, send, recv, slice_count * dtype_size(t), s);
+  else if (slice_count)
+    CG_NCCL(ncclAllGather(send, recv, slice_count, t, comm_for(g), s));
   uint64_t m = 0;
   for (uint64_t w : slot_words) m += w;
   CommCounter& c = ctr(cat);
@@ -130,9 +206,11 @@ void Comm::bcast_all(const Group& g, void* buf, size_t slice_count, ncclDataType
                      Category cat, const std::vector<uint64_t>& words, cudaStream_t s) {
   const int member = g.index_of(rank_);
   if (g.size() == 1) return;
-  const size_t esize = (t == ncclInt64 || t == ncclUint64 || t == ncclFloat64) ? 8 : 4;
+  const size_t esize = dtype_size(t);
   char* base = static_cast<char*>(buf);
-  if (slice_count)
+  if (local_)
+    local_->all_gather(g, base + static_cast<size_t>(member) * slice_count * esize, buf, slice_count * esize, s);
+  else if (slice_count)
     CG_NCCL(ncclAllGather(base + static_cast<size_t>(member) * slice_count * esize, buf, slice_count,
                           t, comm_for(g), s));
   meter_bcast_all(g, cat, words);
@@ -157,13 +235,12 @@ void Comm::meter_bcast_all(const Group& g, Category cat, const std::vector<uint6
 
 void Comm::setup_all_gather(const void* send, void* recv, size_t count, ncclDataType_t t,
                             cudaStream_t s) {
+  const size_t bytes = count * dtype_size(t);
+  if (local_) {
+    local_->setup_all_gather(send, recv, bytes, s);
+    return;
+  }
   if (ranks_ == 1) {
-    size_t bytes = count;
-    switch (t) {
-      case ncclInt64: case ncclUint64: case ncclFloat64: bytes *= 8; break;
-      case ncclInt32: case ncclUint32: case ncclFloat32: bytes *= 4; break;
-      default: break;
-    }
     if (send != recv) CG_CUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, s));
     return;
   }

@@ -12,8 +12,10 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <vector>
 
+#include "comm_local.hpp"
 #include "common.cuh"
 #include "grid.hpp"
 
@@ -38,6 +40,11 @@ struct CommCounter {
                                 __FILE__ + ":" + std::to_string(__LINE__) + ")");        \
   } while (0)
 
+// Two backends behind one interface: NCCL (one rank per GPU, the product
+// path) and an in-process LocalWorld (all ranks as threads on one GPU;
+// comm_local.hpp), chosen by the id: a LocalId selects the local backend.
+// Every collective of one group must be issued from one stream per rank
+// (the trainers use their comm stream), like calls on one NCCL communicator.
 class Comm {
  public:
   // id may be null only when the grid has a single rank.
@@ -81,11 +88,26 @@ class Comm {
 
   // Fuse the collectives issued in between into one NCCL launch.
   void group_start() {
-    if (ranks_ > 1) CG_NCCL(ncclGroupStart());
+    if (ranks_ > 1 && !local_) CG_NCCL(ncclGroupStart());
   }
   void group_end() {
-    if (ranks_ > 1) CG_NCCL(ncclGroupEnd());
+    if (ranks_ > 1 && !local_) CG_NCCL(ncclGroupEnd());
   }
+
+  // In-process world (null on the NCCL backend).
+  LocalWorld* local_world() const { return local_ ? &local_->world() : nullptr; }
+  bool is_local() const { return local_ != nullptr; }
+  // All ranks of the world (local backend; no-op on NCCL).
+  // A fresh host channel id for a peer-memory exchange of the local world
+  // (every rank creates its exchanges in the same order).
+  int next_local_channel() { return -1000 - local_channels_++; }
+  void local_barrier() {
+    if (local_) local_->world().barrier(rank_);
+  }
+  // Raises NcclError when an asynchronous communication failure was
+  // recorded: NCCL's async error (the communicators are aborted first) or a
+  // timed-out device wait of the local world.
+  void check_async();
 
   // Unmetered world all-gather for setup metadata (tile shapes).
   void setup_all_gather(const void* send, void* recv, size_t count, ncclDataType_t t,
@@ -117,6 +139,8 @@ class Comm {
   int rank_ = 0;
   int ranks_ = 1;
   ncclComm_t world_ = nullptr;
+  std::unique_ptr<LocalCollectives> local_;
+  int local_channels_ = 0;
   std::map<int, ncclComm_t> comms_;  // group id -> communicator
   CommCounter counters_[kNumCategories];
 };

@@ -374,8 +374,7 @@ void copy2d(float* dst, int64_t ldd, const float* src, int64_t lds, int64_t rows
             cudaStream_t stream) {
   if (rows <= 0 || cols <= 0) return;
   if (ldd == cols && lds == cols) {
-    CG_CUDA(cudaMemcpyAsync(dst, src, rows * cols * sizeof(float), cudaMemcpyDeviceToDevice,
-                            stream));
+    copy_bytes(dst, src, static_cast<size_t>(rows * cols) * sizeof(float), stream);
     return;
   }
   copy2d_kernel<<<grid_for(rows * cols), 256, 0, stream>>>(dst, ldd, src, lds, rows, cols);
@@ -387,6 +386,58 @@ void transpose2d(float* dst, int64_t ldd, const float* src, int64_t lds, int64_t
   if (rows <= 0 || cols <= 0) return;
   dim3 grid(static_cast<unsigned>(ceil_div64(cols, 32)), static_cast<unsigned>(ceil_div64(rows, 32)));
   transpose2d_kernel<<<grid, dim3(32, 8), 0, stream>>>(dst, ldd, src, lds, rows, cols);
+  CG_LAUNCH_CHECK();
+}
+
+namespace {
+// Byte copies / zero fills as SM kernels, not copy-engine or runtime memset
+// operations: on a GPU shared by several in-process ranks a copy-engine
+// queue entry that waits for its stream can block other ranks' copies behind
+// it (the waits of comm_local.cu would then never be satisfied).
+__global__ void copy16_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void copy1_kernel(unsigned char* __restrict__ dst, const unsigned char* __restrict__ src, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+__global__ void zero16_kernel(uint4* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    dst[i] = make_uint4(0, 0, 0, 0);
+}
+__global__ void zero1_kernel(unsigned char* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    dst[i] = 0;
+}
+unsigned copy_grid(size_t n) {
+  const size_t b = (n + 255) / 256;
+  return static_cast<unsigned>(b < 2048 ? (b ? b : 1) : 2048);
+}
+}  // namespace
+
+void copy_bytes(void* dst, const void* src, size_t bytes, cudaStream_t stream) {
+  if (bytes == 0 || dst == src) return;
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src) | bytes) % 16 == 0) {
+    copy16_kernel<<<copy_grid(bytes / 16), 256, 0, stream>>>(static_cast<uint4*>(dst),
+                                                            static_cast<const uint4*>(src), bytes / 16);
+  } else {
+    copy1_kernel<<<copy_grid(bytes), 256, 0, stream>>>(static_cast<unsigned char*>(dst),
+                                                       static_cast<const unsigned char*>(src), bytes);
+  }
+  CG_LAUNCH_CHECK();
+}
+
+void zero_bytes(void* dst, size_t bytes, cudaStream_t stream) {
+  if (bytes == 0) return;
+  if ((reinterpret_cast<uintptr_t>(dst) | bytes) % 16 == 0)
+    zero16_kernel<<<copy_grid(bytes / 16), 256, 0, stream>>>(static_cast<uint4*>(dst), bytes / 16);
+  else
+    zero1_kernel<<<copy_grid(bytes), 256, 0, stream>>>(static_cast<unsigned char*>(dst), bytes);
   CG_LAUNCH_CHECK();
 }
 

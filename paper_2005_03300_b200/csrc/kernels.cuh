@@ -129,6 +129,9 @@ void push_loss(double* losses, int* slot, const double* partial, cudaStream_t st
 void mask_relu_prime(float* g, int64_t ldg, const float* z, int64_t ldz, int64_t rows,
                      int64_t cols, cudaStream_t stream);
 // dst[r, 0:cols] = src[r, 0:cols] for strided row-major blocks.
+// Device-to-device byte copy / zero fill as SM kernels (stream ordered).
+void copy_bytes(void* dst, const void* src, size_t bytes, cudaStream_t stream);
+void zero_bytes(void* dst, size_t bytes, cudaStream_t stream);
 void copy2d(float* dst, int64_t ldd, const float* src, int64_t lds, int64_t rows, int64_t cols,
             cudaStream_t stream);
 // dst (cols x rows, ldd) = src^T (rows x cols, lds)

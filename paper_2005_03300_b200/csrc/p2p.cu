@@ -4,33 +4,10 @@
 #include <cstring>
 
 #include "p2p.hpp"
+#include "sync.cuh"
 
 namespace cagnet {
 namespace {
-
-constexpr uint64_t kSpinLimitNs = 20ull * 1000 * 1000 * 1000;  // 20 s, then trap
-
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t now_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ void spin_until_geq(const uint64_t* p, uint64_t target) {
-  if (ld_acquire_sys(p) >= target) return;
-  const uint64_t t0 = now_ns();
-  while (ld_acquire_sys(p) < target) {
-    if (now_ns() - t0 > kSpinLimitNs) __trap();
-    __nanosleep(128);
-  }
-}
 
 // Flag block of every rank (uint64): ready[P] | consumed[P] | ctr | arrivals.
 //   ready[q]    = last stage rank q published into this rank's buffers
@@ -107,20 +84,20 @@ __global__ void publish_one_kernel(float* const* bufs, uint64_t* const* flags, i
   }
 }
 
-__global__ void wait_slot_kernel(uint64_t* const* flags, int rank, int P, int q) {
+__global__ void wait_slot_kernel(uint64_t* const* flags, int rank, int P, int q, WaitError* err) {
   const Flags F{P};
   uint64_t* my = flags[rank];
   const uint64_t s = *F.wait_ctr(my) + 1;
-  if (threadIdx.x == 0) spin_until_geq(F.ready(my) + q, s);
+  if (threadIdx.x == 0) spin_until_geq(F.ready(my) + q, s, err, -2, rank, q);
   __threadfence_system();
 }
 
-__global__ void wait_ready_kernel(uint64_t* const* flags, int rank, int P) {
+__global__ void wait_ready_kernel(uint64_t* const* flags, int rank, int P, WaitError* err) {
   const Flags F{P};
   uint64_t* my = flags[rank];
   const uint64_t s = *F.wait_ctr(my) + 1;
   for (int q = threadIdx.x; q < P; q += blockDim.x)
-    if (q != rank) spin_until_geq(F.ready(my) + q, s);
+    if (q != rank) spin_until_geq(F.ready(my) + q, s, err, -2, rank, q);
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) *F.wait_ctr(my) = s;
@@ -146,6 +123,20 @@ PeerPanels::~PeerPanels() {
   for (float* b : base_)
     if (b) cudaFree(b);
   if (flags_) cudaFree(flags_);
+  wait_error_free(err_host_);
+}
+
+void PeerPanels::check() const {
+  const std::string msg = wait_error_message(err_host_, "peer-memory panel exchange");
+  if (!msg.empty()) throw NcclError(msg);
+}
+
+void PeerPanels::post_issued() {
+  if (local_) local_->post(channel_, rank_, ++host_pub_);
+}
+
+void PeerPanels::wait_issued(const std::vector<int>& who, uint64_t stage) {
+  if (local_) local_->wait_posted(channel_, who, stage);
 }
 
 bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes, cudaStream_t s) {
@@ -154,6 +145,13 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
   device_ = device;
   if (ranks <= 1) return false;
   const int P = ranks;
+  local_ = comm.local_world();
+  if (local_) channel_ = comm.next_local_channel();
+  host_pub_ = host_wait_ = 0;
+  peers_.clear();
+  for (int q = 0; q < P; ++q)
+    if (q != rank) peers_.push_back(q);
+  if (!err_host_) err_host_ = wait_error_alloc(&err_dev_);
   // Allocate first so every rank can advertise handles; freed again on fallback.
   for (int b = 0; b < kBuffers; ++b) {
     CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&base_[b]), bytes));
@@ -202,7 +200,11 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
       peer_flags_[q] = flags_;
       continue;
     }
-    if (same_process_) {
+    if (same_process_ && all[q].device == device) {
+      // Ranks sharing one GPU (in-process world): plain device pointers.
+      for (int b = 0; b < kBuffers; ++b) peer_buf_[b][q] = reinterpret_cast<float*>(all[q].ptr[b]);
+      peer_flags_[q] = reinterpret_cast<uint64_t*>(all[q].ptr[kBuffers]);
+    } else if (same_process_) {
       int can = 0;
       cudaDeviceCanAccessPeer(&can, device, all[q].device);
       if (!can) {
@@ -276,6 +278,7 @@ void PeerPanels::publish(int b, const float* src, int64_t ld_src, int64_t rows, 
                                         ld_src, static_cast<uint32_t>(rows), static_cast<uint32_t>(c4),
                                         slot_floats, ld_dst);
   CG_LAUNCH_CHECK();
+  post_issued();
 }
 
 void PeerPanels::publish_to(int b, int dest, const float* src, int64_t ld_src, int64_t rows, int64_t cols,
@@ -294,6 +297,7 @@ void PeerPanels::publish_to(int b, int dest, const float* src, int64_t ld_src, i
                                             ld_src, static_cast<uint32_t>(rows), static_cast<uint32_t>(c4),
                                             slot_floats, ld_dst);
   CG_LAUNCH_CHECK();
+  if (last) post_issued();  // the stage's pushes were issued back to back
 }
 
 void PeerPanels::signal(cudaStream_t s) {
@@ -301,15 +305,18 @@ void PeerPanels::signal(cudaStream_t s) {
   // stored by an earlier kernel on this stream, complete at its boundary).
   publish_kernel<<<1, 32, 0, s>>>(d_bufs_[0].get(), d_flags_.get(), rank_, ranks_, true, nullptr, 0, 0, 0, 0, 0);
   CG_LAUNCH_CHECK();
+  post_issued();
 }
 
 void PeerPanels::wait_slot(int q, cudaStream_t s) {
-  wait_slot_kernel<<<1, 32, 0, s>>>(d_flags_.get(), rank_, ranks_, q);
+  wait_issued({q}, host_wait_ + 1);
+  wait_slot_kernel<<<1, 32, 0, s>>>(d_flags_.get(), rank_, ranks_, q, err_dev_);
   CG_LAUNCH_CHECK();
 }
 
 void PeerPanels::wait_ready(cudaStream_t s) {
-  wait_ready_kernel<<<1, 32 * ((ranks_ + 31) / 32), 0, s>>>(d_flags_.get(), rank_, ranks_);
+  wait_issued(peers_, ++host_wait_);
+  wait_ready_kernel<<<1, 32 * ((ranks_ + 31) / 32), 0, s>>>(d_flags_.get(), rank_, ranks_, err_dev_);
   CG_LAUNCH_CHECK();
 }
 

@@ -21,8 +21,15 @@
 // overwrites — has finished (stream order on the peer), so when a rank
 // publishes stage s nobody still reads that buffer.
 //
-// All waits are bounded (~20 s of spinning, then __trap()), so a broken peer
-// aborts the kernel instead of hanging the GPU.
+// All waits are bounded (~20 s of spinning): a broken peer makes the wait
+// record itself in a host-mapped error word and return instead of hanging
+// the GPU or trapping the context; check() turns the record into an
+// NcclError (CAGNET_ENCCL) at the trainer's next synchronisation.
+//
+// With an in-process LocalWorld (all ranks on one GPU, comm_local.hpp) the
+// same kernels and flags run unchanged; each publish additionally posts a
+// host-side "issued" count and each wait first waits for the peers' posts,
+// so a device wait only ever targets already-issued work.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -81,6 +88,8 @@ class PeerPanels {
                   int64_t slot_floats, int64_t ld_dst, bool last, cudaStream_t s);
   // Waits until peer q published the current stage (no counter change).
   void wait_slot(int q, cudaStream_t s);
+  // Throws NcclError when a device wait of this exchange timed out.
+  void check() const;
 
  private:
   int rank_ = 0, ranks_ = 1, device_ = 0;
@@ -92,6 +101,15 @@ class PeerPanels {
   DevBuf<float*> d_bufs_[kBuffers];      // device copies of peer_buf_
   DevBuf<uint64_t*> d_flags_;            // device copy of peer_flags_
   std::vector<void*> opened_;            // IPC mappings to close
+  WaitError* err_host_ = nullptr;        // host-mapped wait-error word
+  WaitError* err_dev_ = nullptr;
+  // In-process world: host-side issued counts (publish / wait stages).
+  LocalWorld* local_ = nullptr;
+  int channel_ = 0;
+  uint64_t host_pub_ = 0, host_wait_ = 0;
+  std::vector<int> peers_;
+  void post_issued();
+  void wait_issued(const std::vector<int>& who, uint64_t stage);
 };
 
 }  // namespace cagnet

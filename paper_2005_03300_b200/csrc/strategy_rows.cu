@@ -63,7 +63,7 @@ class TrainerRows final : public Trainer {
         }
       }
     }
-    CG_CUDA(cudaDeviceSynchronize());
+    settle();
   }
 
   void forward_layer(int l) override {
@@ -149,7 +149,7 @@ class TrainerRows final : public Trainer {
   void backward_and_step() override {
     const int L = num_layers();
     // Only column 0 contributes the loss so replicated rows count once.
-    if (grid_.col_of(rank_) != 0) CG_CUDA(cudaMemsetAsync(loss_partial_.get(), 0, sizeof(double), cs_));
+    if (grid_.col_of(rank_) != 0) kern::zero_bytes(loss_partial_.get(), sizeof(double), cs_);
     loss_all_reduce(loss_partial_.get());
     for (int l = L - 1; l >= 1; --l) {
       const Mat& g = g_[static_cast<size_t>(l - 1)].m;
@@ -161,7 +161,7 @@ class TrainerRows final : public Trainer {
         if (grid_.col_of(rank_) == 0)
           gemm_hts(saved_t_[static_cast<size_t>(l)].m, g, y, false);
         else
-          CG_CUDA(cudaMemsetAsync(y.p, 0, y.rows * y.ld * sizeof(float), cs_));
+          kern::zero_bytes(y.p, y.rows * y.ld * sizeof(float), cs_);
         // Y is only read by the SGD step: its all-reduce runs on the comm
         // stream behind the remaining backward compute (joined before SGD).
         ms_after_cs();
@@ -218,7 +218,7 @@ class TrainerRows final : public Trainer {
       if (grid_.col_of(rank_) == 0)
         gemm_hts(h_[static_cast<size_t>(l - 1)].m, s, y, false);
       else
-        CG_CUDA(cudaMemsetAsync(y.p, 0, y.rows * y.ld * sizeof(float), cs_));
+        kern::zero_bytes(y.p, y.rows * y.ld * sizeof(float), cs_);
       ms_after_cs();
       comm_->all_reduce(grid_.world(), y.p, static_cast<size_t>(y.rows * y.cols), ncclFloat32,
                         Category::Reduce, words(y), ms_);
@@ -243,6 +243,22 @@ class TrainerRows final : public Trainer {
   }
 
   void begin_epoch() override { epoch_exchanges_ = 0; }
+
+  void check_async() override {
+    // Report both records: the comm world's and the panel exchange's.
+    std::string msg;
+    try {
+      Trainer::check_async();
+    } catch (const NcclError& e) {
+      msg = e.what();
+    }
+    try {
+      if (p2p_ok_) p2p_.check();
+    } catch (const NcclError& e) {
+      msg += (msg.empty() ? "" : "; ") + std::string(e.what());
+    }
+    if (!msg.empty()) throw NcclError(msg);
+  }
 
  private:
   bool one_d() const { return grid_.kind() == GridKind::Row1D; }
@@ -412,7 +428,7 @@ class TrainerRows final : public Trainer {
       spmm(parts[static_cast<size_t>(q)], panel, out, idx > 0, epi);
       if (comm) CG_CUDA(cudaEventRecord(ev_free_[b], cs_));
     }
-    if (idx == 0) CG_CUDA(cudaMemsetAsync(out.p, 0, out.rows * out.ld * sizeof(float), cs_));
+    if (idx == 0) kern::zero_bytes(out.p, out.rows * out.ld * sizeof(float), cs_);
   }
 
   // Activation of a finished pre-activation tile: ReLU, or the fused

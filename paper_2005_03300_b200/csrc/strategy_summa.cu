@@ -87,14 +87,9 @@ class TrainerSumma final : public Trainer {
           sp.col.resize(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
           sp.vals.resize(static_cast<size_t>(std::max<int64_t>(nnz, 1)));
           if (aroot == rank_) {
-            CG_CUDA(cudaMemcpyAsync(sp.row_ptr.get(), local.row_ptr.get(), (sh[0] + 1) * sizeof(int64_t),
-                                    cudaMemcpyDeviceToDevice, ms_));
-            if (nnz) {
-              CG_CUDA(cudaMemcpyAsync(sp.col.get(), local.col_idx.get(), nnz * sizeof(int32_t),
-                                      cudaMemcpyDeviceToDevice, ms_));
-              CG_CUDA(cudaMemcpyAsync(sp.vals.get(), local.vals.get(), nnz * sizeof(float),
-                                      cudaMemcpyDeviceToDevice, ms_));
-            }
+            kern::copy_bytes(sp.row_ptr.get(), local.row_ptr.get(), (sh[0] + 1) * sizeof(int64_t), ms_);
+            kern::copy_bytes(sp.col.get(), local.col_idx.get(), nnz * sizeof(int32_t), ms_);
+            kern::copy_bytes(sp.vals.get(), local.vals.get(), nnz * sizeof(float), ms_);
           }
           comm_->bcast_csr(grid_.row_group(rank_), aroot, sp.row_ptr.get(), sh[0], sp.col.get(),
                            sp.vals.get(), nnz, Category::SBcast, ms_);
@@ -119,7 +114,7 @@ class TrainerSumma final : public Trainer {
     redbuf_.alloc(static_cast<int64_t>(side()) * sub_step, fcols);
     strip_.alloc(fcols, fcols, fcols);
     gather_.alloc(side() * sub_step, fcols, fcols);
-    CG_CUDA(cudaDeviceSynchronize());
+    settle();
   }
 
   void forward_layer(int l) override {
@@ -294,7 +289,7 @@ class TrainerSumma final : public Trainer {
       release_buffer(b);
     }
     if (total_calls == 0) {
-      CG_CUDA(cudaMemsetAsync(dst.p, 0, dst.rows * dst.ld * sizeof(float), cs_));
+      kern::zero_bytes(dst.p, dst.rows * dst.ld * sizeof(float), cs_);
       if (relu) kern::relu(dst.p, dst.rows, static_cast<int>(dst.cols), dst.ld, relu_out.p, relu_out.ld, cs_);
     }
   }

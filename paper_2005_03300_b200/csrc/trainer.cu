@@ -1,12 +1,15 @@
 // Trainer base: tiles, weights, streams, shared GEMM/SpMM plumbing, and the
 // device GraphDataset constructors.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 
 #include "kernels.cuh"
 #include "rng.hpp"
+
 #include "trainer.hpp"
 
 namespace cagnet {
@@ -220,11 +223,17 @@ Trainer::Trainer(const DeviceDataset& data, std::vector<int64_t> dims, const dou
   require(rank >= 0 && rank < grid_.ranks(), "trainer: rank outside the grid");
   CG_CUDA(cudaSetDevice(device_));
   CG_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+  comm_ = std::make_unique<Comm>(grid_, rank, id);
   // The comm stream runs at the highest priority: its NCCL / peer-push
   // kernels then get SM slots as soon as CTAs of a running SpMM retire
   // instead of queueing behind the SpMM's whole grid (measured: SUMMA stage
   // broadcasts otherwise start only after the previous stage's SpMM ends).
-  {
+  // CAGNET_LOCAL_STREAMS=1 gives each rank of an in-process world a single
+  // stream (device order = host issue order; a debugging aid).
+  const char* ls = std::getenv("CAGNET_LOCAL_STREAMS");
+  if (comm_->is_local() && ls && std::atoi(ls) == 1) {
+    ms_ = cs_;
+  } else {
     int lo = 0, hi = 0;
     CG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CG_CUDA(cudaStreamCreateWithPriority(&ms_, cudaStreamNonBlocking, hi));
@@ -237,7 +246,6 @@ Trainer::Trainer(const DeviceDataset& data, std::vector<int64_t> dims, const dou
   }
   CG_CUDA(cudaEventCreate(&ev_t0_));
   CG_CUDA(cudaEventCreate(&ev_t1_));
-  comm_ = std::make_unique<Comm>(grid_, rank, id);
 
   const int L = num_layers();
   W_.resize(static_cast<size_t>(L - 1));
@@ -265,13 +273,13 @@ Trainer::Trainer(const DeviceDataset& data, std::vector<int64_t> dims, const dou
 Trainer::~Trainer() {
   cudaSetDevice(device_);
   if (cs_) cudaStreamSynchronize(cs_);
-  if (ms_) cudaStreamSynchronize(ms_);
+  if (ms_ && ms_ != cs_) cudaStreamSynchronize(ms_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   comm_.reset();
   for (cudaEvent_t e : {ev_cs_, ev_ms_, ev_t0_, ev_t1_, ev_ready_[0], ev_ready_[1], ev_free_[0], ev_free_[1]})
     if (e) cudaEventDestroy(e);
+  if (ms_ && ms_ != cs_) cudaStreamDestroy(ms_);
   if (cs_) cudaStreamDestroy(cs_);
-  if (ms_) cudaStreamDestroy(ms_);
 }
 
 const int2* Trainer::colval(const int32_t* ci, const float* v, int64_t nnz) {
@@ -659,6 +667,9 @@ void Trainer::epoch() {
     // (NCCL, peer pushes) keep their priority inside the replayed graph.
     CG_CUDA(cudaGraphInstantiate(&graph_exec_, g, cudaGraphInstantiateFlagUseNodePriority));
     CG_CUDA(cudaGraphDestroy(g));
+    // In-process world: every rank instantiates before any replays, so a
+    // replayed wait never targets a peer still inside its capture.
+    comm_->local_barrier();
     comm_->snapshot(ledger_after_);  // the capture metered this epoch once
     graph_kernels_ = launch_counter().load() - k0;
   } else {
@@ -697,10 +708,29 @@ double Trainer::last_loss() {
   return losses_host_.empty() ? 0.0 : losses_host_.back();
 }
 
+void Trainer::settle() {
+  CG_CUDA(cudaStreamSynchronize(nullptr));
+  sync();
+}
+
 void Trainer::sync() {
   CG_CUDA(cudaSetDevice(device_));
-  CG_CUDA(cudaStreamSynchronize(ms_));
-  CG_CUDA(cudaStreamSynchronize(cs_));
+  const cudaStream_t streams[2] = {ms_, ms_ == cs_ ? nullptr : cs_};
+  for (cudaStream_t s : streams) {
+    if (!s) continue;  // one stream per rank (in-process world)
+    // Poll instead of blocking: a failed peer surfaces as an NCCL async
+    // error or a recorded wait timeout, not as a hang.
+    int spins = 0;
+    for (;;) {
+      const cudaError_t e = cudaStreamQuery(s);
+      if (e == cudaSuccess) break;
+      if (e != cudaErrorNotReady) CG_CUDA(e);
+      // Busy-poll the first ~thousand queries (short epochs), then back off.
+      if (++spins % 1024 == 0) check_async();
+      if (spins > 1024) std::this_thread::sleep_for(std::chrono::microseconds(100));
+    }
+  }
+  check_async();
 }
 
 namespace {

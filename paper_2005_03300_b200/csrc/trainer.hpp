@@ -104,7 +104,11 @@ class Trainer {
     flush_losses();
     return losses_host_;
   }
+  // Waits for both streams, polling for asynchronous communication failures
+  // (NCCL async errors, timed-out device waits) meanwhile; throws NcclError.
   void sync();
+  // Raises the recorded asynchronous communication failure, if any.
+  virtual void check_async() { comm_->check_async(); }
 
   // Readback helpers (host fp32, dense ld = cols).
   void h_tile(int layer, float* out) const;
@@ -183,6 +187,10 @@ class Trainer {
   virtual void begin_epoch() {}
   // --- helpers shared by the strategies ---
   void init_tiles();  // h/z/g tile shapes from tile_rows/tile_cols, labels, H0
+  // End of distribute(): setup work on the legacy stream (zeroing memsets)
+  // and both trainer streams complete.  Not a device-wide synchronisation:
+  // ranks sharing one GPU must never wait for each other's streams.
+  void settle();
   void ms_after_cs();
   void cs_after_ms();
   // out (+)= a · h.  With epi (f <= 32, acc = false, one pass) the layer's

@@ -2,6 +2,13 @@ import ctypes
 import os
 import sys
 
+# The in-process world runs up to 8 ranks x 2 streams on one GPU: give every
+# stream its own hardware work queue (set before any CUDA context exists).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# Lazy module loading may wait for a context synchronisation that a spinning
+# peer rank on the same GPU never allows (see capi.cu cagnet_env_defaults).
+os.environ.setdefault("CUDA_MODULE_DATA_LOADING", "EAGER")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -49,7 +56,27 @@ def cg():
 
 @pytest.fixture
 def need_gpus():
+    """need_gpus(P): a P-rank run needs one GPU (the in-process world runs
+    every rank on it when there are fewer than P GPUs)."""
     def _need(k: int):
-        if DEVICES < k:
-            pytest.skip(f"needs {k} GPUs, found {DEVICES}")
+        if DEVICES < 1:
+            pytest.skip("needs a GPU")
+    return _need
+
+
+def pytest_generate_tests(metafunc):
+    """Multi-rank tests take a `comm` backend: "local" (every rank on one GPU,
+    the in-process world) always; "nccl" (one GPU per rank) only where the
+    node has several GPUs (per-test rank counts are checked by need_comm)."""
+    if "comm" in metafunc.fixturenames:
+        metafunc.parametrize("comm", ["local", "nccl"] if DEVICES >= 2 else ["local"])
+
+
+@pytest.fixture
+def need_comm():
+    def _need(comm: str, k: int):
+        if DEVICES < 1:
+            pytest.skip("needs a GPU")
+        if comm == "nccl" and DEVICES < k:
+            pytest.skip(f"NCCL backend needs {k} GPUs, found {DEVICES}")
     return _need

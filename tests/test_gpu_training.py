@@ -179,15 +179,15 @@ DIST = {  # name -> (kind, P, repl, block, n, dims)   (tests/golden/make_golden.
 @pytest.mark.parametrize("kind,P,repl", [("1d", 2, 1), ("1.5d", 4, 2), ("1d", 4, 1), ("2d", 4, 1),
                                         ("3d", 8, 1)])
 @pytest.mark.parametrize("dims", [[24, 8, 6], [24, 6, 8, 10]])
-def test_distributed_reassociated(cg, orc, need_gpus, kind, P, repl, dims):
+def test_distributed_reassociated(cg, orc, need_comm, comm, kind, P, repl, dims):
     """Narrow-first propagation on every strategy (2D/3D: row-group GEMM
     first, then SUMMA propagation of the f_out-wide U tiles); the second dims
     have widening layers (Y = Tᵀ G, G_prev = A (G Wᵀ) ⊙ relu′), one of them
     in the middle of the network."""
-    need_gpus(P)
+    need_comm(comm, P)
     model = cg.init_glorot(dims, 5, 0.5)
     out = cg.run_distributed(lambda dev: cg.generate_dataset(50, 6.0, 24, dims[-1], 2, 3, 4, device=dev),
-                             model, cg.Strategy(kind, P, repl, reassociate=True), 3)
+                             model, cg.Strategy(kind, P, repl, reassociate=True), 3, comm=comm)
     od = orc.generate_dataset(50, 6.0, 24, dims[-1], 2, 3, 4)
     losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.5, 3)
     res = dict(losses=out.losses, h_final=out.h_final, y=out.y_final, g=out.g_final,
@@ -199,20 +199,20 @@ def test_distributed_reassociated(cg, orc, need_gpus, kind, P, repl, dims):
 @pytest.mark.parametrize("P", [2, 4])
 @pytest.mark.parametrize("p2p,overlap,pipeline", [(True, True, False), (True, False, False),
                                                   (True, False, True), (False, False, False)])
-def test_1d_exchange_paths(cg, orc, need_gpus, monkeypatch, P, p2p, overlap, pipeline):
+def test_1d_exchange_paths(cg, orc, need_comm, comm, monkeypatch, P, p2p, overlap, pipeline):
     """1D stage exchanges: NVLink peer-memory pushes with the own-block SpMM
     overlapped, peer memory in one SpMM after the exchange, the pipelined form
     (per-destination pushes, per-block SpMMs as slots land; forced here by a
     zero slot threshold), and the NCCL all-gather — same numbers as the serial
     oracle over graph-replayed epochs (the flag protocol runs inside the
     replays)."""
-    need_gpus(P)
+    need_comm(comm, P)
     monkeypatch.setenv("CAGNET_PIPELINE_MIN_MB", "0" if pipeline else "1e9")
     dims = [24, 8, 8, 6]
     model = cg.init_glorot(dims, 5, 0.5)
     strat = cg.Strategy("1d", P, 1, reassociate=True, p2p=p2p, overlap=overlap)
     out = cg.run_distributed(lambda dev: cg.generate_dataset(300, 12.0, 24, 6, 2, 3, 4, device=dev),
-                             model, strat, 5)
+                             model, strat, 5, comm=comm)
     od = orc.generate_dataset(300, 12.0, 24, 6, 2, 3, 4)
     losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.5, 5)
     res = dict(losses=out.losses, h_final=out.h_final, y=out.y_final, g=out.g_final,
@@ -222,16 +222,16 @@ def test_1d_exchange_paths(cg, orc, need_gpus, monkeypatch, P, p2p, overlap, pip
 
 @pytest.mark.multigpu
 @pytest.mark.parametrize("P", [2, 4])
-def test_1d_odd_exchange_count(cg, orc, need_gpus, P):
+def test_1d_odd_exchange_count(cg, orc, need_comm, comm, P):
     """A widening first layer skips the last backward SpMM, leaving an odd
     number of peer-memory exchanges per epoch; the trainer evens it out with a
     flag-only exchange so the replayed epoch graph never reuses the buffer of
     the exchange before it (many replays, result still matches the oracle)."""
-    need_gpus(P)
+    need_comm(comm, P)
     dims = [8, 16, 4]
     model = cg.init_glorot(dims, 5, 0.5)
     out = cg.run_distributed(lambda dev: cg.generate_dataset(400, 12.0, 8, 4, 2, 3, 4, device=dev),
-                             model, cg.Strategy("1d", P, 1, reassociate=True), 12)
+                             model, cg.Strategy("1d", P, 1, reassociate=True), 12, comm=comm)
     od = orc.generate_dataset(400, 12.0, 8, 4, 2, 3, 4)
     losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.5, 12)
     res = dict(losses=out.losses, h_final=out.h_final, y=out.y_final, g=out.g_final,
@@ -241,17 +241,17 @@ def test_1d_odd_exchange_count(cg, orc, need_gpus, P):
 
 @pytest.mark.multigpu
 @pytest.mark.parametrize("kind,P", [("2d", 4), ("3d", 8)])
-def test_resident_sparse_tiles(cg, need_gpus, kind, P):
+def test_resident_sparse_tiles(cg, need_comm, comm, kind, P):
     """SUMMA with the sparse tiles kept resident after distribute(): the same
     numbers bit for bit, and no per-epoch sparse broadcast in the ledger."""
-    need_gpus(P)
+    need_comm(comm, P)
     dims = [8, 6, 4]
     model = cg.init_glorot(dims, 14, 0.5)
     outs = []
     for resident in (False, True):
         outs.append(cg.run_distributed(
             lambda dev: cg.generate_dataset(18, 4.0, dims[0], dims[-1], 11, 12, 13, device=dev),
-            model, cg.Strategy(kind, P, 1, 0, resident_sparse=resident), 3))
+            model, cg.Strategy(kind, P, 1, 0, resident_sparse=resident), 3, comm=comm))
     a, b = outs
     assert np.array_equal(a.losses, b.losses)
     assert np.array_equal(a.h_final, b.h_final)
@@ -264,15 +264,15 @@ def test_resident_sparse_tiles(cg, need_gpus, kind, P):
 
 @pytest.mark.multigpu
 @pytest.mark.parametrize("name", list(DIST))
-def test_distributed_matches_reference(cg, need_gpus, name):
+def test_distributed_matches_reference(cg, need_comm, comm, name):
     kind, P, repl, block, n, dims = DIST[name]
-    need_gpus(P)
+    need_comm(comm, P)
     gd = np.load(os.path.join(GOLD, "reference_dist.npz"))
     model = cg.init_glorot(dims, 14, 0.5)
     # The reference's own communication schedule (per-stage sparse broadcasts).
     strat = cg.Strategy(kind, P, repl, block, resident_sparse=False)
     out = cg.run_distributed(lambda dev: cg.generate_dataset(n, 4.0, dims[0], dims[-1], 11, 12, 13,
-                                                             device=dev), model, strat, 3)
+                                                             device=dev), model, strat, 3, comm=comm)
     L = len(dims)
     res = dict(losses=out.losses, h_final=out.h_final, y=out.y_final, g=out.g_final,
                w=out.model.weights)
