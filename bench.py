@@ -29,19 +29,18 @@ METRIC = "GCN epoch time (ms) at 1/2/4/8 B200 per 1D/1.5D/2D/3D; SpMM GB/s vs HB
 REDDIT_N, REDDIT_E = 232965, 114848857
 CONFIGS = {
     # BASELINE.json configs[0]
-    "config1": dict(n=4096, degree=16.0, dims=[128, 16, 8], generator="reference", sample_div=1,
+    "config1": dict(n=4096, degree=16.0, dims=[128, 16, 8], generator="reference",
                     label="ER n=4096 d=16, 2-layer GCN {128,16,8}"),
     # configs[1]/[2]: Reddit-shaped, the bit-exact reference ER generator on the GPU
     "reddit": dict(n=REDDIT_N, degree=REDDIT_E / REDDIT_N, dims=[602, 16, 16, 41],
-                   generator="reference", sample_div=16,
+                   generator="reference",
                    label="Reddit-shaped ER n=232965 nnz=115M f=602, 3-layer GCN {602,16,16,41}"),
     # configs[3]: Amazon-shaped, O(nnz) ER-shaped generator
     "amazon": dict(n=14249639, degree=230788269 / 14249639, dims=[300, 16, 16, 24],
-                   generator="skip", sample_div=512,
+                   generator="skip",
                    label="Amazon-shaped ER n=14.2M nnz=245M f=300, 3-layer GCN {300,16,16,24}"),
     # configs[4]: Protein-shaped (BASELINE's 1.3B edges)
     "protein": dict(n=8745542, degree=1.3e9 / 8745542, dims=[128, 16, 16, 256], generator="skip",
-                    sample_div=256,
                     label="Protein-shaped ER n=8.7M nnz=1.3B f=128, 3-layer GCN {128,16,16,256}"),
 }
 SEEDS = dict(seed_graph=1, seed_features=2, seed_labels=3)
@@ -68,10 +67,6 @@ def parse():
                    help="fused SpMM row epilogues: 0 off, 1 ReLU/relu' (default), 2 + dense W")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--sample-div", type=int, default=0,
-                   help="CPU sample = the config's graph with n/div vertices, same degree "
-                        "(default per config: the reference's O(n^2) ER generator must stay "
-                        "within seconds)")
     return p.parse_args()
 
 
@@ -145,31 +140,38 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle/_ref = the unmodified reference sources) on a sample
+# CPU reference (oracle/_ref = the unmodified reference sources), full size
 # ---------------------------------------------------------------------------
-def reference_sample(cfg, div, ranks, epochs, warmup):
-    """Times the reference's run_distributed (1D, `ranks` threads) on the
-    config's graph scaled to n/div vertices at the same average degree and
-    feature widths; returns (per-epoch seconds list, sample dict)."""
+def ref_threads() -> int:
+    return max(1, min(os.cpu_count() or 1, 64))
+
+
+def reference_session(cfg, ranks):
+    """The reference's run_distributed (dist_common.cpp:205-222), 1D with
+    `ranks` rank threads, on the config's FULL graph: the raw ER graph is the
+    reference generator's (csr.cpp:195-218) output, produced on all host
+    threads by the oracle's jump-ahead restatement (bit-identical, pinned in
+    tests/test_oracle.py) because the reference's own loop is single-threaded
+    (~8 min for Reddit); features / labels / make_dataset / distribute are
+    the reference's own code.  Returns (session, setup dict)."""
     import oracle
-    ref = oracle.Ref()
-    n_s = max(cfg["n"] // div, 64)
-    dims = cfg["dims"]
+    orc, ref = oracle.Oracle(), oracle.Ref()
+    n, dims = cfg["n"], cfg["dims"]
     t0 = time.perf_counter()
-    data = ref.dataset(n_s, min(cfg["degree"], n_s - 1), dims[0], dims[-1], 1, 2, 3)
-    gen_s = time.perf_counter() - t0
+    raw = orc.er_generate_mt(n, cfg["degree"], SEEDS["seed_graph"], ref_threads())
+    t1 = time.perf_counter()
+    x = orc.random_features(n, dims[0], SEEDS["seed_features"])
+    y = orc.random_labels(n, dims[-1], SEEDS["seed_labels"])
+    data = ref.dataset_make(raw, x, y, dims[-1])
+    del x, raw
+    t2 = time.perf_counter()
     model = ref.model(dims, SEED_W, LR)
-    times = []
-    for e in range(warmup + epochs):
-        res = ref.distributed(data, model, "1d", ranks, 1, 0, epochs=1)
-        if e >= warmup:
-            times.append(res.seconds)
-    sample = dict(n=n_s, nnz=int(data.nnz), dims=dims, ranks=ranks, gen_s=round(gen_s, 2))
-    return times, sample
-
-
-def full_nnz(cfg):
-    return cfg["n"] * cfg["degree"] + cfg["n"]  # E[raw nnz] + self loops
+    sess = ref.session(data, model, "1d", ranks)
+    t3 = time.perf_counter()
+    setup = {"er_threads_s": round(t1 - t0, 1), "make_dataset_s": round(t2 - t1, 1),
+             "distribute_s": round(t3 - t2, 1), "nnz": int(data.nnz)}
+    sess._keep = (data, model)
+    return sess, setup
 
 
 def run_reference(args, cfg):
@@ -183,13 +185,20 @@ def run_reference(args, cfg):
     except Exception as e:  # pragma: no cover
         print(json.dumps({"impl": "reference", "unavailable": str(e)}))
         return
-    threads = max(1, min(os.cpu_count() or 1, 16))
-    times, sample = reference_sample(cfg, args.sample_div, threads, args.steps, args.warmup)
-    scale = full_nnz(cfg) / sample["nnz"]
-    ms = statistics.median(times) * 1e3 * scale
-    desc = (f"reference run_distributed 1D P={threads} threads on n={sample['n']} "
-            f"(nnz={sample['nnz']}, same degree and dims), epoch time x{scale:.1f} "
-            f"(linear in nnz) to the full graph")
+    if cfg["generator"] != "reference":
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "the reference's O(n^2) ER generator and fp64 dense features do not "
+                          "scale to this config (SURVEY 8d); run --config reddit"}))
+        return
+    threads = ref_threads()
+    sess, setup = reference_session(cfg, threads)
+    for _ in range(args.warmup):
+        sess.epoch()
+    times = [sess.epoch() for _ in range(args.steps)]
+    ms = statistics.mean(times) * 1e3
+    desc = (f"reference run_distributed 1D P={threads} rank threads on the full graph "
+            f"(n={cfg['n']}, nnz={setup['nnz']}), {args.steps} timed epochs after "
+            f"{args.warmup} warm-up epochs, mean epoch wall time")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -200,6 +209,8 @@ def run_reference(args, cfg):
                          "kind": "reference", "sample": desc},
         "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "epoch_ms": [round(t * 1e3, 1) for t in times],
+        "setup_s": setup,
     }
     print(json.dumps(line))
 
@@ -414,15 +425,17 @@ def run_ours(args, cfg):
         return
 
     cpu = None
-    if N == 1 and not args.no_cpu_baseline:
+    if N == 1 and not args.no_cpu_baseline and cfg["generator"] == "reference":
         try:
-            times, sample = reference_sample(cfg, args.sample_div, 1, 1, 0)
-            scale = full_nnz(cfg) / sample["nnz"]
-            cpu = {"value": round(times[0] * 1e3 * scale, 1), "unit": "ms", "cores": 1,
+            threads = ref_threads()
+            sess, setup = reference_session(cfg, threads)
+            sec = sess.epoch()
+            cpu = {"value": round(sec * 1e3, 1), "unit": "ms", "cores": threads,
                    "kind": "reference",
-                   "sample": f"reference run_distributed 1D P=1 (serial) on n={sample['n']} "
-                             f"nnz={sample['nnz']} (same degree/dims), one epoch, x{scale:.1f} "
-                             f"linear-in-nnz extrapolation to the full graph"}
+                   "sample": f"one epoch of the reference run_distributed 1D P={threads} rank "
+                             f"threads on the full graph (n={cfg['n']}, nnz={setup['nnz']}); "
+                             f"no extrapolation", "setup_s": setup}
+            del sess
         except Exception as e:
             cpu = {"value": None, "unit": "ms", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -464,8 +477,6 @@ def run_ours(args, cfg):
 def main():
     args = parse()
     cfg = CONFIGS[args.config]
-    if not args.sample_div:
-        args.sample_div = cfg.get("sample_div", 16)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

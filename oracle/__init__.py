@@ -67,6 +67,14 @@ class Oracle:
         L = self.lib = C.CDLL(path)
         L.orc_er_generate.restype = C.c_int64
         L.orc_er_generate.argtypes = [C.c_int64, C.c_double, C.c_uint64, _i64p, C.c_void_p]
+        L.orc_er_generate_mt.restype = C.c_int64
+        L.orc_er_generate_mt.argtypes = [C.c_int64, C.c_double, C.c_uint64, C.c_int, _i64p,
+                                         C.POINTER(C.c_void_p)]
+        L.orc_free.argtypes = [C.c_void_p]
+        L.orc_rng_jump.argtypes = [C.c_void_p, C.c_uint64]
+        L.orc_rng_seed.argtypes = [C.c_void_p, C.c_uint64]
+        L.orc_rng_next.restype = C.c_uint64
+        L.orc_rng_next.argtypes = [C.c_void_p]
         L.orc_from_edge_list.restype = C.c_int64
         L.orc_from_edge_list.argtypes = [C.c_int64, C.c_int64, _i64p, _i64p, C.c_int, _i64p, C.c_void_p]
         L.orc_normalize.restype = C.c_int64
@@ -99,6 +107,26 @@ class Oracle:
         ci = np.zeros(max(nnz, 1), np.int64)
         self.lib.orc_er_generate(n, degree, seed, rp, ci.ctypes.data)
         return CSR(n, n, rp, ci[:nnz], np.ones(nnz))
+
+    def er_generate_mt(self, n: int, degree: float, seed: int, threads: int = 0) -> CSR:
+        """csr.cpp:195-218 on host threads (row sub-streams by GF(2) jump-ahead),
+        bit-identical to er_generate."""
+        threads = threads or (os.cpu_count() or 1)
+        rp = np.zeros(n + 1, np.int64)
+        buf = C.c_void_p()
+        nnz = self.lib.orc_er_generate_mt(n, degree, seed, threads, rp, C.byref(buf))
+        if nnz < 0:
+            raise ValueError("er_generate_mt failed")
+        ci = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_int64)), shape=(max(nnz, 1),))[:nnz].copy()
+        self.lib.orc_free(buf)
+        return CSR(n, n, rp, ci, np.ones(nnz))
+
+    def rng_draws(self, seed: int, skip: int, count: int) -> np.ndarray:
+        """`count` raw draws of Rng(seed) after jumping `skip` draws ahead."""
+        st = (C.c_uint64 * 4)()
+        self.lib.orc_rng_seed(st, seed)
+        self.lib.orc_rng_jump(st, skip)
+        return np.array([self.lib.orc_rng_next(st) for _ in range(count)], np.uint64)
 
     def from_edge_list(self, n, u, v, undirected=False) -> CSR:
         u = np.ascontiguousarray(u, np.int64)
@@ -273,6 +301,13 @@ class Ref:
         L.ref_serial_run.argtypes = [vp, vp, C.c_int]
         L.ref_dist_run.restype = vp
         L.ref_dist_run.argtypes = [vp, vp] + [C.c_int] * 6
+        L.ref_session_create.restype = vp
+        L.ref_session_create.argtypes = [vp, vp] + [C.c_int] * 5
+        L.ref_session_epoch.restype = C.c_double
+        L.ref_session_epoch.argtypes = [vp]
+        L.ref_session_outcome.restype = vp
+        L.ref_session_outcome.argtypes = [vp]
+        L.ref_session_free.argtypes = [vp]
         L.ref_result_free.argtypes = [vp]
         L.ref_result_seconds.restype = C.c_double
         L.ref_result_seconds.argtypes = [vp]
@@ -328,6 +363,11 @@ class Ref:
         h = self.lib.ref_dist_run(data.h, model.h, self.KIND[kind], ranks, repl, block, epochs,
                                   sched)
         return RefResult(self, self._check(h), data, model, epochs, ranks=ranks)
+
+    def session(self, data, model, kind, ranks, repl=1, block=0, sched=0):
+        """run_distributed split into distribute() once + one call per epoch."""
+        return RefSession(self, self._check(self.lib.ref_session_create(
+            data.h, model.h, self.KIND[kind], ranks, repl, block, sched)), data, model, ranks)
 
     def distribute(self, data, model, kind, ranks, repl=1, block=0):
         h = self.lib.ref_trainer_distribute(data.h, model.h, self.KIND[kind], ranks, repl, block)
@@ -422,6 +462,31 @@ class RefResult:
                     L.ref_result_ledger(h, c, r, buf)
                     self.ledger[c, r] = buf
         L.ref_result_free(h)
+
+
+class RefSession:
+    def __init__(self, ref, h, data, model, ranks):
+        self.ref, self.h, self.data, self.model, self.ranks = ref, h, data, model, ranks
+        self.epochs = 0
+
+    def epoch(self) -> float:
+        sec = self.ref.lib.ref_session_epoch(self.h)
+        if sec < 0:
+            raise RuntimeError(self.ref.lib.ref_last_error().decode())
+        self.epochs += 1
+        return sec
+
+    def outcome(self) -> "RefResult":
+        h = self.ref._check(self.ref.lib.ref_session_outcome(self.h))
+        return RefResult(self.ref, h, self.data, self.model, self.epochs, ranks=self.ranks)
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.ref.lib.ref_session_free(self.h)
+        except Exception:
+            pass
+        self.h = None
 
 
 class RefTrainer:

@@ -2,6 +2,7 @@
 #include "cagnet_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -83,6 +84,135 @@ int64_t orc_er_generate(int64_t n, double degree, uint64_t seed, int64_t* row_pt
   }
   return nnz;
 }
+
+/* ---- GF(2) jump-ahead of the xoshiro256** state update (rng.hpp:45-57) ---- */
+/* A 256 x 256 bit matrix stored as the images of the 256 basis states. */
+typedef struct { uint64_t col[256][4]; } gf2mat;
+
+static void state_step(uint64_t* s) { /* the update of orc_rng_next without the output */
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = rotl64(s[3], 45);
+}
+
+static void gf2_apply(const gf2mat* m, const uint64_t* v, uint64_t* out) {
+  uint64_t r[4] = {0, 0, 0, 0};
+  for (int j = 0; j < 256; ++j)
+    if ((v[j >> 6] >> (j & 63)) & 1) {
+      r[0] ^= m->col[j][0];
+      r[1] ^= m->col[j][1];
+      r[2] ^= m->col[j][2];
+      r[3] ^= m->col[j][3];
+    }
+  memcpy(out, r, sizeof(r));
+}
+
+static gf2mat* jump_table(void) { /* T^(2^i), i = 0..63, built once */
+  static gf2mat* tab = NULL;
+  if (tab) return tab;
+  gf2mat* t = (gf2mat*)malloc(64 * sizeof(gf2mat));
+  for (int j = 0; j < 256; ++j) {
+    uint64_t v[4] = {0, 0, 0, 0};
+    v[j >> 6] = 1ULL << (j & 63);
+    state_step(v);
+    memcpy(t[0].col[j], v, sizeof(v));
+  }
+  for (int i = 1; i < 64; ++i)
+    for (int j = 0; j < 256; ++j) gf2_apply(&t[i - 1], t[i - 1].col[j], t[i].col[j]);
+  tab = t;
+  return tab;
+}
+
+void orc_rng_jump(orc_rng* r, uint64_t draws) {
+  const gf2mat* t = jump_table();
+  for (int i = 0; i < 64; ++i)
+    if ((draws >> i) & 1) gf2_apply(&t[i], r->s, r->s);
+}
+
+typedef struct {
+  int64_t n, chunk_rows, nchunks;
+  double p;
+  uint64_t seed;
+  int64_t* row_cnt;   /* n counts */
+  int64_t** chunk_cols;
+  int64_t* chunk_nnz;
+  volatile int64_t next;
+} er_job;
+
+static void* er_worker(void* arg) {
+  er_job* job = (er_job*)arg;
+  for (;;) {
+    const int64_t c = __atomic_fetch_add(&job->next, 1, __ATOMIC_RELAXED);
+    if (c >= job->nchunks) break;
+    const int64_t u0 = c * job->chunk_rows;
+    int64_t u1 = u0 + job->chunk_rows;
+    if (u1 > job->n) u1 = job->n;
+    orc_rng r;
+    orc_rng_seed(&r, job->seed);
+    orc_rng_jump(&r, (uint64_t)u0 * (uint64_t)(job->n - 1));
+    int64_t cap = 1024, cnt = 0;
+    int64_t* cols = (int64_t*)malloc((size_t)cap * sizeof(int64_t));
+    for (int64_t u = u0; u < u1; ++u) {
+      int64_t deg = 0;
+      for (int64_t v = 0; v < job->n; ++v) {
+        if (u == v) continue;
+        if (orc_rng_double(&r) < job->p) {
+          if (cnt == cap) {
+            cap *= 2;
+            cols = (int64_t*)realloc(cols, (size_t)cap * sizeof(int64_t));
+          }
+          cols[cnt++] = v;
+          ++deg;
+        }
+      }
+      job->row_cnt[u] = deg;
+    }
+    job->chunk_cols[c] = cols;
+    job->chunk_nnz[c] = cnt;
+  }
+  return NULL;
+}
+
+int64_t orc_er_generate_mt(int64_t n, double degree, uint64_t seed, int threads,
+                           int64_t* row_ptr, int64_t** col_idx) {
+  if (n <= 0 || threads <= 0) return -1;
+  er_job job;
+  job.n = n;
+  job.p = degree / (double)n;
+  job.seed = seed;
+  job.chunk_rows = n / (64 * threads) + 1;
+  job.nchunks = (n + job.chunk_rows - 1) / job.chunk_rows;
+  job.row_cnt = (int64_t*)calloc((size_t)n, sizeof(int64_t));
+  job.chunk_cols = (int64_t**)calloc((size_t)job.nchunks, sizeof(int64_t*));
+  job.chunk_nnz = (int64_t*)calloc((size_t)job.nchunks, sizeof(int64_t));
+  job.next = 0;
+  jump_table();
+  pthread_t* tid = (pthread_t*)malloc((size_t)threads * sizeof(pthread_t));
+  for (int t = 0; t < threads; ++t) pthread_create(&tid[t], NULL, er_worker, &job);
+  for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+  free(tid);
+  row_ptr[0] = 0;
+  for (int64_t u = 0; u < n; ++u) row_ptr[u + 1] = row_ptr[u] + job.row_cnt[u];
+  const int64_t nnz = row_ptr[n];
+  int64_t* ci = (int64_t*)malloc((size_t)(nnz > 0 ? nnz : 1) * sizeof(int64_t));
+  int64_t off = 0;
+  for (int64_t c = 0; c < job.nchunks; ++c) {
+    memcpy(ci + off, job.chunk_cols[c], (size_t)job.chunk_nnz[c] * sizeof(int64_t));
+    off += job.chunk_nnz[c];
+    free(job.chunk_cols[c]);
+  }
+  free(job.chunk_cols);
+  free(job.chunk_nnz);
+  free(job.row_cnt);
+  *col_idx = ci;
+  return nnz;
+}
+
+void orc_free(void* p) { free(p); }
 
 /* ---- csr.cpp:59-92 -------------------------------------------------------- */
 typedef struct { int64_t r, c; } pair64;

@@ -35,6 +35,17 @@ void orc_block_range(int64_t n, int parts, int idx, int64_t* begin, int64_t* end
 int64_t orc_er_generate(int64_t n, double degree, uint64_t seed, int64_t* row_ptr,
                         int64_t* col_idx);
 
+/* csr.cpp:195-218 on `threads` host threads, bit-identical to orc_er_generate:
+ * row u of the reference loop consumes exactly n-1 draws, so a chunk of rows
+ * starting at u0 starts its sub-stream at draw u0*(n-1), reached by GF(2)
+ * jump-ahead of the (linear) xoshiro256** state update.  Allocates *col_idx
+ * (malloc, caller frees); row_ptr has n+1 entries.  Returns nnz or -1. */
+int64_t orc_er_generate_mt(int64_t n, double degree, uint64_t seed, int threads,
+                           int64_t* row_ptr, int64_t** col_idx);
+void orc_free(void* p);
+/* Jump-ahead of a seeded generator by `draws` draws (used above; exposed for tests). */
+void orc_rng_jump(orc_rng* r, uint64_t draws);
+
 /* csr.cpp:59-92 — from_edge_list (sort + dedup, optional mirroring).  Returns
  * nnz; col_idx == NULL: count only.  Edges are (u[i], v[i]). */
 int64_t orc_from_edge_list(int64_t n, int64_t m, const int64_t* u, const int64_t* v,

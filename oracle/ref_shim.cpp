@@ -226,6 +226,60 @@ void* ref_dist_run(void* data, void* model, int kind, int ranks, int repl, int b
   return r;
 }
 
+// A persistent run_distributed (dist_common.cpp:205-222) split into its
+// steps so bench.py can time warm-up and measured epochs separately:
+// make_trainer + distribute() once, then Trainer::run_epochs(rt, 1) per call
+// (dist_common.cpp:102-108: each call runs every rank's epoch on its own
+// thread, the ledger accumulating), then the assembled DistOutcome fields.
+struct RefSession {
+  std::unique_ptr<Trainer> t;
+  std::unique_ptr<SimRuntime> rt;
+  std::size_t layers = 0;
+};
+void* ref_session_create(void* data, void* model, int kind, int ranks, int repl, int block, int sched) {
+  RefSession* s = nullptr;
+  if (guarded([&] {
+        auto up = std::make_unique<RefSession>();
+        const GnnModel& m = *static_cast<GnnModel*>(model);
+        up->t = make_trainer(*static_cast<GraphDataset*>(data), m, make_strategy(kind, ranks, repl, block));
+        up->t->distribute();
+        up->rt = std::make_unique<SimRuntime>(up->t->grid(), static_cast<Scheduler>(sched));
+        up->layers = m.num_layers();
+        s = up.release();
+      }))
+    return nullptr;
+  return s;
+}
+// One epoch on every rank; returns its wall seconds (< 0 on error).
+double ref_session_epoch(void* sp) {
+  double sec = -1.0;
+  guarded([&] {
+    RefSession& s = *static_cast<RefSession*>(sp);
+    auto t0 = std::chrono::steady_clock::now();
+    s.t->run_epochs(*s.rt, 1);
+    sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+  return sec;
+}
+void* ref_session_outcome(void* sp) {
+  RefResult* r = nullptr;
+  if (guarded([&] {
+        RefSession& s = *static_cast<RefSession*>(sp);
+        auto res = std::make_unique<RefResult>();
+        res->losses = s.t->verified_losses();
+        res->h_final = s.t->assemble_h_final();
+        for (std::size_t i = 0; i + 1 < s.layers; ++i) res->g.push_back(s.t->assemble_g(i));
+        res->y = s.t->verified_y();
+        res->w = s.t->verified_model().weights;
+        res->ledger = s.rt->ledger();
+        res->has_ledger = true;
+        r = res.release();
+      }))
+    return nullptr;
+  return r;
+}
+void ref_session_free(void* s) { delete static_cast<RefSession*>(s); }
+
 void ref_result_free(void* r) { delete static_cast<RefResult*>(r); }
 double ref_result_seconds(void* r) { return static_cast<RefResult*>(r)->seconds; }
 void ref_result_losses(void* r, double* out) {

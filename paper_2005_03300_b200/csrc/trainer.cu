@@ -414,10 +414,9 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const ke
 }
 
 double Trainer::l2_panel_bytes() {
-  static const double v = [] {
-    const char* e = std::getenv("CAGNET_L2_PANEL_MB");
-    return (e ? std::atof(e) : 48.0) * 1048576.0;
-  }();
+  // Read per call (a getenv per SpMM dispatch): tests force the multi-pass path.
+  const char* e = std::getenv("CAGNET_L2_PANEL_MB");
+  const double v = (e ? std::atof(e) : 48.0) * 1048576.0;
   return v > 0 ? v : 1e30;
 }
 

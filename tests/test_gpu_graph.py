@@ -25,6 +25,17 @@ def test_er_generator_bitwise(cg, orc, n, d, seed):
     assert np.all(v == 1.0)
 
 
+def test_er_generator_bitwise_past_2_32_draws(cg, orc):
+    """n = 65,536: rows start at draw offsets up to 4.29e9 (> 2^32), so every
+    high power of the GPU's GF(2) jump-ahead is exercised; compared with the
+    oracle's SEQUENTIAL generator (one stream, no jumps)."""
+    n, d, seed = 65536, 10.0, 17
+    rp, ci, _ = cg.generate_erdos_renyi(n, d, seed).download()
+    o = orc.er_generate(n, d, seed)
+    assert np.array_equal(rp, o.row_ptr)
+    assert np.array_equal(ci, o.col_idx)
+
+
 def test_er_pinned_counts_on_gpu(cg):
     assert cg.generate_erdos_renyi(32, 8.0, 1).nnz == 249
     assert cg.generate_erdos_renyi(64, 8.0, 7).nnz == 495

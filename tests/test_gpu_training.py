@@ -288,3 +288,99 @@ def test_distributed_matches_reference(cg, need_comm, comm, name):
             got = [out.ledger[r][cat][f] for f in ("messages", "words_sent", "words_received",
                                                    "payload_words", "calls")]
             assert got == [int(x) for x in want[ci, r]], (name, r, cat)
+
+
+def distributed_trainers(cg, make_data, model, strat):
+    """P trainers of an in-process world on GPU 0, each created and
+    distributed on its own thread (distribute() holds collectives)."""
+    import threading
+    P = strat.ranks
+    nid = cg.comm_local_id(P, 0) if P > 1 else None
+    datas = [make_data() for _ in range(P)]
+    trainers, errors = [None] * P, []
+
+    def body(r):
+        try:
+            t = cg.Trainer(datas[r], model, strat, r, nid)
+            t.distribute()
+            trainers[r] = t
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+            cg.comm_local_abort(nid, str(e))
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(P)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors
+    return trainers, datas
+
+
+@pytest.mark.parametrize("kind,P,repl", [("1d", 8, 1), ("1.5d", 8, 2), ("2d", 4, 1), ("3d", 8, 1)])
+def test_trainer_parts_match_reference_distribute(cg, ref, kind, P, repl):
+    """Trainer::distribute() of the product (every rank's own a_parts /
+    at_parts, read back through cagnet_trainer_part) against the reference's
+    distribute() (dist_1d.cpp:28-44, dist_15d.cpp:32-47, dist_2d.cpp:41-54,
+    dist_3d.cpp:39-55) on config 1: structure bit-exact, values (float) of
+    the reference's doubles, per-part nnz equal to the committed golden."""
+    gold = np.load(os.path.join(GOLD, "reference_config1.npz"))[f"parts_{kind}_p{P}"]
+    dims = [128, 16, 8]
+    model = cg.init_glorot(dims, 4, 0.5)
+    strat = cg.Strategy(kind, P, repl)
+    trainers, _ = distributed_trainers(
+        cg, lambda: cg.generate_dataset(4096, 16.0, 128, 8, 1, 2, 3, device=0), model, strat)
+    rdata = ref.dataset(4096, 16.0, 128, 8, 1, 2, 3)
+    rt = ref.distribute(rdata, ref.model(dims, 4, 0.5), kind, P, repl)
+    rows = []
+    for r, t in enumerate(trainers):
+        assert t.num_parts() == rt.num_parts(r)
+        for q in range(t.num_parts()):
+            nnz = []
+            for which in (0, 1):
+                rp, ci, v = t.part(which, q).download()
+                want = rt.part(r, which, q)
+                assert np.array_equal(rp, want.row_ptr), (kind, r, q, which)
+                assert np.array_equal(ci, want.col_idx), (kind, r, q, which)
+                assert np.array_equal(v, want.vals.astype(np.float32)), (kind, r, q, which)
+                nnz.append(len(ci))
+            rows.append([r, q] + nnz)
+    assert np.array_equal(np.asarray(rows), gold)
+
+
+@pytest.mark.parametrize("panel_mb,passes", [(0.4, 2), (0.15, 5), (0.06, 12)])
+def test_l2_multipass_spmm_matches_serial(cg, orc, monkeypatch, panel_mb, passes):
+    """L2 column-blocked SpMM (trainer.cu spmm_passes: one pass per column
+    block when the gathered panel exceeds the L2 budget and rows carry >= 64
+    nonzeros): forced to 2 / 5 / 12 passes by shrinking the budget; the
+    reference propagation order keeps the f = 64 SpMM, which blocks."""
+    n, deg, dims = 3000, 150.0, [64, 16, 8]
+    model = cg.init_glorot(dims, 5, 0.5)
+    od = orc.generate_dataset(n, deg, dims[0], dims[-1], 2, 3, 4)
+    losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.5, 2)
+    launches = {}
+    for mb in (1e6, panel_mb):
+        monkeypatch.setenv("CAGNET_L2_PANEL_MB", str(mb))
+        data = cg.generate_dataset(n, deg, dims[0], dims[-1], 2, 3, 4)
+        t = cg.make_trainer(data, model, cg.Strategy("1d", 1, graph=False))
+        t.distribute()
+        got = list(t.run_epochs(1))  # first epoch also builds the column blocks
+        k0 = cg.kernel_launches()
+        got += list(t.run_epochs(1))
+        launches[mb] = cg.kernel_launches() - k0
+        L = len(dims)
+        out = dict(losses=got, h_final=t.h_tile(L - 1).astype(np.float64),
+                   y=[t.y(l).astype(np.float64) for l in range(L - 1)],
+                   g=[t.g_tile(l).astype(np.float64) for l in range(L - 1)],
+                   w=[t.weight(l).astype(np.float64) for l in range(L - 1)])
+        assert max_rel_error(out, losses, h, y, g, w) < TOL, mb
+    # Passes per SpMM (trainer.cu spmm_passes): ceil(panel / budget), at most
+    # 64 and at most nnz-per-row / 12.  Per epoch the reference order runs
+    # SpMMs of width 64 and 16 forward and 8 and 16 backward.
+    def nb(f):
+        import math
+        per_row = (od["adj"].nnz) / n
+        return max(1, min(64, math.ceil(n * f * 4 / (panel_mb * 1048576)), int(per_row / 12)))
+    assert nb(64) == passes
+    extra = sum(nb(f) - 1 for f in (64, 16, 8, 16))
+    assert launches[panel_mb] - launches[1e6] == extra, launches

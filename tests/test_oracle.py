@@ -34,6 +34,26 @@ def test_er_matches_reference_fixture(orc):
         assert np.array_equal(a.col_idx, gd[key + "_col_idx"])
 
 
+def test_er_multithreaded_equals_sequential(orc):
+    """The jump-ahead restatement (row sub-streams at draw u*(n-1)) reproduces
+    the sequential generator bit for bit, for any thread count."""
+    for n, d, s, t in ((32, 8.0, 1, 3), (64, 8.0, 7, 8), (2500, 9.0, 11, 5)):
+        a, b = orc.er_generate(n, d, s), orc.er_generate_mt(n, d, s, t)
+        assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col_idx, b.col_idx)
+    assert orc.er_generate_mt(32, 8.0, 1, 4).nnz == 249  # test_sparse_core.cpp:163
+
+
+def test_rng_jump_ahead(orc):
+    seq = orc.rng_draws(9, 0, 600)
+    for k in (1, 63, 64, 65, 599):
+        assert np.array_equal(orc.rng_draws(9, k, 600 - k), seq[k:])
+
+
+def test_er_multithreaded_matches_live_reference(orc, ref):
+    a, b = ref.er(1500, 12.0, 3), orc.er_generate_mt(1500, 12.0, 3, 6)
+    assert np.array_equal(a.row_ptr, b.row_ptr) and np.array_equal(a.col_idx, b.col_idx)
+
+
 # test_sparse_core.cpp:39-55
 def test_from_edge_list_golden(orc):
     a = orc.from_edge_list(3, [0, 0, 2], [1, 1, 0], undirected=False)
