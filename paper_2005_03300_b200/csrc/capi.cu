@@ -375,9 +375,9 @@ int cagnet_dataset_load(int device, const char* edges_path, const char* features
                         const char* labels_path, int undirected, cagnet_dataset_t* out) {
   return guarded([&] {
     cagnet::require(edges_path && features_path && labels_path, "load_dataset: null path");
-    set_device(device);
     auto d = std::make_unique<cagnet_dataset_s>();
-    d->data = cagnet::dataset_load(edges_path, features_path, labels_path, undirected != 0);
+    // Parsing (and its errors) happens on the host before the device is touched.
+    d->data = cagnet::dataset_load(edges_path, features_path, labels_path, undirected != 0, device);
     wrap_dataset(d.get());
     *out = d.release();
   });

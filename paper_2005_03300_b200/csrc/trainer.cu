@@ -145,28 +145,44 @@ std::unique_ptr<DeviceDataset> dataset_make(int64_t n, const int64_t* raw_rp,
                                             const int64_t* raw_ci, const double* features,
                                             int64_t f, const int64_t* labels,
                                             const uint8_t* mask, int64_t classes) {
+  // validate_csr-style checks on the raw structure (csr.cpp:25-48).
+  require(raw_rp[0] == 0, "make_dataset: row_ptr must start at 0");
+  for (int64_t i = 0; i < n; ++i) {
+    require(raw_rp[i] <= raw_rp[i + 1], "make_dataset: row_ptr decreases at row " + std::to_string(i));
+    for (int64_t k = raw_rp[i]; k < raw_rp[i + 1]; ++k) {
+      require(raw_ci[k] >= 0 && raw_ci[k] < n, "make_dataset: column index out of range in row " + std::to_string(i));
+      require(k == raw_rp[i] || raw_ci[k - 1] < raw_ci[k],
+              "make_dataset: columns not strictly increasing in row " + std::to_string(i));
+    }
+  }
+  cudaStream_t s;
+  CG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  DeviceCsr raw;
+  try {
+    raw = upload_csr(n, n, raw_rp, raw_ci, nullptr, s);
+    CG_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    cudaStreamDestroy(s);
+    throw;
+  }
+  CG_CUDA(cudaStreamDestroy(s));
+  return dataset_make_device(std::move(raw), features, f, labels, mask, classes);
+}
+
+std::unique_ptr<DeviceDataset> dataset_make_device(DeviceCsr raw, const double* features, int64_t f,
+                                                   const int64_t* labels, const uint8_t* mask,
+                                                   int64_t classes) {
   auto d = std::make_unique<DeviceDataset>();
   d->device = current_device();
+  const int64_t n = raw.n_rows;
   d->n = n;
   d->f = f;
   d->num_classes = classes;
   cudaStream_t s;
   CG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   try {
-    // validate_csr-style checks on the raw structure (csr.cpp:25-48).
-    require(raw_rp[0] == 0, "make_dataset: row_ptr must start at 0");
-    for (int64_t i = 0; i < n; ++i) {
-      require(raw_rp[i] <= raw_rp[i + 1], "make_dataset: row_ptr decreases at row " + std::to_string(i));
-      for (int64_t k = raw_rp[i]; k < raw_rp[i + 1]; ++k) {
-        require(raw_ci[k] >= 0 && raw_ci[k] < n, "make_dataset: column index out of range in row " + std::to_string(i));
-        require(k == raw_rp[i] || raw_ci[k - 1] < raw_ci[k],
-                "make_dataset: columns not strictly increasing in row " + std::to_string(i));
-      }
-    }
-    {
-      DeviceCsr raw = upload_csr(n, n, raw_rp, raw_ci, nullptr, s);
-      d->adj = normalize_device(raw, nullptr, s);
-    }
+    d->adj = normalize_device(raw, nullptr, s);
+    { DeviceCsr drop = std::move(raw); }
     d->adj_t = transpose_device(d->adj, s);
     d->ldf = padded_ld(f);
     d->features.resize(static_cast<size_t>(n * d->ldf));

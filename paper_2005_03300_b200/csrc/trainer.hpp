@@ -42,11 +42,17 @@ std::unique_ptr<DeviceDataset> dataset_generate(int64_t n, double degree, int64_
 // (n entries) receives perm.
 std::unique_ptr<DeviceDataset> dataset_permute(const DeviceDataset& d, uint64_t seed,
                                                std::vector<int64_t>* perm_out);
-// load_dataset (dataset.cpp:293-307): the reference's text formats parsed on
-// the host (io.cu), then make_dataset on the current device.
+// load_dataset (dataset.cpp:293-307): the reference's text formats parsed
+// from mapped files on all host cores, from_edge_list's sort + unique on the
+// GPU (io.cu), then make_dataset on the current device.
 std::unique_ptr<DeviceDataset> dataset_load(const std::string& edges_path,
                                             const std::string& features_path,
-                                            const std::string& labels_path, bool undirected);
+                                            const std::string& labels_path, bool undirected, int device);
+// make_dataset (dataset.cpp:76-90) from a raw unit-valued CSR already on the
+// current device (load_dataset's GPU-built from_edge_list).
+std::unique_ptr<DeviceDataset> dataset_make_device(DeviceCsr raw, const double* features, int64_t f,
+                                                   const int64_t* labels, const uint8_t* mask,
+                                                   int64_t classes);
 // make_dataset (dataset.cpp:76-90) from host arrays.
 std::unique_ptr<DeviceDataset> dataset_make(int64_t n, const int64_t* raw_rp,
                                             const int64_t* raw_ci, const double* features,
