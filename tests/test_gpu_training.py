@@ -384,3 +384,51 @@ def test_l2_multipass_spmm_matches_serial(cg, orc, monkeypatch, panel_mb, passes
     assert nb(64) == passes
     extra = sum(nb(f) - 1 for f in (64, 16, 8, 16))
     assert launches[panel_mb] - launches[1e6] == extra, launches
+
+
+def on_all_ranks(trainers, fn):
+    """fn(trainer) on every rank concurrently (collective calls)."""
+    import threading
+    errors = []
+
+    def body(t):
+        try:
+            fn(t)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    th = [threading.Thread(target=body, args=(t,)) for t in trainers]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("layers", [[1], [1, 2], [2, 1, 2]])
+def test_forward_layer_between_replayed_epochs(cg, orc, P, layers):
+    """run_forward_layer (dist_common.cpp:110-115) between CUDA-graph epochs on
+    the 1D peer-memory exchange: the layer's direct push is settled and the
+    buffer rotation padded, so the replays that follow still match the
+    serial oracle (forward_layer recomputes activations from the same
+    weights, so it leaves the training trajectory unchanged)."""
+    dims = [24, 8, 8, 6]
+    model = cg.init_glorot(dims, 5, 0.5)
+    strat = cg.Strategy("1d", P, 1, reassociate=True)
+    trainers, _ = distributed_trainers(
+        cg, lambda: cg.generate_dataset(300, 12.0, 24, 6, 2, 3, 4, device=0), model, strat)
+    losses = {t.rank: [] for t in trainers}
+    on_all_ranks(trainers, lambda t: losses[t.rank].extend(t.run_epochs(3)))
+    for l in layers:
+        on_all_ranks(trainers, lambda t: t.forward_layer(l))
+    on_all_ranks(trainers, lambda t: losses[t.rank].extend(t.run_epochs(4)))
+    od = orc.generate_dataset(300, 12.0, 24, 6, 2, 3, 4)
+    ref_losses, h, y, g, w = orc.train_serial(od, dims, model.weights, 0.5, 7)
+    L = len(dims)
+    for t in trainers:
+        r0, r1 = t.tile_rows(t.rank)
+        assert np.allclose(losses[t.rank], ref_losses, rtol=TOL, atol=TOL)
+        import oracle
+        assert oracle.rel_frobenius(t.weight(0), w[0]) < TOL
+        assert oracle.rel_frobenius(t.h_tile(L - 1), h[r0:r1]) < TOL
