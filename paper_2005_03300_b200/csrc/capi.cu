@@ -536,7 +536,7 @@ int cagnet_trainer_distribute(cagnet_trainer_t t) {
 int cagnet_trainer_forward_layer(cagnet_trainer_t t, int l) {
   return guarded([&] {
     set_device(t->t->device());
-    t->t->forward_layer(l);
+    t->t->run_forward_layer(l);
   });
 }
 

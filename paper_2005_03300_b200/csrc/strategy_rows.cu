@@ -244,6 +244,20 @@ class TrainerRows final : public Trainer {
 
   void begin_epoch() override { epoch_exchanges_ = 0; }
 
+  void finish_external_layer() override {
+    // A push the layer committed for an exchange that will not come is
+    // waited for (device wait count back in step with the publish count),
+    // and flag-only exchanges pad the rotation to a multiple of the buffer
+    // count, where every epoch starts.
+    settle_pending();
+    while (p2p_ok_ && p2p_stage_ % PeerPanels::kBuffers != 0) {
+      next_p2p_buffer();
+      p2p_.signal(cs_);
+      p2p_.wait_ready(cs_);
+    }
+    epoch_exchanges_ = 0;
+  }
+
   void check_async() override {
     // Report both records: the comm world's and the panel exchange's.
     std::string msg;

@@ -317,6 +317,7 @@ const int2* Trainer::colval(const int32_t* ci, const float* v, int64_t nnz) {
 
 void Trainer::init_tiles() {
   colval_.clear();
+  colblocks_.clear();  // keyed by row_ptr addresses, which a new distribute() may reuse
   const int L = num_layers();
   const BlockRange rows = tile_rows(rank_);
   h_.clear();
@@ -632,6 +633,13 @@ void Trainer::loss_all_reduce(double* partial_dev) {
   comm_->all_reduce(grid_.world(), partial_dev, 1, ncclFloat64, Category::Reduce, 1, ms_);
   kern::push_loss(losses_dev_.get(), loss_slot_.get(), partial_dev, ms_);
   ++epochs_done_;
+}
+
+void Trainer::run_forward_layer(int l) {
+  CG_CUDA(cudaSetDevice(device_));
+  forward_layer(l);
+  finish_external_layer();
+  cs_after_ms();
 }
 
 void Trainer::epoch_body() {

@@ -87,6 +87,11 @@ class Trainer {
 
   virtual void distribute() = 0;
   virtual void forward_layer(int l) = 0;  // 1-based, consumes h[l-1]
+  // Trainer::run_forward_layer (dist_common.cpp:110-115): one layer outside
+  // an epoch, called on every rank.  Leaves the exchange machinery at an
+  // epoch boundary (see finish_external_layer), so later eager or replayed
+  // epochs are unaffected.
+  void run_forward_layer(int l);
   // Loss (into the device loss slot), gradients and the SGD update.
   virtual void backward_and_step() = 0;
   virtual BlockRange tile_rows(int rank) const = 0;
@@ -191,6 +196,10 @@ class Trainer {
   // Per-epoch reset of strategy-private host state so every epoch issues the
   // identical launch sequence (required for graph replay).
   virtual void begin_epoch() {}
+  // After a layer run outside an epoch: strategy-private exchange state back
+  // to an epoch boundary (pending direct pushes waited for, buffer rotation
+  // padded) so a replayed epoch graph sees the state it was captured with.
+  virtual void finish_external_layer() {}
   // --- helpers shared by the strategies ---
   void init_tiles();  // h/z/g tile shapes from tile_rows/tile_cols, labels, H0
   // End of distribute(): setup work on the legacy stream (zeroing memsets)
