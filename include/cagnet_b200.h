@@ -280,6 +280,46 @@ CAGNET_API int cagnet_trainer_profile_reset(cagnet_trainer_t t);
  * the epoch, D2H of the loss (blocking). */
 CAGNET_API int cagnet_trainer_step_host(cagnet_trainer_t t, const float* x_tile,
                                         const int32_t* labels_tile, double* loss);
+/* --- run_distributed → DistOutcome (dist.hpp:138-150, dist_common.cpp:117-222) ---
+ * The whole distributed run on the device path: one host thread per rank
+ * (SimRuntime::run's thread-per-rank model), each rank a Trainer on its GPU,
+ * then the outcome assembled on the host with the reference's bitwise replica
+ * checks (replica divergence -> CAGNET_ERUNTIME, message as the reference).
+ * backend: CAGNET_BACKEND_AUTO (NCCL with one GPU per rank when there are at
+ * least `ranks` GPUs, else the in-process world on the dataset's GPU),
+ * _NCCL or _LOCAL.  The dataset is read-only and shared; the NCCL backend
+ * copies it to each rank's GPU. */
+typedef struct cagnet_outcome_s* cagnet_outcome_t;
+#define CAGNET_BACKEND_AUTO 0
+#define CAGNET_BACKEND_NCCL 1
+#define CAGNET_BACKEND_LOCAL 2
+#define CAGNET_OPT_REASSOCIATE 1u           /* narrow-first propagation (extension) */
+#define CAGNET_OPT_NO_GRAPH 2u              /* eager epochs instead of CUDA-graph replays */
+#define CAGNET_OPT_NO_RESIDENT_SPARSE 4u    /* 2D/3D: the reference's per-stage sparse broadcasts */
+#define CAGNET_OPT_NO_P2P 8u                /* 1D: NCCL all-gather instead of peer-memory pushes */
+#define CAGNET_OPT_FUSE0 16u                /* no fused SpMM row epilogues */
+#define CAGNET_OPT_FUSE2 32u                /* fused epilogues incl. the dense W transforms */
+#define CAGNET_OPT_OVERLAP 64u              /* 1D peer memory: own-block SpMM during the pushes */
+#define CAGNET_OPT_PIPELINE 128u            /* 1D peer memory: per-destination pipelined stages */
+CAGNET_API int cagnet_run_distributed(cagnet_dataset_t data, const int64_t* dims, int ndims,
+                                      const double* weights, double learning_rate, int kind,
+                                      int ranks, int repl, int block, int epochs, int backend,
+                                      uint32_t options, cagnet_outcome_t* out);
+/* out8 = {n, ndims, epochs, ranks, backend used, #prereduction totals,
+ *         last epoch device time in microseconds (max over ranks), 0}. */
+CAGNET_API int cagnet_outcome_info(cagnet_outcome_t o, int64_t* out8);
+CAGNET_API int cagnet_outcome_losses(cagnet_outcome_t o, double* out /* epochs */);
+CAGNET_API int cagnet_outcome_h_final(cagnet_outcome_t o, double* out /* n x dims[L-1] */);
+CAGNET_API int cagnet_outcome_g(cagnet_outcome_t o, int l, double* out /* n x dims[l+1] */);
+CAGNET_API int cagnet_outcome_y(cagnet_outcome_t o, int l, double* out /* dims[l] x dims[l+1] */);
+CAGNET_API int cagnet_outcome_weight(cagnet_outcome_t o, int l, double* out /* dims[l] x dims[l+1] */);
+/* rank's ledger: [dbcast, sbcast, reduce, allgather] x {messages, words_sent,
+ * words_received, payload_words, calls} (ledger.hpp:41-47). */
+CAGNET_API int cagnet_outcome_ledger(cagnet_outcome_t o, int rank, uint64_t* out20);
+CAGNET_API int cagnet_outcome_prereduction_totals(cagnet_outcome_t o, uint64_t* out);
+CAGNET_API int cagnet_outcome_memory_peaks(cagnet_outcome_t o, uint64_t* out /* ranks */);
+CAGNET_API int cagnet_outcome_free(cagnet_outcome_t o);
+
 /* Total hot-path kernel launches issued by this library so far. */
 CAGNET_API int cagnet_kernel_launches(uint64_t* out);
 /* The compute stream the trainer launches on (a cudaStream_t). */

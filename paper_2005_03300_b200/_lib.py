@@ -110,6 +110,18 @@ SIGNATURES = {
     "cagnet_trainer_profile_reset": [vp],
     "cagnet_trainer_step_host": [vp, vp, vp, C.POINTER(f64)],
     "cagnet_kernel_launches": [C.POINTER(u64)],
+    "cagnet_run_distributed": [vp, _i64p, i32, _f64p, f64, i32, i32, i32, i32, i32, i32, C.c_uint32,
+                               C.POINTER(vp)],
+    "cagnet_outcome_info": [vp, _i64p],
+    "cagnet_outcome_losses": [vp, _f64p],
+    "cagnet_outcome_h_final": [vp, _f64p],
+    "cagnet_outcome_g": [vp, i32, _f64p],
+    "cagnet_outcome_y": [vp, i32, _f64p],
+    "cagnet_outcome_weight": [vp, i32, _f64p],
+    "cagnet_outcome_ledger": [vp, i32, _u64p],
+    "cagnet_outcome_prereduction_totals": [vp, _u64p],
+    "cagnet_outcome_memory_peaks": [vp, _u64p],
+    "cagnet_outcome_free": [vp],
     "cagnet_trainer_free": [vp],
 }
 _RESTYPES = {"cagnet_last_error": C.c_char_p, "cagnet_version": i32}

@@ -12,7 +12,6 @@ reference; state lives on the GPU behind the library's handles.
 from __future__ import annotations
 
 import ctypes as C
-import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -535,6 +534,9 @@ class DistOutcome:
     model: GnnModel
     ledger: list  # per rank
     epoch_ms: float = 0.0  # last epoch, device time, max over ranks (GPU extension)
+    prereduction_totals: np.ndarray = None  # SimRuntime gauges (3D only, runtime.cpp:287-295)
+    memory_peaks: np.ndarray = None
+    backend: str = "local"
 
 
 def assemble_tiles(trainers, n, width, pick) -> np.ndarray:
@@ -555,85 +557,80 @@ def assemble_tiles(trainers, n, width, pick) -> np.ndarray:
     return out
 
 
-def _verified(trainers, get, what):
-    ref = get(trainers[0])
-    for t in trainers[1:]:
-        x = get(t)
-        if not np.array_equal(np.asarray(x).view(np.uint8), np.asarray(ref).view(np.uint8)):
-            raise RuntimeError(f"{what} replica divergence at rank {t.rank}")
-    return ref
+BACKENDS = {"auto": 0, "nccl": 1, "local": 2}
+OPT = dict(reassociate=1, no_graph=2, no_resident_sparse=4, no_p2p=8, fuse0=16, fuse2=32,
+           overlap=64, pipeline=128)
 
 
-def run_distributed(data_factory, model: GnnModel, strat: Strategy, epochs: int,
-                    devices=None, comm: str = "auto") -> DistOutcome:
-    """run_distributed (dist_common.cpp:205-222) in one process: one host
-    thread per rank (the reference's thread-per-rank model,
-    runtime.cpp:270-285).  comm = "nccl": one GPU per rank, NCCL and NVLink
-    peer memory between them; "local": every rank on one GPU through the
-    in-process world (device-memory collectives, same flag protocol);
-    "auto": NCCL when there are at least P GPUs, else local.
-    data_factory(device) must build the same dataset on each call."""
+def strategy_options(strat: Strategy) -> int:
+    """Strategy extension flags as the C-ABI's CAGNET_OPT_* bits."""
+    opts = 0
+    opts |= OPT["reassociate"] if strat.reassociate else 0
+    opts |= 0 if strat.graph else OPT["no_graph"]
+    opts |= 0 if strat.resident_sparse else OPT["no_resident_sparse"]
+    opts |= 0 if strat.p2p else OPT["no_p2p"]
+    opts |= OPT["fuse0"] if strat.fuse == 0 else OPT["fuse2"] if strat.fuse == 2 else 0
+    opts |= OPT["overlap"] if strat.overlap else 0
+    opts |= OPT["pipeline"] if strat.pipeline else 0
+    return opts
+
+
+def run_distributed(data, model: GnnModel, strat: Strategy, epochs: int,
+                    comm: str = "auto") -> DistOutcome:
+    """run_distributed (dist_common.cpp:205-222) through the C++ host
+    (cagnet_run_distributed): one host thread per rank, each a Trainer on its
+    GPU, the outcome assembled with the reference's bitwise replica checks.
+    comm = "nccl": one GPU per rank (NCCL and NVLink peer memory; the dataset
+    is copied to every rank's GPU); "local": every rank on the dataset's GPU
+    through the in-process world; "auto": NCCL when there are >= P GPUs.
+    `data` is a GraphDataset or a factory data(device) that builds it (called
+    once, for device 0)."""
     if epochs <= 0:
         raise InvalidArgument(1, "run_epochs: epoch count must be positive")
-    P = strat.ranks
-    ProcessGrid(strat)  # validates the geometry before any GPU work
-    if comm not in ("auto", "nccl", "local"):
+    if comm not in BACKENDS:
         raise InvalidArgument(1, f"run_distributed: unknown comm backend {comm!r}")
-    if devices is None:
-        n_dev = C.c_int()
-        check(lib.cagnet_device_count(C.byref(n_dev)))
-        if comm == "auto":
-            comm = "nccl" if n_dev.value >= P else "local"
-        if comm == "nccl" and n_dev.value < P:
-            raise InvalidArgument(1, f"run_distributed: {P} ranks need {P} GPUs, "
-                                     f"found {n_dev.value}")
-        if n_dev.value < 1:
-            raise InvalidArgument(1, "run_distributed: no GPU")
-        devices = list(range(P)) if comm == "nccl" else [0] * P
-    elif comm == "auto":
-        comm = "local" if P > 1 and len(set(devices)) == 1 else "nccl"
-    if comm == "local" and len(set(devices)) != 1:
-        raise InvalidArgument(1, "run_distributed: the local world runs every rank on one GPU")
-    local = comm == "local" and P > 1
-    nid = (comm_local_id(P, devices[0]) if local else comm_unique_id()) if P > 1 else None
-    datas = [None] * P
-    trainers = [None] * P
-    losses = [None] * P
-    errors = []
-
-    def body(r):
-        try:
-            datas[r] = data_factory(devices[r])
-            trainers[r] = Trainer(datas[r], model, strat, r, nid)
-            trainers[r].distribute()
-            losses[r] = trainers[r].run_epochs(epochs)
-        except Exception as e:  # the lowest-rank exception wins (runtime.cpp:281-284)
-            errors.append((r, e))
-            if local:  # release the peers blocked in this rank's collectives
-                comm_local_abort(nid, f"rank {r} raised: {e}")
-
-    threads = [threading.Thread(target=body, args=(r,)) for r in range(P)]
-    for th in threads:
-        th.start()
-    for th in threads:
-        th.join()
-    if errors:
-        # The lowest-rank original failure wins; peers released by an abort
-        # only report its echo.
-        primary = [x for x in errors if "local world aborted" not in str(x[1])] or errors
-        raise sorted(primary, key=lambda x: x[0])[0][1]
-    n = datas[0].n
-    L = len(model.layer_dims)
-    out_losses = _verified(trainers, lambda t: losses[t.rank], "loss")
-    h_final = assemble_tiles(trainers, n, model.layer_dims[-1], lambda t: t.h_tile(L - 1))
-    g_final = [assemble_tiles(trainers, n, model.layer_dims[i + 1], lambda t, i=i: t.g_tile(i))
-               for i in range(L - 1)]
-    y_final = [_verified(trainers, lambda t, i=i: t.y(i), "gradient").astype(np.float64)
-               for i in range(L - 1)]
-    w_final = [_verified(trainers, lambda t, i=i: t.weight(i), "weight").astype(np.float64)
-               for i in range(L - 1)]
-    ledgers = [t.ledger() for t in trainers]
-    epoch_ms = max(t.last_epoch_ms() for t in trainers)
-    return DistOutcome(np.asarray(out_losses), h_final, y_final, g_final,
-                       GnnModel(list(model.layer_dims), w_final, model.learning_rate), ledgers,
-                       epoch_ms)
+    ProcessGrid(strat)  # validates the geometry before any GPU work
+    if not isinstance(data, GraphDataset):
+        data = data(0)
+    dims = np.asarray(model.layer_dims, np.int64)
+    out = C.c_void_p()
+    check(lib.cagnet_run_distributed(data.h, dims, len(dims), model.flat_weights(),
+                                     model.learning_rate, strat.kind_id, strat.ranks, strat.repl,
+                                     strat.block, epochs, BACKENDS[comm], strategy_options(strat),
+                                     C.byref(out)))
+    h = out.value
+    try:
+        info = np.zeros(8, np.int64)
+        check(lib.cagnet_outcome_info(h, info))
+        n, L, E, P, backend, n_pre, epoch_us = (int(x) for x in info[:7])
+        losses = np.zeros(E)
+        check(lib.cagnet_outcome_losses(h, losses))
+        h_final = np.zeros((n, int(dims[-1])))
+        check(lib.cagnet_outcome_h_final(h, h_final))
+        ys, gs, ws = [], [], []
+        for l in range(L - 1):
+            y = np.zeros((int(dims[l]), int(dims[l + 1])))
+            check(lib.cagnet_outcome_y(h, l, y))
+            w = np.zeros_like(y)
+            check(lib.cagnet_outcome_weight(h, l, w))
+            g = np.zeros((n, int(dims[l + 1])))
+            check(lib.cagnet_outcome_g(h, l, g))
+            ys.append(y)
+            ws.append(w)
+            gs.append(g)
+        ledgers = []
+        for r in range(P):
+            buf = np.zeros(20, np.uint64)
+            check(lib.cagnet_outcome_ledger(h, r, buf))
+            ledgers.append({c: dict(zip(COUNTER_FIELDS, (int(x) for x in buf[5 * i:5 * i + 5])))
+                            for i, c in enumerate(CATEGORIES)})
+        pre = np.zeros(max(n_pre, 1), np.uint64)
+        check(lib.cagnet_outcome_prereduction_totals(h, pre))
+        peaks = np.zeros(max(P, 1), np.uint64)
+        check(lib.cagnet_outcome_memory_peaks(h, peaks))
+    finally:
+        lib.cagnet_outcome_free(h)
+    return DistOutcome(losses, h_final, ys, gs,
+                       GnnModel([int(d) for d in dims], ws, model.learning_rate), ledgers,
+                       epoch_us / 1000.0, pre[:n_pre], peaks[:P],
+                       {v: k for k, v in BACKENDS.items()}[backend])

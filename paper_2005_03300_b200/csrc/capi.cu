@@ -12,6 +12,7 @@
 
 #include "kernels.cuh"
 #include "rng.hpp"
+#include "run.hpp"
 #include "trainer.hpp"
 
 struct cagnet_csr_s {
@@ -21,6 +22,9 @@ struct cagnet_csr_s {
 struct cagnet_dataset_s {
   std::unique_ptr<cagnet::DeviceDataset> data;
   cagnet_csr_s adj, adj_t;
+};
+struct cagnet_outcome_s {
+  cagnet::DistOutcome o;
 };
 struct cagnet_trainer_s {
   std::unique_ptr<cagnet::Trainer> t;
@@ -508,6 +512,88 @@ int cagnet_comm_local_abort(const uint8_t* id128, const char* why) {
     std::memcpy(&id, id128, sizeof(id));
     cagnet::LocalWorld::abort_id(id, why ? why : "aborted by a rank");
   });
+}
+
+int cagnet_run_distributed(cagnet_dataset_t data, const int64_t* dims, int ndims, const double* weights,
+                           double learning_rate, int kind, int ranks, int repl, int block, int epochs,
+                           int backend, uint32_t options, cagnet_outcome_t* out) {
+  return guarded([&] {
+    cagnet::require(data && dims && weights && out, "run_distributed: null argument");
+    cagnet::require(ndims >= 2, "init_glorot: need at least two layer dims, got " + std::to_string(ndims));
+    cagnet::require(backend >= 0 && backend <= 2, "run_distributed: unknown backend");
+    set_device(data->data->device);
+    cagnet::RunOptions opt;
+    opt.reassociate = (options & CAGNET_OPT_REASSOCIATE) != 0;
+    opt.graph = (options & CAGNET_OPT_NO_GRAPH) == 0;
+    opt.resident_sparse = (options & CAGNET_OPT_NO_RESIDENT_SPARSE) == 0;
+    opt.p2p = (options & CAGNET_OPT_NO_P2P) == 0;
+    opt.fuse = (options & CAGNET_OPT_FUSE0) ? 0 : (options & CAGNET_OPT_FUSE2) ? 2 : 1;
+    opt.overlap = (options & CAGNET_OPT_OVERLAP) != 0;
+    opt.pipeline = (options & CAGNET_OPT_PIPELINE) != 0;
+    auto o = std::make_unique<cagnet_outcome_s>();
+    o->o = cagnet::run_distributed(*data->data, std::vector<int64_t>(dims, dims + ndims), weights, learning_rate,
+                                   make_strategy(kind, ranks, repl, block), epochs,
+                                   static_cast<cagnet::Backend>(backend), opt);
+    *out = o.release();
+  });
+}
+
+int cagnet_outcome_info(cagnet_outcome_t o, int64_t* out8) {
+  return guarded([&] {
+    const cagnet::DistOutcome& d = o->o;
+    const int64_t v[8] = {d.n, static_cast<int64_t>(d.dims.size()), static_cast<int64_t>(d.losses.size()),
+                          d.ranks, d.backend, static_cast<int64_t>(d.prereduction_totals.size()),
+                          static_cast<int64_t>(d.epoch_ms * 1000.0), 0};
+    std::memcpy(out8, v, sizeof(v));
+  });
+}
+
+namespace {
+void copy_out(const std::vector<double>& v, double* out) {
+  if (!v.empty()) std::memcpy(out, v.data(), v.size() * sizeof(double));
+}
+const std::vector<double>& layer_of(const std::vector<std::vector<double>>& v, int l) {
+  if (l < 0 || l >= static_cast<int>(v.size())) throw std::invalid_argument("outcome: layer index out of range");
+  return v[static_cast<size_t>(l)];
+}
+}  // namespace
+
+int cagnet_outcome_losses(cagnet_outcome_t o, double* out) {
+  return guarded([&] { copy_out(o->o.losses, out); });
+}
+int cagnet_outcome_h_final(cagnet_outcome_t o, double* out) {
+  return guarded([&] { copy_out(o->o.h_final, out); });
+}
+int cagnet_outcome_g(cagnet_outcome_t o, int l, double* out) {
+  return guarded([&] { copy_out(layer_of(o->o.g_final, l), out); });
+}
+int cagnet_outcome_y(cagnet_outcome_t o, int l, double* out) {
+  return guarded([&] { copy_out(layer_of(o->o.y_final, l), out); });
+}
+int cagnet_outcome_weight(cagnet_outcome_t o, int l, double* out) {
+  return guarded([&] { copy_out(layer_of(o->o.weights, l), out); });
+}
+int cagnet_outcome_ledger(cagnet_outcome_t o, int rank, uint64_t* out20) {
+  return guarded([&] {
+    cagnet::require(rank >= 0 && rank < o->o.ranks, "outcome: rank out of range");
+    for (int c = 0; c < cagnet::kNumCategories; ++c)
+      for (int f = 0; f < 5; ++f) out20[c * 5 + f] = o->o.ledger[static_cast<size_t>(rank)][c][f];
+  });
+}
+int cagnet_outcome_prereduction_totals(cagnet_outcome_t o, uint64_t* out) {
+  return guarded([&] {
+    const auto& v = o->o.prereduction_totals;
+    if (!v.empty()) std::memcpy(out, v.data(), v.size() * sizeof(uint64_t));
+  });
+}
+int cagnet_outcome_memory_peaks(cagnet_outcome_t o, uint64_t* out) {
+  return guarded([&] {
+    const auto& v = o->o.memory_peaks;
+    if (!v.empty()) std::memcpy(out, v.data(), v.size() * sizeof(uint64_t));
+  });
+}
+int cagnet_outcome_free(cagnet_outcome_t o) {
+  return guarded([&] { delete o; });
 }
 
 int cagnet_trainer_create(cagnet_dataset_t data, const int64_t* dims, int ndims, const double* weights,

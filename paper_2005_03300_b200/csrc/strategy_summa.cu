@@ -137,6 +137,7 @@ class TrainerSumma final : public Trainer {
       Mat u = row_gemm_reduce(h, l, wprev, wcur);
       Mat part{partial_.m.p, blockrow.size(), mycur.size(), padded_ld(mycur.size())};
       propagate(at_parts_[0], /*transpose=*/true, u, chunks(mycur.size()), part);
+      meter_partial(part, at_parts_[0], l);
       Mat t = fiber_reduce_scatter(part, i);
       kern::copy2d(z.p, z.ld, t.p, t.ld, t.rows, t.cols, cs_);
       if (!last)
@@ -146,6 +147,7 @@ class TrainerSumma final : public Trainer {
       // Phase 1: partial = sum_q At[i, (q,k)] * H[(q,k), j]  (chunked panels in 2D).
       Mat part{partial_.m.p, blockrow.size(), prevc.size(), padded_ld(prevc.size())};
       propagate(at_parts_[0], /*transpose=*/true, h, chunks(prevc.size()), part);
+      meter_partial(part, at_parts_[0], l);
       Mat t = fiber_reduce_scatter(part, i);
       // A widening layer keeps its T tile for the narrow-first backward
       // (Y = Tᵀ G instead of Hᵀ (A G), see backward_and_step).
@@ -204,6 +206,7 @@ class TrainerSumma final : public Trainer {
       // S = A * G with the same split as the forward propagation.
       Mat part{partial_.m.p, blockrow.size(), mycur.size(), padded_ld(mycur.size())};
       propagate(a_parts_[0], /*transpose=*/false, g, {BlockRange{0, mycur.size()}}, part);
+      meter_partial(part, a_parts_[0], 0);
       Mat st = fiber_reduce_scatter(part, i);
 
       // Shared S panel sweep: Y strips (column + fiber all-reduce) and G_prev.
@@ -390,11 +393,27 @@ class TrainerSumma final : public Trainer {
     }
     Mat part{partial_.m.p, blockrow.size(), myprev.size(), padded_ld(myprev.size())};
     propagate(a_parts_[0], /*transpose=*/false, u, {BlockRange{0, myprev.size()}}, part);
+    meter_partial(part, a_parts_[0], 0);
     Mat st = fiber_reduce_scatter(part, i);
     Mat gprev = g_[static_cast<size_t>(l - 2)].m;
     const Mat& zp = z_[static_cast<size_t>(l - 2)].m;
     kern::copy2d(gprev.p, gprev.ld, st.p, st.ld, st.rows, st.cols, cs_);
     kern::mask_relu_prime(gprev.p, gprev.ld, zp.p, zp.ld, gprev.rows, gprev.cols, cs_);
+  }
+
+  // The 3D trainer's SimRuntime gauges (dist_3d.cpp:84-87 forward, 147-150
+  // backward): the partial's words, and the resident words = the sparse
+  // tile's nonzeros + the partial + the H tiles (those below layer l in the
+  // forward pass, fwd_layer > 0; all of them in the backward pass, 0).
+  void meter_partial(const Mat& part, const DeviceCsr& tile, int fwd_layer) {
+    if (strat_.kind != StrategyKind::ThreeD) return;
+    const uint64_t pw = static_cast<uint64_t>(part.rows * part.cols);
+    note_prereduction(pw);
+    uint64_t resident = static_cast<uint64_t>(tile.nnz) + pw;
+    const int upto = fwd_layer > 0 ? fwd_layer : num_layers();
+    for (int l2 = 0; l2 < upto; ++l2)
+      resident += static_cast<uint64_t>(h_[static_cast<size_t>(l2)].m.rows * h_[static_cast<size_t>(l2)].m.cols);
+    note_memory_words(resident);
   }
 
   void keep_t_valid(int l, bool v) {

@@ -238,6 +238,8 @@ Trainer::Trainer(const DeviceDataset& data, std::vector<int64_t> dims, const dou
   require(train_total_ > 0, "distributed training: empty training set");
   require(rank >= 0 && rank < grid_.ranks(), "trainer: rank outside the grid");
   CG_CUDA(cudaSetDevice(device_));
+  if (const char* fb = std::getenv("CAGNET_L2_FETCH_BYTES"))  // experiment knob (device-wide)
+    CG_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(std::atoi(fb))));
   CG_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
   comm_ = std::make_unique<Comm>(grid_, rank, id);
   // The comm stream runs at the highest priority: its NCCL / peer-push
@@ -673,6 +675,7 @@ void Trainer::epoch() {
     return;
   }
   if (!graph_exec_) {
+    const size_t notes0 = prered_.size();
     comm_->snapshot(ledger_before_);
     const uint64_t k0 = launch_counter().load();
     CG_CUDA(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeRelaxed));
@@ -694,9 +697,11 @@ void Trainer::epoch() {
     // replayed wait never targets a peer still inside its capture.
     comm_->local_barrier();
     comm_->snapshot(ledger_after_);  // the capture metered this epoch once
+    prered_graph_.assign(prered_.begin() + static_cast<std::ptrdiff_t>(notes0), prered_.end());
     graph_kernels_ = launch_counter().load() - k0;
   } else {
     comm_->add_delta(ledger_before_, ledger_after_);
+    prered_.insert(prered_.end(), prered_graph_.begin(), prered_graph_.end());
     launch_counter().fetch_add(graph_kernels_);  // the replay runs the captured kernels
     ++epochs_done_;
   }
@@ -720,6 +725,10 @@ void Trainer::flush_losses() {
 std::vector<double> Trainer::run_epochs(int epochs) {
   if (epochs < 0) throw std::invalid_argument("run_epochs: epoch count must be positive");
   const size_t first = losses_host_.size() + static_cast<size_t>(epochs_done_ - epochs_read_);
+  if (epochs > 0) {  // gauges reset per run (runtime.cpp:235-240)
+    prered_.clear();
+    mem_peak_ = 0;
+  }
   for (int e = 0; e < epochs; ++e) epoch();
   flush_losses();
   if (epochs > 0) CG_CUDA(cudaEventElapsedTime(&last_epoch_ms_, ev_t0_, ev_t1_));

@@ -131,6 +131,13 @@ class Trainer {
     return which == 0 ? a_parts_.at(static_cast<size_t>(idx)) : at_parts_.at(static_cast<size_t>(idx));
   }
   const Comm& comm() const { return *comm_; }
+  Comm& comm_mut() { return *comm_; }
+  // SimRuntime gauges of the last run_epochs call (runtime.cpp:287-295,
+  // 450-459; only the 3D strategy notes them, dist_3d.cpp:84-87, 147-150):
+  // per-note words of the pre-reduction partials in call order, and the peak
+  // resident words.  Reset by every run_epochs, like the reference's run().
+  const std::vector<uint64_t>& prereductions() const { return prered_; }
+  uint64_t memory_peak() const { return mem_peak_; }
   cudaStream_t stream() const { return cs_; }
   float last_epoch_ms() const { return last_epoch_ms_; }
 
@@ -235,6 +242,8 @@ class Trainer {
   void run_gemm(const kern::GemmDesc& d, const char* kind);
   void bcast_mat(const Group& g, int root, Mat m, Category cat);
   void sgd_all();
+  void note_prereduction(uint64_t words) { prered_.push_back(words); }
+  void note_memory_words(uint64_t words) { mem_peak_ = words > mem_peak_ ? words : mem_peak_; }
   void loss_all_reduce(double* partial_dev);
   uint64_t words(const Mat& m) const { return static_cast<uint64_t>(m.rows * m.cols); }
   // Brackets one kernel launch on cs_ with events when timing is on.
@@ -294,6 +303,8 @@ class Trainer {
   cudaGraphExec_t graph_exec_ = nullptr;
   uint64_t graph_kernels_ = 0;  // kernels per replay (added to the launch counter)
   CommCounter ledger_before_[kNumCategories], ledger_after_[kNumCategories];
+  std::vector<uint64_t> prered_, prered_graph_;  // notes; the captured epoch's notes
+  uint64_t mem_peak_ = 0;
   int epochs_done_ = 0;
   int epochs_read_ = 0;
   std::vector<double> losses_host_;

@@ -12,21 +12,46 @@ pytestmark = pytest.mark.gpu
 
 
 def test_rank_failure_releases_peers(cg, need_gpus):
-    """Rank 1 raises before its first collective; rank 0, already waiting in
-    the rendezvous, is released and the original error is reported."""
+    """Rank 1 raises before joining; ranks 0, 2, 3, already blocked in
+    distribute()'s collectives, are released by its abort with the reason."""
     need_gpus(1)
-
-    def factory(dev, calls=[0]):
-        calls[0] += 1
-        if calls[0] == 2:
-            raise ValueError("dataset for rank 1 failed")
-        return cg.generate_dataset(40, 6.0, 8, 4, 1, 2, 3, device=dev)
-
+    nid = cg.comm_local_id(4, 0)
     model = cg.init_glorot([8, 6, 4], 5, 0.5)
+    strat = cg.Strategy("2d", 4, 1)
+    errors = {}
+
+    def body(r):
+        try:
+            if r == 1:
+                raise ValueError("dataset for rank 1 failed")
+            d = cg.generate_dataset(40, 6.0, 8, 4, 1, 2, 3, device=0)
+            t = cg.Trainer(d, model, strat, r, nid)
+            t.distribute()
+        except Exception as e:
+            errors[r] = e
+            if r == 1:
+                cg.comm_local_abort(nid, f"rank {r} raised: {e}")
+
     t0 = time.time()
-    with pytest.raises(ValueError, match="rank 1 failed"):
-        cg.run_distributed(factory, model, cg.Strategy("2d", 4, 1), 2, comm="local")
+    th = [threading.Thread(target=body, args=(r,)) for r in range(4)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
     assert time.time() - t0 < 60
+    assert isinstance(errors[1], ValueError)
+    for r in (0, 2, 3):
+        assert "aborted" in str(errors[r]) and "rank 1 raised" in str(errors[r]), errors[r]
+
+
+def test_run_distributed_invalid_model_raises(cg, need_gpus):
+    """A model that does not fit the dataset fails on every rank at
+    construction; run_distributed raises the reference's error, no hang."""
+    need_gpus(1)
+    d = cg.generate_dataset(40, 6.0, 8, 4, 1, 2, 3, device=0)
+    model = cg.init_glorot([9, 6, 4], 5, 0.5)
+    with pytest.raises(cg.InvalidArgument, match="input width 9"):
+        cg.run_distributed(d, model, cg.Strategy("3d", 8), 1, comm="local")
 
 
 def test_silent_rank_times_out_without_trap(cg, need_gpus, monkeypatch):
