@@ -238,8 +238,6 @@ Trainer::Trainer(const DeviceDataset& data, std::vector<int64_t> dims, const dou
   require(train_total_ > 0, "distributed training: empty training set");
   require(rank >= 0 && rank < grid_.ranks(), "trainer: rank outside the grid");
   CG_CUDA(cudaSetDevice(device_));
-  if (const char* fb = std::getenv("CAGNET_L2_FETCH_BYTES"))  // experiment knob (device-wide)
-    CG_CUDA(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(std::atoi(fb))));
   CG_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
   comm_ = std::make_unique<Comm>(grid_, rank, id);
   // The comm stream runs at the highest priority: its NCCL / peer-push
