@@ -280,6 +280,52 @@ CAGNET_API int cagnet_trainer_profile_reset(cagnet_trainer_t t);
  * the epoch, D2H of the loss (blocking). */
 CAGNET_API int cagnet_trainer_step_host(cagnet_trainer_t t, const float* x_tile,
                                         const int32_t* labels_tile, double* loss);
+/* --- collective seams: RankContext (runtime.hpp:55-96) ----------------------
+ * One rank's communicator for the groups of Strategy{kind, ranks, repl}'s
+ * process grid (grid.hpp:44-81): NCCL with ncclCommSplit per group when id128
+ * came from cagnet_comm_unique_id, the in-process world when it came from
+ * cagnet_comm_local_id (NULL when ranks == 1).  Buffers are device memory;
+ * `stream` is a cudaStream_t (all collectives of one communicator on one
+ * stream, like NCCL).  Every call meters the reference ledger's counters;
+ * singleton groups short-circuit and meter nothing (runtime.cpp:142-184). */
+typedef struct cagnet_comm_s* cagnet_comm_t;
+#define CAGNET_GROUP_WORLD 0
+#define CAGNET_GROUP_ROW 1
+#define CAGNET_GROUP_COL 2
+#define CAGNET_GROUP_FIBER 3
+#define CAGNET_DTYPE_F32 0
+#define CAGNET_DTYPE_F64 1
+#define CAGNET_DTYPE_I32 2
+#define CAGNET_DTYPE_I64 3
+/* category: 0 dbcast, 1 sbcast, 2 reduce, 3 allgather (ledger.hpp:27-33) */
+CAGNET_API int cagnet_comm_create(int kind, int ranks, int repl, int rank, const uint8_t* id128,
+                                  int device, cagnet_comm_t* out);
+/* Members (global ranks, ascending) of this rank's group `which`. */
+CAGNET_API int cagnet_comm_group(cagnet_comm_t c, int which, int* members, int* size);
+/* broadcast (runtime.hpp:64-65): `count` elements in place. */
+CAGNET_API int cagnet_comm_bcast(cagnet_comm_t c, int which, int root_rank, void* buf, int64_t count,
+                                 int dtype, int category, void* stream);
+/* broadcast_csr (runtime.hpp:66-67): the three CSR arrays of the root; ledger payload = nnz. */
+CAGNET_API int cagnet_comm_bcast_csr(cagnet_comm_t c, int which, int root_rank, int64_t* row_ptr,
+                                     int64_t n_rows, int32_t* col_idx, float* vals, int64_t nnz,
+                                     int category, void* stream);
+/* all_reduce / all_reduce_scalar (runtime.hpp:69-73): in-place sum, f32 or f64. */
+CAGNET_API int cagnet_comm_allreduce(cagnet_comm_t c, int which, void* buf, int64_t count, int dtype,
+                                     int category, void* stream);
+/* reduce_scatter_rows (runtime.hpp:75-79): send is sum(row_counts) x cols
+ * (dense); member m receives its row_counts[m] x cols block of the sum. */
+CAGNET_API int cagnet_comm_reduce_scatter_rows(cagnet_comm_t c, int which, const float* send, float* recv,
+                                               const int64_t* row_counts, int64_t cols, int category,
+                                               void* stream);
+/* all_gather_rows (runtime.hpp:81-83): member m contributes row_counts[m] x
+ * cols rows; recv = the blocks concatenated in member order. */
+CAGNET_API int cagnet_comm_allgather_rows(cagnet_comm_t c, int which, const float* send, float* recv,
+                                          const int64_t* row_counts, int64_t cols, int category,
+                                          void* stream);
+/* Ledger counters of this rank, as cagnet_trainer_ledger. */
+CAGNET_API int cagnet_comm_ledger(cagnet_comm_t c, uint64_t* out20);
+CAGNET_API int cagnet_comm_free(cagnet_comm_t c);
+
 /* --- run_distributed → DistOutcome (dist.hpp:138-150, dist_common.cpp:117-222) ---
  * The whole distributed run on the device path: one host thread per rank
  * (SimRuntime::run's thread-per-rank model), each rank a Trainer on its GPU,

@@ -301,6 +301,7 @@ class Ref:
         L.ref_serial_run.argtypes = [vp, vp, C.c_int]
         L.ref_dist_run.restype = vp
         L.ref_dist_run.argtypes = [vp, vp] + [C.c_int] * 6
+        L.ref_collectives_script.argtypes = [C.c_int, C.c_int, C.c_int, _u64p, _f64p, _f64p]
         L.ref_session_create.restype = vp
         L.ref_session_create.argtypes = [vp, vp] + [C.c_int] * 5
         L.ref_session_epoch.restype = C.c_double
@@ -363,6 +364,16 @@ class Ref:
         h = self.lib.ref_dist_run(data.h, model.h, self.KIND[kind], ranks, repl, block, epochs,
                                   sched)
         return RefResult(self, self._check(h), data, model, epochs, ranks=ranks)
+
+    def collectives_script(self, kind, ranks, repl=1):
+        """The collective script of tests/test_gpu_comm.py on SimRuntime:
+        (ledger[cat, rank, 5], reduce_scatter results, all_gather results)."""
+        led = np.zeros(4 * ranks * 5, np.uint64)
+        rs = np.zeros(64 * ranks)
+        ag = np.zeros(64 * ranks)
+        if self.lib.ref_collectives_script(self.KIND[kind], ranks, repl, led, rs, ag) != 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return led.reshape(4, ranks, 5), rs.reshape(ranks, 64), ag.reshape(ranks, 64)
 
     def session(self, data, model, kind, ranks, repl=1, block=0, sched=0):
         """run_distributed split into distribute() once + one call per epoch."""

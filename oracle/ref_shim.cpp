@@ -280,6 +280,73 @@ void* ref_session_outcome(void* sp) {
 }
 void ref_session_free(void* s) { delete static_cast<RefSession*>(s); }
 
+// The collective script of tests/test_gpu_comm.py on the reference's
+// SimRuntime (runtime.cpp): per rank, in order
+//   1 broadcast(row, first member)      DBcast   3 x 5
+//   2 all_reduce(world)                 Reduce   2 x 4
+//   3 all_reduce_scalar(world)          Reduce
+//   4 reduce_scatter_rows(col, {3,1,..}) Reduce  (3 + S-1) x 3
+//   5 all_gather_rows(row)              AllGather (2 rows on member 0, else 1) x 3
+//   6 broadcast_csr(row, last member)   SBcast   3 x 4, nnz 4
+//   7 all_reduce(fiber) (3D only)       Reduce   1 x 3
+// Writes the ledger [category][rank][5] and each rank's step-4 and step-5
+// results (flattened, fixed capacity 64 doubles per rank each).
+int ref_collectives_script(int kind, int ranks, int repl, uint64_t* ledger_out, double* rs_out,
+                           double* ag_out) {
+  return guarded([&] {
+    const Strategy st = make_strategy(kind, ranks, repl, 0);
+    const ProcessGrid grid = make_grid(st);
+    SimRuntime rt(grid, Scheduler::Concurrent);
+    rt.run([&](RankContext& ctx) {
+      const int r = ctx.rank();
+      const Group& row = grid.row_group(r);
+      const Group& col = grid.col_group(r);
+      DenseMatrix m(3, 5);
+      for (std::size_t i = 0; i < m.words(); ++i) m.data()[i] = r + 1 + 0.01 * static_cast<double>(i);
+      DenseMatrix b = ctx.broadcast(row, row.members.front(), r == row.members.front() ? &m : nullptr,
+                                    Category::DBcast);
+      DenseMatrix x(2, 4);
+      for (std::size_t i = 0; i < x.words(); ++i) x.data()[i] = r + 0.5 * static_cast<double>(i);
+      x = ctx.all_reduce(grid.world(), x, Category::Reduce);
+      (void)ctx.all_reduce_scalar(grid.world(), r * 1.5, Category::Reduce);
+      std::vector<int> counts(col.size(), 1);
+      counts[0] = 3;
+      DenseMatrix y(3 + col.size() - 1, 3);
+      for (std::size_t i = 0; i < y.words(); ++i) y.data()[i] = r * 0.25 + static_cast<double>(i);
+      DenseMatrix rs = ctx.reduce_scatter_rows(col, y, counts, Category::Reduce);
+      std::memcpy(rs_out + 64 * r, rs.data(), rs.words() * sizeof(double));
+      DenseMatrix z(row.index_of(r) == 0 ? 2 : 1, 3);
+      for (std::size_t i = 0; i < z.words(); ++i) z.data()[i] = 100.0 * r + static_cast<double>(i);
+      DenseMatrix ag = ctx.all_gather_rows(row, z, Category::AllGather);
+      std::memcpy(ag_out + 64 * r, ag.data(), ag.words() * sizeof(double));
+      CsrMatrix a;
+      a.n_rows = 3;
+      a.n_cols = 4;
+      a.row_ptr = {0, 2, 2, 4};
+      a.col_idx = {0, 3, 1, 2};
+      a.values = {1.0, 2.0, 3.0, 4.0};
+      (void)ctx.broadcast_csr(row, row.members.back(), r == row.members.back() ? &a : nullptr,
+                              Category::SBcast);
+      if (st.kind == StrategyKind::ThreeD) {
+        DenseMatrix f(1, 3);
+        for (std::size_t i = 0; i < f.words(); ++i) f.data()[i] = r;
+        (void)ctx.all_reduce(grid.fiber_group(r), f, Category::Reduce);
+      }
+      (void)b;
+    });
+    for (int c = 0; c < 4; ++c)
+      for (int r = 0; r < ranks; ++r) {
+        const CommCounter& k = rt.ledger().at(static_cast<Category>(c), r);
+        uint64_t* o = ledger_out + (c * ranks + r) * 5;
+        o[0] = k.messages;
+        o[1] = k.words_sent;
+        o[2] = k.words_received;
+        o[3] = k.payload_words;
+        o[4] = k.calls;
+      }
+  });
+}
+
 void ref_result_free(void* r) { delete static_cast<RefResult*>(r); }
 double ref_result_seconds(void* r) { return static_cast<RefResult*>(r)->seconds; }
 void ref_result_losses(void* r, double* out) {

@@ -8,6 +8,7 @@ API over that C-ABI.
 from ._lib import LIB_PATH, CagnetError, InvalidArgument, build, check, lib  # noqa: F401
 from .api import (  # noqa: F401
     CATEGORIES,
+    Comm,
     DeviceCSR,
     DistOutcome,
     GnnModel,

@@ -110,6 +110,15 @@ SIGNATURES = {
     "cagnet_trainer_profile_reset": [vp],
     "cagnet_trainer_step_host": [vp, vp, vp, C.POINTER(f64)],
     "cagnet_kernel_launches": [C.POINTER(u64)],
+    "cagnet_comm_create": [i32, i32, i32, i32, C.c_char_p, i32, C.POINTER(vp)],
+    "cagnet_comm_group": [vp, i32, C.POINTER(i32), C.POINTER(i32)],
+    "cagnet_comm_bcast": [vp, i32, i32, vp, i64, i32, i32, vp],
+    "cagnet_comm_bcast_csr": [vp, i32, i32, vp, i64, vp, vp, i64, i32, vp],
+    "cagnet_comm_allreduce": [vp, i32, vp, i64, i32, i32, vp],
+    "cagnet_comm_reduce_scatter_rows": [vp, i32, vp, vp, _i64p, i64, i32, vp],
+    "cagnet_comm_allgather_rows": [vp, i32, vp, vp, _i64p, i64, i32, vp],
+    "cagnet_comm_ledger": [vp, _u64p],
+    "cagnet_comm_free": [vp],
     "cagnet_run_distributed": [vp, _i64p, i32, _f64p, f64, i32, i32, i32, i32, i32, i32, C.c_uint32,
                                C.POINTER(vp)],
     "cagnet_outcome_info": [vp, _i64p],

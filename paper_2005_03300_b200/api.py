@@ -360,6 +360,68 @@ def comm_local_abort(nid: bytes, why: str) -> None:
     lib.cagnet_comm_local_abort(nid, why.encode())
 
 
+GROUPS = {"world": 0, "row": 1, "col": 2, "fiber": 3}
+DTYPES = {"f32": 0, "f64": 1, "i32": 2, "i64": 3}
+
+
+class Comm:
+    """RankContext (runtime.hpp:55-96): one rank's collectives over the groups
+    of the strategy's process grid, on device buffers (raw pointers) and a
+    CUDA stream handle; NCCL or the in-process world depending on the id."""
+
+    def __init__(self, strat: Strategy, rank: int, comm_id: bytes | None, device: int = 0):
+        out = C.c_void_p()
+        check(lib.cagnet_comm_create(strat.kind_id, strat.ranks, strat.repl, rank, comm_id, device,
+                                     C.byref(out)))
+        self.h, self.rank = out.value, rank
+
+    def group(self, which: str) -> list:
+        members = (C.c_int * 512)()
+        size = C.c_int()
+        check(lib.cagnet_comm_group(self.h, GROUPS[which], members, C.byref(size)))
+        return list(members[:size.value])
+
+    def bcast(self, which, root, ptr, count, dtype="f32", category="dbcast", stream=0):
+        check(lib.cagnet_comm_bcast(self.h, GROUPS[which], root, ptr, count, DTYPES[dtype],
+                                    CATEGORIES.index(category), stream))
+
+    def bcast_csr(self, which, root, row_ptr, n_rows, col_idx, vals, nnz, category="sbcast",
+                  stream=0):
+        check(lib.cagnet_comm_bcast_csr(self.h, GROUPS[which], root, row_ptr, n_rows, col_idx, vals,
+                                        nnz, CATEGORIES.index(category), stream))
+
+    def all_reduce(self, which, ptr, count, dtype="f32", category="reduce", stream=0):
+        check(lib.cagnet_comm_allreduce(self.h, GROUPS[which], ptr, count, DTYPES[dtype],
+                                        CATEGORIES.index(category), stream))
+
+    def reduce_scatter_rows(self, which, send, recv, row_counts, cols, category="reduce", stream=0):
+        check(lib.cagnet_comm_reduce_scatter_rows(self.h, GROUPS[which], send, recv,
+                                                  np.asarray(row_counts, np.int64), cols,
+                                                  CATEGORIES.index(category), stream))
+
+    def all_gather_rows(self, which, send, recv, row_counts, cols, category="allgather", stream=0):
+        check(lib.cagnet_comm_allgather_rows(self.h, GROUPS[which], send, recv,
+                                             np.asarray(row_counts, np.int64), cols,
+                                             CATEGORIES.index(category), stream))
+
+    def ledger(self) -> dict:
+        buf = np.zeros(20, np.uint64)
+        check(lib.cagnet_comm_ledger(self.h, buf))
+        return {c: dict(zip(COUNTER_FIELDS, (int(x) for x in buf[5 * i:5 * i + 5])))
+                for i, c in enumerate(CATEGORIES)}
+
+    def free(self):
+        if self.h:
+            lib.cagnet_comm_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class Trainer:
     """One rank of a partitioned trainer (dist.hpp:83-131) on the dataset's GPU."""
 

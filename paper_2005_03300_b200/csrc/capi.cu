@@ -23,6 +23,13 @@ struct cagnet_dataset_s {
   std::unique_ptr<cagnet::DeviceDataset> data;
   cagnet_csr_s adj, adj_t;
 };
+struct cagnet_comm_s {
+  int device = 0;
+  int rank = 0;
+  cagnet::ProcessGrid grid;
+  std::unique_ptr<cagnet::Comm> comm;
+  cagnet::DevBuf<float> pad_send, pad_recv;
+};
 struct cagnet_outcome_s {
   cagnet::DistOutcome o;
 };
@@ -511,6 +518,175 @@ int cagnet_comm_local_abort(const uint8_t* id128, const char* why) {
     cagnet::LocalId id;
     std::memcpy(&id, id128, sizeof(id));
     cagnet::LocalWorld::abort_id(id, why ? why : "aborted by a rank");
+  });
+}
+
+// ---- collective seams (RankContext, runtime.hpp:55-96) ---------------------------------
+namespace {
+const cagnet::Group& comm_group(cagnet_comm_t c, int which) {
+  switch (which) {
+    case CAGNET_GROUP_WORLD: return c->grid.world();
+    case CAGNET_GROUP_ROW: return c->grid.row_group(c->rank);
+    case CAGNET_GROUP_COL: return c->grid.col_group(c->rank);
+    case CAGNET_GROUP_FIBER: return c->grid.fiber_group(c->rank);
+    default: throw std::invalid_argument("comm: unknown group " + std::to_string(which));
+  }
+}
+ncclDataType_t nccl_dtype(int dtype) {
+  switch (dtype) {
+    case CAGNET_DTYPE_F32: return ncclFloat32;
+    case CAGNET_DTYPE_F64: return ncclFloat64;
+    case CAGNET_DTYPE_I32: return ncclInt32;
+    case CAGNET_DTYPE_I64: return ncclInt64;
+    default: throw std::invalid_argument("comm: unknown dtype " + std::to_string(dtype));
+  }
+}
+cagnet::Category comm_category(int c) {
+  if (c < 0 || c >= cagnet::kNumCategories) throw std::invalid_argument("comm: unknown category");
+  return static_cast<cagnet::Category>(c);
+}
+}  // namespace
+
+int cagnet_comm_create(int kind, int ranks, int repl, int rank, const uint8_t* id128, int device,
+                       cagnet_comm_t* out) {
+  return guarded([&] {
+    set_device(device);
+    auto c = std::make_unique<cagnet_comm_s>();
+    c->device = device;
+    c->rank = rank;
+    c->grid = cagnet::ProcessGrid::make(make_strategy(kind, ranks, repl, 0));
+    cagnet::require(rank >= 0 && rank < c->grid.ranks(), "comm: rank outside the grid");
+    ncclUniqueId id;
+    if (id128) std::memcpy(&id, id128, sizeof(id));
+    c->comm = std::make_unique<cagnet::Comm>(c->grid, rank, id128 ? &id : nullptr);
+    *out = c.release();
+  });
+}
+
+int cagnet_comm_group(cagnet_comm_t c, int which, int* members, int* size) {
+  return guarded([&] {
+    const cagnet::Group& g = comm_group(c, which);
+    *size = static_cast<int>(g.size());
+    if (members)
+      for (size_t i = 0; i < g.size(); ++i) members[i] = g.members[i];
+  });
+}
+
+int cagnet_comm_bcast(cagnet_comm_t c, int which, int root_rank, void* buf, int64_t count, int dtype,
+                      int category, void* stream) {
+  return guarded([&] {
+    set_device(c->device);
+    cagnet::require(count >= 0, "broadcast: negative count");
+    c->comm->bcast(comm_group(c, which), root_rank, buf, static_cast<size_t>(count), nccl_dtype(dtype),
+                   comm_category(category), static_cast<uint64_t>(count), as_stream(stream));
+  });
+}
+
+int cagnet_comm_bcast_csr(cagnet_comm_t c, int which, int root_rank, int64_t* row_ptr, int64_t n_rows,
+                          int32_t* col_idx, float* vals, int64_t nnz, int category, void* stream) {
+  return guarded([&] {
+    set_device(c->device);
+    cagnet::require(n_rows >= 0 && nnz >= 0, "broadcast_csr: negative size");
+    c->comm->bcast_csr(comm_group(c, which), root_rank, row_ptr, n_rows, col_idx, vals, nnz,
+                       comm_category(category), as_stream(stream));
+  });
+}
+
+int cagnet_comm_allreduce(cagnet_comm_t c, int which, void* buf, int64_t count, int dtype, int category,
+                          void* stream) {
+  return guarded([&] {
+    set_device(c->device);
+    cagnet::require(dtype == CAGNET_DTYPE_F32 || dtype == CAGNET_DTYPE_F64, "all_reduce: f32 or f64 only");
+    c->comm->all_reduce(comm_group(c, which), buf, static_cast<size_t>(count), nccl_dtype(dtype),
+                        comm_category(category), static_cast<uint64_t>(count), as_stream(stream));
+  });
+}
+
+// Member-ordered row blocks of unequal heights move through equal padded
+// slots (max rows per member), like every other reduce-scatter / all-gather
+// of the library; the ledger counts the logical rows x cols per member.
+int cagnet_comm_reduce_scatter_rows(cagnet_comm_t c, int which, const float* send, float* recv,
+                                    const int64_t* row_counts, int64_t cols, int category, void* stream) {
+  return guarded([&] {
+    set_device(c->device);
+    const cagnet::Group& g = comm_group(c, which);
+    const cagnet::Category cat = comm_category(category);
+    const cudaStream_t s = as_stream(stream);
+    const int m = g.index_of(c->rank);
+    int64_t maxr = 0, off = 0, mine_off = 0;
+    std::vector<uint64_t> words;
+    for (size_t q = 0; q < g.size(); ++q) {
+      cagnet::require(row_counts[q] >= 0, "reduce_scatter_rows: negative row count");
+      maxr = std::max(maxr, row_counts[q]);
+      words.push_back(static_cast<uint64_t>(row_counts[q] * cols));
+    }
+    const size_t slot = static_cast<size_t>(maxr * cols);
+    c->pad_send.resize(std::max<size_t>(slot * g.size(), 1));
+    c->pad_recv.resize(std::max<size_t>(slot, 1));
+    cagnet::kern::zero_bytes(c->pad_send.get(), slot * g.size() * sizeof(float), s);
+    for (size_t q = 0; q < g.size(); ++q) {
+      if (static_cast<int>(q) == m) mine_off = off;
+      cagnet::kern::copy_bytes(c->pad_send.get() + q * slot, send + off * cols,
+                               static_cast<size_t>(row_counts[q] * cols) * sizeof(float), s);
+      off += row_counts[q];
+    }
+    (void)mine_off;
+    if (g.size() == 1) {
+      cagnet::kern::copy_bytes(recv, send, static_cast<size_t>(row_counts[0] * cols) * sizeof(float), s);
+      return;
+    }
+    c->comm->reduce_scatter(g, c->pad_send.get(), c->pad_recv.get(), slot, ncclFloat32, cat, words, s);
+    cagnet::kern::copy_bytes(recv, c->pad_recv.get(), static_cast<size_t>(row_counts[m] * cols) * sizeof(float), s);
+  });
+}
+
+int cagnet_comm_allgather_rows(cagnet_comm_t c, int which, const float* send, float* recv,
+                               const int64_t* row_counts, int64_t cols, int category, void* stream) {
+  return guarded([&] {
+    set_device(c->device);
+    const cagnet::Group& g = comm_group(c, which);
+    const cagnet::Category cat = comm_category(category);
+    const cudaStream_t s = as_stream(stream);
+    const int m = g.index_of(c->rank);
+    int64_t maxr = 0;
+    std::vector<uint64_t> words;
+    for (size_t q = 0; q < g.size(); ++q) {
+      cagnet::require(row_counts[q] >= 0, "all_gather_rows: negative row count");
+      maxr = std::max(maxr, row_counts[q]);
+      words.push_back(static_cast<uint64_t>(row_counts[q] * cols));
+    }
+    if (g.size() == 1) {
+      cagnet::kern::copy_bytes(recv, send, static_cast<size_t>(row_counts[0] * cols) * sizeof(float), s);
+      return;
+    }
+    const size_t slot = static_cast<size_t>(maxr * cols);
+    c->pad_send.resize(std::max<size_t>(slot, 1));
+    c->pad_recv.resize(std::max<size_t>(slot * g.size(), 1));
+    cagnet::kern::copy_bytes(c->pad_send.get(), send, static_cast<size_t>(row_counts[m] * cols) * sizeof(float), s);
+    c->comm->all_gather(g, c->pad_send.get(), c->pad_recv.get(), slot, ncclFloat32, cat, words, s);
+    int64_t off = 0;
+    for (size_t q = 0; q < g.size(); ++q) {
+      cagnet::kern::copy_bytes(recv + off * cols, c->pad_recv.get() + q * slot,
+                               static_cast<size_t>(row_counts[q] * cols) * sizeof(float), s);
+      off += row_counts[q];
+    }
+  });
+}
+
+int cagnet_comm_ledger(cagnet_comm_t c, uint64_t* out20) {
+  return guarded([&] {
+    for (int k = 0; k < cagnet::kNumCategories; ++k) {
+      const cagnet::CommCounter& x = c->comm->counter(static_cast<cagnet::Category>(k));
+      const uint64_t v[5] = {x.messages, x.words_sent, x.words_received, x.payload_words, x.calls};
+      std::memcpy(out20 + 5 * k, v, sizeof(v));
+    }
+  });
+}
+
+int cagnet_comm_free(cagnet_comm_t c) {
+  return guarded([&] {
+    if (c) set_device(c->device);
+    delete c;
   });
 }
 
