@@ -366,6 +366,25 @@ CAGNET_API int cagnet_outcome_prereduction_totals(cagnet_outcome_t o, uint64_t* 
 CAGNET_API int cagnet_outcome_memory_peaks(cagnet_outcome_t o, uint64_t* out /* ranks */);
 CAGNET_API int cagnet_outcome_free(cagnet_outcome_t o);
 
+/* --- analytic communication model (cost.hpp:27-115, cost.cpp:48-161) ---------
+ * params6 = {n, nnz, f, layers, ranks, repl}.  out6 = {words, messages, term0,
+ * term1, term2, #terms} per rank per epoch; terms: 1D {embedding_broadcast,
+ * weight_gradient_reduce}, 1.5D {embedding_broadcast, partial_reduce}, 2D
+ * {dense_panels, sparse_panels, weight_gradient_gather}, 3D {sparse_panels,
+ * dense_panels}.  Invalid shapes -> CAGNET_EINVAL with the reference's message. */
+CAGNET_API int cagnet_cost_predict(int kind, const int64_t* params6, int64_t* out6);
+CAGNET_API int cagnet_cost_ceil_lg(int64_t p, int64_t* out);
+CAGNET_API int cagnet_cost_2d_rect_layer(const int64_t* params6, int64_t p_rows, int64_t p_cols,
+                                         double alpha, double beta, double* out);
+/* out4 = {serial, repl15d, repl15d_single_adj, split3d_peak} words. */
+CAGNET_API int cagnet_cost_memory(int64_t n, int64_t nnz, int64_t f, int64_t fmax, int64_t dims,
+                                  int64_t repl, int64_t ranks, int64_t* out4);
+/* compare_cost: ledgers = ranks x 20 counters (cagnet_*_ledger layout) of a
+ * run of `epochs` epochs.  out4 = {predicted_words, extra_words,
+ * measured_words, ratio}; flags3 = {exact, degenerate, within_band}. */
+CAGNET_API int cagnet_cost_compare(int kind, const int64_t* params6, const uint64_t* ledgers, int ranks,
+                                   int epochs, double* out4, int* flags3);
+
 /* Total hot-path kernel launches issued by this library so far. */
 CAGNET_API int cagnet_kernel_launches(uint64_t* out);
 /* The compute stream the trainer launches on (a cudaStream_t). */

@@ -9,6 +9,12 @@ from ._lib import LIB_PATH, CagnetError, InvalidArgument, build, check, lib  # n
 from .api import (  # noqa: F401
     CATEGORIES,
     Comm,
+    CostParams,
+    ceil_lg,
+    compare_cost,
+    memory_footprints,
+    predict_2d_rect_layer,
+    predict_cost,
     DeviceCSR,
     DistOutcome,
     GnnModel,

@@ -119,6 +119,11 @@ SIGNATURES = {
     "cagnet_comm_allgather_rows": [vp, i32, vp, vp, _i64p, i64, i32, vp],
     "cagnet_comm_ledger": [vp, _u64p],
     "cagnet_comm_free": [vp],
+    "cagnet_cost_predict": [i32, _i64p, _i64p],
+    "cagnet_cost_ceil_lg": [i64, C.POINTER(i64)],
+    "cagnet_cost_2d_rect_layer": [_i64p, i64, i64, f64, f64, C.POINTER(f64)],
+    "cagnet_cost_memory": [i64, i64, i64, i64, i64, i64, i64, _i64p],
+    "cagnet_cost_compare": [i32, _i64p, _u64p, i32, i32, _f64p, _i32p],
     "cagnet_run_distributed": [vp, _i64p, i32, _f64p, f64, i32, i32, i32, i32, i32, i32, C.c_uint32,
                                C.POINTER(vp)],
     "cagnet_outcome_info": [vp, _i64p],

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import InvalidArgument, check, lib
+from ._lib import CagnetError, InvalidArgument, check, lib  # noqa: F401
 
 KINDS = {"1d": 0, "1.5d": 1, "2d": 2, "3d": 3}
 KIND_NAMES = {v: k for k, v in KINDS.items()}
@@ -696,3 +696,71 @@ def run_distributed(data, model: GnnModel, strat: Strategy, epochs: int,
                        GnnModel([int(d) for d in dims], ws, model.learning_rate), ledgers,
                        epoch_us / 1000.0, pre[:n_pre], peaks[:P],
                        {v: k for k, v in BACKENDS.items()}[backend])
+
+
+# ---------------------------------------------------------------------------
+# analytic communication model (cost.hpp:27-115, cost.cpp:48-161)
+# ---------------------------------------------------------------------------
+COST_TERMS = {"1d": ("embedding_broadcast", "weight_gradient_reduce"),
+              "1.5d": ("embedding_broadcast", "partial_reduce"),
+              "2d": ("dense_panels", "sparse_panels", "weight_gradient_gather"),
+              "3d": ("sparse_panels", "dense_panels")}
+
+
+@dataclass
+class CostParams:
+    """cost.hpp:33-40: n, nnz, uniform width f, L graph convolutions, P, c."""
+    n: int
+    nnz: int
+    f: int
+    layers: int
+    ranks: int = 1
+    repl: int = 1
+
+    def array(self) -> np.ndarray:
+        return np.array([self.n, self.nnz, self.f, self.layers, self.ranks, self.repl], np.int64)
+
+
+def ceil_lg(p: int) -> int:
+    v = C.c_int64()
+    check(lib.cagnet_cost_ceil_lg(p, C.byref(v)))
+    return int(v.value)
+
+
+def predict_cost(kind: str, params: CostParams) -> dict:
+    """predict_{1d,15d,2d,3d} (cost.cpp:48-85): per-rank words / messages per
+    epoch and the word terms (which sum to words)."""
+    out = np.zeros(6, np.int64)
+    check(lib.cagnet_cost_predict(KINDS[kind], params.array(), out))
+    return {"words": int(out[0]), "messages": int(out[1]),
+            "terms": dict(zip(COST_TERMS[kind], (int(x) for x in out[2:2 + int(out[5])])))}
+
+
+def predict_2d_rect_layer(params: CostParams, p_rows: int, p_cols: int, alpha: float,
+                          beta: float) -> float:
+    v = C.c_double()
+    check(lib.cagnet_cost_2d_rect_layer(params.array(), p_rows, p_cols, alpha, beta, C.byref(v)))
+    return v.value
+
+
+def memory_footprints(n, nnz, f, fmax, dims, repl, ranks) -> dict:
+    out = np.zeros(4, np.int64)
+    check(lib.cagnet_cost_memory(n, nnz, f, fmax, dims, repl, ranks, out))
+    return dict(zip(("serial", "repl15d", "repl15d_single_adj", "split3d_peak"), (int(x) for x in out)))
+
+
+def compare_cost(strat: Strategy, params: CostParams, ledgers: list, epochs: int) -> dict:
+    """compare_cost (cost.cpp:115-161): the metered payload words per rank per
+    epoch against the closed form; ledgers = per-rank dicts as Trainer.ledger()."""
+    P = len(ledgers)
+    buf = np.zeros(max(P, 1) * 20, np.uint64)
+    for r, led in enumerate(ledgers):
+        for i, c in enumerate(CATEGORIES):
+            for j, fld in enumerate(COUNTER_FIELDS):
+                buf[r * 20 + i * 5 + j] = led[c][fld]
+    out = np.zeros(4)
+    flags = np.zeros(3, np.int32)
+    check(lib.cagnet_cost_compare(strat.kind_id, params.array(), buf, P, epochs, out, flags))
+    return {"strategy": strat.kind, "predicted_words": int(out[0]), "extra_words": int(out[1]),
+            "measured_words": float(out[2]), "ratio": float(out[3]), "exact": bool(flags[0]),
+            "degenerate": bool(flags[1]), "within_band": bool(flags[2])}

@@ -12,6 +12,7 @@
 
 #include "kernels.cuh"
 #include "rng.hpp"
+#include "cost.hpp"
 #include "run.hpp"
 #include "trainer.hpp"
 
@@ -687,6 +688,64 @@ int cagnet_comm_free(cagnet_comm_t c) {
   return guarded([&] {
     if (c) set_device(c->device);
     delete c;
+  });
+}
+
+// ---- analytic communication model ------------------------------------------------------
+namespace {
+cagnet::cost::Params cost_params(const int64_t* p6) {
+  cagnet::require(p6 != nullptr, "cost model: null parameters");
+  return cagnet::cost::Params{p6[0], p6[1], p6[2], p6[3], p6[4], p6[5]};
+}
+cagnet::StrategyKind cost_kind(int kind) {
+  cagnet::require(kind >= 0 && kind <= 3, "strategy: unknown kind");
+  return static_cast<cagnet::StrategyKind>(kind);
+}
+}  // namespace
+
+int cagnet_cost_predict(int kind, const int64_t* params6, int64_t* out6) {
+  return guarded([&] {
+    const cagnet::cost::Prediction p = cagnet::cost::predict(cost_kind(kind), cost_params(params6));
+    int64_t v[6] = {p.words, p.messages, 0, 0, 0, static_cast<int64_t>(p.terms.size())};
+    for (size_t i = 0; i < p.terms.size() && i < 3; ++i) v[2 + i] = p.terms[i].second;
+    std::memcpy(out6, v, sizeof(v));
+  });
+}
+
+int cagnet_cost_ceil_lg(int64_t p, int64_t* out) {
+  return guarded([&] { *out = cagnet::cost::ceil_lg(p); });
+}
+
+int cagnet_cost_2d_rect_layer(const int64_t* params6, int64_t p_rows, int64_t p_cols, double alpha, double beta,
+                              double* out) {
+  return guarded([&] { *out = cagnet::cost::rect_layer(cost_params(params6), p_rows, p_cols, alpha, beta); });
+}
+
+int cagnet_cost_memory(int64_t n, int64_t nnz, int64_t f, int64_t fmax, int64_t dims, int64_t repl, int64_t ranks,
+                       int64_t* out4) {
+  return guarded([&] {
+    const cagnet::cost::Footprints m = cagnet::cost::footprints(n, nnz, f, fmax, dims, repl, ranks);
+    const int64_t v[4] = {m.serial, m.repl15d, m.repl15d_single_adj, m.split3d_peak};
+    std::memcpy(out4, v, sizeof(v));
+  });
+}
+
+int cagnet_cost_compare(int kind, const int64_t* params6, const uint64_t* ledgers, int ranks, int epochs,
+                        double* out4, int* flags3) {
+  return guarded([&] {
+    cagnet::require(ranks >= 1 && ledgers != nullptr, "compare_cost: no ledger");
+    uint64_t payload = 0;
+    for (int r = 0; r < ranks; ++r)
+      for (int c = 0; c < cagnet::kNumCategories; ++c) payload += ledgers[r * 20 + c * 5 + 3];
+    const cagnet::cost::Comparison c =
+        cagnet::cost::compare(cost_kind(kind), cost_params(params6), payload, ranks, epochs);
+    out4[0] = static_cast<double>(c.predicted_words);
+    out4[1] = static_cast<double>(c.extra_words);
+    out4[2] = c.measured_words;
+    out4[3] = c.ratio;
+    flags3[0] = c.exact;
+    flags3[1] = c.degenerate;
+    flags3[2] = c.within_band;
   });
 }
 

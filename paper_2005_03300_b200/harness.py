@@ -160,7 +160,17 @@ def run_report(cfg: ExperimentConfig) -> dict:
     report["h_final_norm"] = _frobenius(out.h_final)
     report["weight_norms"] = [_frobenius(w) for w in out.model.weights]
     report["ledger"] = ledger_report(out.ledger, cfg.strategy)
+    report["prereduction_totals"] = [int(x) for x in out.prereduction_totals]
+    report["memory_peaks"] = [int(x) for x in out.memory_peaks]
     s = cfg.strategy
+    # B200 extension: the metered traffic against the analytic model
+    # (compare_cost, cost.cpp:115-161) at the config's widest layer.
+    params = api.CostParams(data.n, data.nnz, max(cfg.layer_dims), len(cfg.layer_dims) - 1, s.ranks,
+                            s.repl)
+    try:
+        report["cost_model"] = api.compare_cost(s, params, out.ledger, cfg.epochs)
+    except api.CagnetError as e:
+        report["cost_model"] = {"unavailable": str(e)}
     report["b200"] = {"last_epoch_ms": out.epoch_ms, "ranks": s.ranks,
                       "reassociate": s.reassociate, "fuse": s.fuse, "cuda_graph": s.graph,
                       "p2p": s.p2p, "resident_sparse": s.resident_sparse}
