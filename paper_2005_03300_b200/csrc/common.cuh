@@ -110,4 +110,11 @@ struct DevBuf {
   T* get() const { return ptr; }
 };
 
+// Per-stream device workspace (split-K partials, loss partials): grows on
+// demand outside graph capture and is reused by every later call on the same
+// stream (stream order makes the reuse safe), so eager epochs do no
+// allocation churn and captured graphs reference a fixed address.  Never
+// shrinks; lives until process exit.
+void* stream_scratch(cudaStream_t s, size_t bytes);
+
 }  // namespace cagnet

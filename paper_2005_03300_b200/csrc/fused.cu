@@ -2,6 +2,9 @@
 // the small layout helpers the partition layer needs (strided copies,
 // transposes).  All are HBM-streaming kernels.
 #include "common.cuh"
+#include <map>
+#include <mutex>
+
 #include "kernels.cuh"
 
 namespace cagnet {
@@ -192,8 +195,7 @@ void launch_lsm(const RowBlocks& zb, int64_t rows, int c0, int c1, float* logp, 
     blocks = ceil_div64(rows > 0 ? rows : 1, 8);
     if (blocks > 4 * sms) blocks = 4 * sms;
   }
-  double* partials = nullptr;
-  CG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&partials), blocks * sizeof(double), s));
+  double* partials = static_cast<double*>(stream_scratch(s, blocks * sizeof(double)));
   if (cols <= 8 * 32) {
     if (tpr == 8)
       launch_lsm_rows<8>(zb, rows, c0, c1, logp, ldl, G, ldg, labels, mask, inv, partials, blocks, s);
@@ -208,7 +210,6 @@ void launch_lsm(const RowBlocks& zb, int64_t rows, int c0, int c1, float* logp, 
     sum_partials_kernel<<<1, 256, 0, s>>>(partials, static_cast<int>(blocks), loss_out);
     CG_LAUNCH_CHECK();
   }
-  CG_CUDA(cudaFreeAsync(partials, s));
 }
 
 // (row, col) of flat element e; 32-bit division whenever the extent allows.
@@ -454,4 +455,29 @@ void f64_to_f32(const double* src, float* dst, int64_t count, cudaStream_t strea
 }
 
 }  // namespace kern
+
+void* stream_scratch(cudaStream_t s, size_t bytes) {
+  struct Entry {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  static std::mutex mu;
+  static std::map<cudaStream_t, Entry> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  Entry& e = cache[s];
+  if (e.bytes >= bytes && e.p) return e.p;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  CG_CUDA(cudaStreamIsCapturing(s, &st));
+  if (st != cudaStreamCaptureStatusNone)
+    throw std::logic_error("stream_scratch: workspace growth inside a graph capture");
+  if (e.p) {
+    CG_CUDA(cudaStreamSynchronize(s));
+    CG_CUDA(cudaFree(e.p));
+  }
+  const size_t want = bytes + bytes / 4 + 256;
+  CG_CUDA(cudaMalloc(&e.p, want));
+  e.bytes = want;
+  return e.p;
+}
+
 }  // namespace cagnet

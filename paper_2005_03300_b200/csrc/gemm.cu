@@ -387,8 +387,7 @@ void gemm_tf32x3(const GemmDesc& d, cudaStream_t stream) {
 
   float* work = nullptr;
   if (splits > 1) {
-    CG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&work),
-                            static_cast<size_t>(splits) * d.m * d.n * sizeof(float), stream));
+    work = static_cast<float*>(stream_scratch(stream, static_cast<size_t>(splits) * d.m * d.n * sizeof(float)));
     p.partial = work;
   }
   const int amode = pick_mode(d.A, d.a_sm, d.a_sk);
@@ -406,7 +405,6 @@ void gemm_tf32x3(const GemmDesc& d, cudaStream_t stream) {
                                                                           : 4 * sms);
     splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(p, static_cast<int>(splits));
     CG_LAUNCH_CHECK();
-    CG_CUDA(cudaFreeAsync(work, stream));
   }
 }
 

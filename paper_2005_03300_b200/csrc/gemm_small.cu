@@ -128,6 +128,108 @@ __global__ void __launch_bounds__(kRowThreads) gemm_rows_small_kernel(const Gemm
   }
 }
 
+// k <= 16, n <= 16, 16 B-aligned rows: a quad of lanes per row, every lane
+// loading ONE float4 of its row (a warp instruction moves 8 whole rows, 512
+// contiguous bytes) instead of the team-wide whole-row broadcast loads above,
+// which cost one L1 wavefront per row per vector (LSU-bound at 98 %).  Lane q
+// multiplies its k-slice [4q, 4q + 4) by B's matching rows (slices in shared
+// memory at bank offsets 8q, conflict-free) into 16 partial outputs, then a
+// two-round butterfly reduce-scatter (xor 2: keep 8 columns, xor 1: keep 4)
+// leaves lane q with columns [4q, 4q + 4) summed over the row, stored as one
+// float4.  Sum order: slices in fixed butterfly order (deterministic).
+constexpr int kQuadSlice = 72;  // floats per k-slice of B (64 + 8 bank shift)
+template <int R>
+__global__ void __launch_bounds__(kRowThreads) gemm_rows_quad_kernel(const GemmDesc d) {
+  __shared__ __align__(16) float Bs[4 * kQuadSlice];
+  const int k = static_cast<int>(d.k), n = static_cast<int>(d.n);
+  for (int e = threadIdx.x; e < 4 * kQuadSlice; e += blockDim.x) {
+    const int q = e / kQuadSlice, w = e % kQuadSlice, i = w / 16, j = w % 16;
+    const int kk = 4 * q + i;
+    Bs[e] = (w < 64 && kk < k && j < n) ? d.B[kk * d.b_sk + j * d.b_sn] : 0.f;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, q = lane & 3;
+  const float* bq = Bs + q * kQuadSlice;
+  const bool live_k = 4 * q < k;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kRowThreads / 32);
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * kRowThreads + threadIdx.x) >> 5;
+  for (int64_t base = warp * 8 * R; base < d.m; base += warps * 8 * R) {
+    float4 a[R];
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int64_t r = base + u * 8 + (lane >> 2);
+      a[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < d.m && live_k) a[u] = __ldg(reinterpret_cast<const float4*>(d.A + r * d.a_sm) + q);
+      // junk past k inside the last vector contributes nothing
+      if (4 * q + 1 >= k) a[u].y = 0.f;
+      if (4 * q + 2 >= k) a[u].z = 0.f;
+      if (4 * q + 3 >= k) a[u].w = 0.f;
+      if (4 * q >= k) a[u].x = 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      float p[16];
+#pragma unroll
+      for (int j4 = 0; j4 < 4; ++j4) {
+        const float4 b0 = *reinterpret_cast<const float4*>(bq + 0 * 16 + 4 * j4);
+        const float4 b1 = *reinterpret_cast<const float4*>(bq + 1 * 16 + 4 * j4);
+        const float4 b2 = *reinterpret_cast<const float4*>(bq + 2 * 16 + 4 * j4);
+        const float4 b3 = *reinterpret_cast<const float4*>(bq + 3 * 16 + 4 * j4);
+        p[4 * j4 + 0] = fmaf(a[u].w, b3.x, fmaf(a[u].z, b2.x, fmaf(a[u].y, b1.x, a[u].x * b0.x)));
+        p[4 * j4 + 1] = fmaf(a[u].w, b3.y, fmaf(a[u].z, b2.y, fmaf(a[u].y, b1.y, a[u].x * b0.y)));
+        p[4 * j4 + 2] = fmaf(a[u].w, b3.z, fmaf(a[u].z, b2.z, fmaf(a[u].y, b1.z, a[u].x * b0.z)));
+        p[4 * j4 + 3] = fmaf(a[u].w, b3.w, fmaf(a[u].z, b2.w, fmaf(a[u].y, b1.w, a[u].x * b0.w)));
+      }
+      // xor 2: lane keeps columns [8 (q >> 1), +8)
+      const bool hi = (q >> 1) != 0;
+      float h[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const float send = hi ? p[t] : p[8 + t];
+        const float keep = hi ? p[8 + t] : p[t];
+        h[t] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+      // xor 1: lane keeps columns [4q, 4q + 4)
+      const bool odd = (q & 1) != 0;
+      float c[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float send = odd ? h[t] : h[4 + t];
+        const float keep = odd ? h[4 + t] : h[t];
+        c[t] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+      }
+      const int64_t r = base + u * 8 + (lane >> 2);
+      const int c0 = 4 * q;
+      if (r >= d.m || c0 >= n) continue;
+      float4 v = make_float4(c[0], c[1], c[2], c[3]);
+      float* cr = d.C + r * d.ldc + c0;
+      if (d.accumulate) {
+        const float4 o = *reinterpret_cast<const float4*>(cr);
+        v.x += o.x;
+        v.y += o.y;
+        v.z += o.z;
+        v.w += o.w;
+      }
+      if (d.epilogue == EPI_RELU && d.aux_out) {
+        *reinterpret_cast<float4*>(d.aux_out + r * d.ldao + c0) =
+            make_float4(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f), fmaxf(v.z, 0.f), fmaxf(v.w, 0.f));
+      } else if (d.epilogue == EPI_RELU_PRIME) {
+        const float4 z = __ldg(reinterpret_cast<const float4*>(d.aux + r * d.ldaux + c0));
+        v.x = z.x > 0.f ? v.x : v.x * 0.f;
+        v.y = z.y > 0.f ? v.y : v.y * 0.f;
+        v.z = z.z > 0.f ? v.z : v.z * 0.f;
+        v.w = z.w > 0.f ? v.w : v.w * 0.f;
+      }
+      if (c0 + 4 <= n) {
+        *reinterpret_cast<float4*>(cr) = v;
+      } else {
+        const float cv[4] = {v.x, v.y, v.z, v.w};
+        for (int t = 0; t < n - c0; ++t) cr[t] = cv[t];
+      }
+    }
+  }
+}
+
 template <int LV, int NG, int R>
 void launch_rows(const GemmDesc& d, bool vec, unsigned blocks, cudaStream_t s) {
   if (d.k <= 16) {
@@ -298,6 +400,12 @@ void launch_tn_mi(int mi, const GemmDesc& d, int blocks, int64_t rpw, float* par
 
 bool aligned16(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
 
+// CAGNET_GEMM_QUAD=0 keeps the row-team kernel for k, n <= 16 (comparison).
+bool quad_enabled() {
+  const char* e = std::getenv("CAGNET_GEMM_QUAD");
+  return !(e && e[0] == '0');
+}
+
 // CAGNET_GEMM_SMALL=0 routes these shapes back to the tensor-core kernels.
 bool small_enabled() {
   static const bool on = [] {
@@ -326,6 +434,25 @@ bool gemm_small_try(const GemmDesc& d, cudaStream_t s) {
   const int sms = num_sms(current_device());
   if (d.k <= 32 && d.n <= 256 && d.m >= kMinRows) {
     const bool vec = d.a_sk == 1 && d.a_sm % 4 == 0 && aligned16(d.A) && d.a_sm >= ((d.k + 3) / 4) * 4;
+    const bool cvec = d.ldc % 4 == 0 && aligned16(d.C) &&
+                      (d.epilogue != EPI_RELU || !d.aux_out || (d.ldao % 4 == 0 && aligned16(d.aux_out))) &&
+                      (d.epilogue != EPI_RELU_PRIME || (d.ldaux % 4 == 0 && aligned16(d.aux)));
+    if (vec && cvec && d.k <= 16 && d.n <= 16 && quad_enabled()) {
+      static const int R = [] {
+        const char* e = std::getenv("CAGNET_GEMM_QUAD_R");  // rows in flight per lane (measured: 4 best)
+        return e ? std::atoi(e) : 4;
+      }();
+      const int64_t want = ceil_div64(ceil_div64(d.m, 8 * R), kRowThreads / 32);
+      const unsigned blocks = static_cast<unsigned>(want < 16LL * sms ? want : 16LL * sms);
+      if (R >= 4)
+        gemm_rows_quad_kernel<4><<<blocks, kRowThreads, 0, s>>>(d);
+      else if (R == 1)
+        gemm_rows_quad_kernel<1><<<blocks, kRowThreads, 0, s>>>(d);
+      else
+        gemm_rows_quad_kernel<2><<<blocks, kRowThreads, 0, s>>>(d);
+      CG_LAUNCH_CHECK();
+      return true;
+    }
     const int lv = d.n <= 16 ? 4 : 8;
     const int ng = d.n <= 32 ? 1 : d.n <= 64 ? 2 : d.n <= 128 ? 4 : 8;
     const int r = ng == 1 ? 2 : 1;
@@ -364,8 +491,7 @@ bool gemm_small_try(const GemmDesc& d, cudaStream_t s) {
       const int64_t scap = ceil_div64(d.k, 4LL * kTile);
       if (sblocks > scap) sblocks = static_cast<int>(scap < 1 ? 1 : scap);
       const int64_t rpb = ceil_div64(d.k, sblocks);
-      CG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part),
-                              static_cast<size_t>(sblocks) * d.m * d.n * sizeof(float), s));
+      part = static_cast<float*>(stream_scratch(s, static_cast<size_t>(sblocks) * d.m * d.n * sizeof(float)));
       auto go = [&](auto kern) {
         CG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         kern<<<sblocks, kTnThreads, smem, s>>>(d, rpb, part, mp, np);
@@ -386,11 +512,9 @@ bool gemm_small_try(const GemmDesc& d, cudaStream_t s) {
       CG_LAUNCH_CHECK();
       gemm_tn_fold_kernel<<<static_cast<unsigned>(ceil_div64(d.m * d.n, 256)), 256, 0, s>>>(d, part, sblocks);
       CG_LAUNCH_CHECK();
-      CG_CUDA(cudaFreeAsync(part, s));
       return true;
     }
-    CG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&part),
-                            static_cast<size_t>(blocks) * d.m * d.n * sizeof(float), s));
+    part = static_cast<float*>(stream_scratch(s, static_cast<size_t>(blocks) * d.m * d.n * sizeof(float)));
     switch (nt) {
       case 4: launch_tn_mi<4>(mi, d, blocks, rpw, part, s); break;
       case 8: launch_tn_mi<8>(mi, d, blocks, rpw, part, s); break;
@@ -400,7 +524,6 @@ bool gemm_small_try(const GemmDesc& d, cudaStream_t s) {
     CG_LAUNCH_CHECK();
     gemm_tn_fold_kernel<<<static_cast<unsigned>(ceil_div64(d.m * d.n, 256)), 256, 0, s>>>(d, part, blocks);
     CG_LAUNCH_CHECK();
-    CG_CUDA(cudaFreeAsync(part, s));
     return true;
   }
   return false;

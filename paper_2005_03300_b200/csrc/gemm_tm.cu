@@ -884,8 +884,8 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
     p.chains = p.k_chunk / BK >= 2 ? (bn <= 16 ? 4 : bn <= 48 ? 2 : 1) : 1;
     float* work = nullptr;
     if (splits > 1) {
-      CG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&work),
-                              static_cast<size_t>(splits) * p.mpad * p.pld * sizeof(float), stream));
+      work = static_cast<float*>(
+          stream_scratch(stream, static_cast<size_t>(splits) * p.mpad * p.pld * sizeof(float)));
       p.partial = work;
       p.tstore = encode_2d(&maps.c, work, static_cast<uint64_t>(d.n),
                            static_cast<uint64_t>(splits * p.mpad), static_cast<uint64_t>(p.pld),
@@ -904,7 +904,6 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
       const int blocks = static_cast<int>(ceil_div64(total, 8) < 8 * sms ? ceil_div64(total, 8) : 8 * sms);
       tm_reduce_kernel<<<blocks, 256, 0, stream>>>(p, static_cast<int>(splits));
       CG_LAUNCH_CHECK();
-      CG_CUDA(cudaFreeAsync(work, stream));
     }
     return true;
   }

@@ -199,7 +199,10 @@ TM_CASES = [
     (30000, 24, 16, 0, 1),     # S·Wᵀ (16 -> 24)
     (16, 16, 70000, 1, 0),     # Hᵀ·S, the 16-wide weight gradient
     # >= 1 M rows: the CUDA-core narrow x narrow kernels (gemm_small.cu)
-    (1000003, 16, 16, 0, 0),   # H·W (16 -> 16), Amazon / Protein hidden layers
+    (1000003, 16, 16, 0, 0),   # H·W (16 -> 16), Amazon / Protein hidden layers (quad kernel)
+    (1000003, 16, 16, 0, 1),   # S·Wᵀ (16 -> 16), quad kernel with a transposed B
+    (1000003, 14, 13, 0, 0),   # quad kernel, ragged k and n
+    (1000005, 3, 5, 0, 1),     # quad kernel, tiny ragged tile
     (1000003, 24, 16, 0, 1),   # S·Wᵀ (16 -> 24)
     (1000003, 16, 24, 0, 1),
     (1000003, 40, 32, 0, 0),   # two column groups per lane, ragged
