@@ -297,6 +297,30 @@ def run_ours(args, cfg):
         barrier()
     launches = cg.kernel_launches() - launches0
     ledger1 = trainer.ledger()
+    cost = None
+    if world > 1:
+        # The timed epochs' metered traffic of every rank against the analytic
+        # model (compare_cost, cost.cpp:115-161) at the hidden width, which is
+        # what the narrow-first panels carry.
+        delta = torch.tensor([ledger1[c][f] - ledger0[c][f] for c in cg.CATEGORIES
+                              for f in ("messages", "words_sent", "words_received", "payload_words",
+                                        "calls")], dtype=torch.int64, device="cuda")
+        allled = [torch.zeros_like(delta) for _ in range(world)]
+        pg.all_gather(allled, delta)
+        if rank == 0:
+            leds = []
+            for t in allled:
+                v = t.cpu().numpy().tolist()
+                leds.append({c: dict(zip(("messages", "words_sent", "words_received",
+                                          "payload_words", "calls"), v[5 * i:5 * i + 5]))
+                             for i, c in enumerate(cg.CATEGORIES)})
+            try:
+                cost = cg.compare_cost(strat, cg.CostParams(cfg["n"], data.nnz, cfg["dims"][1],
+                                                            len(cfg["dims"]) - 1, N, repl),
+                                       leds, args.steps)
+                cost["f"] = cfg["dims"][1]
+            except Exception as e:  # pragma: no cover
+                cost = {"unavailable": str(e)}
     # NVLink words received per rank per epoch (reference ledger conventions).
     recv_words = sum(ledger1[c]["words_received"] - ledger0[c]["words_received"]
                      for c in ledger1) / max(args.steps, 1)
@@ -393,6 +417,24 @@ def run_ours(args, cfg):
                 # the kernel's device time per epoch over the graph-replayed epoch time
                 "share_of_step": round(dom["ms"] / max(args.steps, 1) / max(ms_step, 1e-9), 4),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"}
+        if dom_name.startswith("spmm_f"):
+            # SURVEY 8(d)'s second byte model: every nonzero gathers one whole
+            # f-wide row of H (no reuse), and the L1 wavefront floor of that
+            # access pattern — one 128 B L1TEX wavefront per gathered row (the
+            # rows are <= 64 B) plus one per 8 streamed {col, val} entries,
+            # 148 SMs at the sampled SM clock.
+            f = int(dom_name.split("_f")[1])
+            rows = trainer.part_shape(0, 0)[0]  # every part of a rank spans its block rows
+            nnz = sum(trainer.part_shape(0, q)[2] for q in range(trainer.num_parts()))
+            gather = 8.0 * (rows + 1) + 8.0 * nnz + 4.0 * f * nnz + 4.0 * f * rows
+            sm_hz = (clocks.summary().get("sm_mhz") or 1965) * 1e6
+            lsu_floor_ms = nnz * (1.0 + 1.0 / 8.0) / (148 * sm_hz) * 1e3
+            roof.update({"gather_bytes_per_launch": gather,
+                         "gather_GBps": round(gather / (per_launch_ms * 1e-3) / 1e9, 1),
+                         "lsu_floor_ms": round(lsu_floor_ms, 4),
+                         "lsu_frac": round(lsu_floor_ms / per_launch_ms, 4),
+                         "gather_model": "no-reuse bytes 8(r+1)+8nnz+4f*nnz+4fr; L1 floor = "
+                                         "nnz*(1+1/8) wavefronts / (148 SMs x SM clock)"})
 
     # ---- epoch roofline (north star): the slower of this rank's kernel bytes at
     # HBM bandwidth and its received block bytes at NVLink bandwidth, max over ranks.
@@ -460,6 +502,7 @@ def run_ours(args, cfg):
         "eager_ms_per_step": round(eager_ms_step, 4),
         "roofline": roof,
         "epoch_roofline": epoch_roof,
+        "cost_model": cost,
         "cpu_baseline": cpu,
         "clocks": clk,
         "kernels": {k: {"launches": v["launches"], "ms_per_launch": round(v["ms"] / v["launches"], 4),

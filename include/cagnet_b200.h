@@ -249,6 +249,8 @@ CAGNET_API int cagnet_trainer_y(cagnet_trainer_t t, int l, float* out);
  * (which 0 = A, 1 = A^T).  shape = {n_rows, n_cols, nnz}. */
 CAGNET_API int cagnet_trainer_num_parts(cagnet_trainer_t t, int* out);
 CAGNET_API int cagnet_trainer_part(cagnet_trainer_t t, int which, int part, cagnet_csr_t* out);
+/* shape3 = {n_rows, n_cols, nnz} of a part without copying it. */
+CAGNET_API int cagnet_trainer_part_shape(cagnet_trainer_t t, int which, int part, int64_t* shape3);
 /* Per-category device time of the last epoch in ms: [spmm, gemm, elementwise,
  * dbcast, sbcast, reduce, allgather, epoch_total] and per-category NCCL bytes
  * received by this rank per the reference ledger conventions

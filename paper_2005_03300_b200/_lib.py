@@ -100,6 +100,7 @@ SIGNATURES = {
     "cagnet_trainer_y": [vp, i32, _f32p],
     "cagnet_trainer_num_parts": [vp, C.POINTER(i32)],
     "cagnet_trainer_part": [vp, i32, i32, C.POINTER(vp)],
+    "cagnet_trainer_part_shape": [vp, i32, i32, _i64p],
     "cagnet_trainer_stats": [vp, _f64p, _u64p],
     "cagnet_trainer_ledger": [vp, _u64p],
     "cagnet_trainer_set_timing": [vp, i32],

@@ -528,6 +528,12 @@ class Trainer:
     def part(self, which: int, idx: int) -> DeviceCSR:
         return _new_csr(lib.cagnet_trainer_part, self.h, which, idx)
 
+    def part_shape(self, which: int, idx: int) -> tuple:
+        """(n_rows, n_cols, nnz) of a part without copying it."""
+        out = np.zeros(3, np.int64)
+        check(lib.cagnet_trainer_part_shape(self.h, which, idx, out))
+        return tuple(int(x) for x in out)
+
     def ledger(self) -> dict:
         buf = np.zeros(20, np.uint64)
         check(lib.cagnet_trainer_ledger(self.h, buf))

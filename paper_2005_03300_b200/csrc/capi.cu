@@ -937,6 +937,15 @@ int cagnet_trainer_num_parts(cagnet_trainer_t t, int* out) {
   return guarded([&] { *out = t->t->num_parts(); });
 }
 
+int cagnet_trainer_part_shape(cagnet_trainer_t t, int which, int part, int64_t* shape3) {
+  return guarded([&] {
+    const cagnet::DeviceCsr& src = t->t->part(which, part);
+    shape3[0] = src.n_rows;
+    shape3[1] = src.n_cols;
+    shape3[2] = src.nnz;
+  });
+}
+
 int cagnet_trainer_part(cagnet_trainer_t t, int which, int part, cagnet_csr_t* out) {
   return guarded([&] {
     const cagnet::DeviceCsr& src = t->t->part(which, part);
