@@ -182,6 +182,12 @@ CAGNET_API int cagnet_dataset_make(int device, int64_t n, const int64_t* raw_row
  * doubles per vertex) and labels ("vertex,label" per line); from_edge_list
  * (both directions when undirected), normalisation and transpose on `device`.
  * I/O and format errors return CAGNET_ERUNTIME with the reference's message. */
+/* Binary dataset cache (the survey's §8(f).2 CSR cache): a finished
+ * GraphDataset — normalised adj and adj_t, features, labels, mask — written
+ * once ("CAGNETD1" header + raw arrays) and mapped back without generation,
+ * parsing or sorting. */
+CAGNET_API int cagnet_dataset_save(cagnet_dataset_t d, const char* path);
+CAGNET_API int cagnet_dataset_load_binary(int device, const char* path, cagnet_dataset_t* out);
 CAGNET_API int cagnet_dataset_load(int device, const char* edges_path, const char* features_path,
                         const char* labels_path, int undirected, cagnet_dataset_t* out);
 /* permute_random (dataset.hpp:70-77, dataset.cpp:120-144): relabels vertices
@@ -196,6 +202,12 @@ CAGNET_API int cagnet_dataset_csr(cagnet_dataset_t d, int which, cagnet_csr_t* o
 CAGNET_API int cagnet_dataset_features(cagnet_dataset_t d, float* out /* n x f, host */);
 CAGNET_API int cagnet_dataset_labels(cagnet_dataset_t d, int64_t* out);
 CAGNET_API int cagnet_dataset_free(cagnet_dataset_t d);
+
+/* from_edge_list (csr.cpp:79-92): canonical unit-valued CSR of the m (u, v)
+ * pairs (duplicates collapse; undirected adds (v, u) for u != v), sorted and
+ * deduplicated on the GPU. */
+CAGNET_API int cagnet_csr_from_edge_list(int device, int64_t n, int64_t m, const int64_t* u, const int64_t* v,
+                                         int undirected, cagnet_csr_t* out);
 
 /* --- model (gnn.hpp:29-42) --------------------------------------------------- */
 /* init_glorot (gnn.cpp:24-44): fp64 weights for every layer, concatenated

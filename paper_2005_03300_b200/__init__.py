@@ -40,6 +40,8 @@ from .api import (  # noqa: F401
     make_dataset,
     make_grid,
     load_dataset,
+    load_dataset_binary,
+    from_edge_list,
     make_trainer,
     permute_random,
     run_distributed,

@@ -75,6 +75,9 @@ SIGNATURES = {
     "cagnet_dataset_make": [i32, i64, _i64p, _i64p, _f64p, i64, _i64p, vp, i64, C.POINTER(vp)],
     "cagnet_dataset_info": [vp, _i64p],
     "cagnet_dataset_permute_random": [vp, u64, vp, C.POINTER(vp)],
+    "cagnet_dataset_save": [vp, C.c_char_p],
+    "cagnet_dataset_load_binary": [i32, C.c_char_p, C.POINTER(vp)],
+    "cagnet_csr_from_edge_list": [i32, i64, i64, _i64p, _i64p, i32, C.POINTER(vp)],
     "cagnet_dataset_load": [i32, C.c_char_p, C.c_char_p, C.c_char_p, i32, C.POINTER(vp)],
     "cagnet_dataset_csr": [vp, i32, C.POINTER(vp)],
     "cagnet_dataset_features": [vp, _f32p],

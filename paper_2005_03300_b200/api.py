@@ -209,6 +209,10 @@ class GraphDataset:
         check(lib.cagnet_dataset_info(self.h, info))
         self.n, self.nnz, self.num_features, self.num_classes, self._train = (int(x) for x in info)
 
+    def save(self, path) -> None:
+        """Binary dataset cache (CAGNETD1): load back with load_dataset_binary."""
+        check(lib.cagnet_dataset_save(self.h, str(path).encode()))
+
     def train_count(self) -> int:
         return self._train
 
@@ -266,6 +270,22 @@ def load_dataset(edges_path, features_path, labels_path, undirected=False,
     check(lib.cagnet_dataset_load(device, str(edges_path).encode(), str(features_path).encode(),
                                   str(labels_path).encode(), int(bool(undirected)), C.byref(out)))
     return GraphDataset(out, device)
+
+
+def load_dataset_binary(path, device=0) -> GraphDataset:
+    """A dataset written by GraphDataset.save (binary cache, no regeneration)."""
+    out = C.c_void_p()
+    check(lib.cagnet_dataset_load_binary(device, str(path).encode(), C.byref(out)))
+    return GraphDataset(out, device)
+
+
+def from_edge_list(n, u, v, undirected=False, device=0) -> DeviceCSR:
+    """from_edge_list (csr.cpp:79-92) on the GPU: unit-valued canonical CSR."""
+    u = np.ascontiguousarray(u, np.int64)
+    v = np.ascontiguousarray(v, np.int64)
+    if u.shape != v.shape:
+        raise InvalidArgument(1, "from_edge_list: u and v differ in length")
+    return _new_csr(lib.cagnet_csr_from_edge_list, device, n, len(u), u, v, int(bool(undirected)))
 
 
 def permute_random(data: GraphDataset, seed: int):

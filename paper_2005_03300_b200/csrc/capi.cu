@@ -395,6 +395,42 @@ int cagnet_dataset_load(int device, const char* edges_path, const char* features
   });
 }
 
+int cagnet_dataset_save(cagnet_dataset_t d, const char* path) {
+  return guarded([&] {
+    cagnet::require(d && path, "save_dataset: null argument");
+    cagnet::dataset_save(*d->data, path);
+  });
+}
+
+int cagnet_dataset_load_binary(int device, const char* path, cagnet_dataset_t* out) {
+  return guarded([&] {
+    cagnet::require(path != nullptr, "load_dataset_binary: null path");
+    auto d = std::make_unique<cagnet_dataset_s>();
+    d->data = cagnet::dataset_load_binary(path, device);
+    wrap_dataset(d.get());
+    *out = d.release();
+  });
+}
+
+int cagnet_csr_from_edge_list(int device, int64_t n, int64_t m, const int64_t* u, const int64_t* v, int undirected,
+                              cagnet_csr_t* out) {
+  return guarded([&] {
+    cagnet::require(m == 0 || (u && v), "from_edge_list: null edge arrays");
+    set_device(device);
+    auto h = std::make_unique<cagnet_csr_s>();
+    cudaStream_t s;
+    CG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    try {
+      h->csr = cagnet::csr_from_edges_device(n, m, u, v, undirected != 0, s);
+    } catch (...) {
+      cudaStreamDestroy(s);
+      throw;
+    }
+    CG_CUDA(cudaStreamDestroy(s));
+    *out = h.release();
+  });
+}
+
 int cagnet_dataset_permute_random(cagnet_dataset_t d, uint64_t seed, int64_t* perm_out,
                                   cagnet_dataset_t* out) {
   return guarded([&] {

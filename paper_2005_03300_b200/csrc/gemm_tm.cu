@@ -643,14 +643,14 @@ __global__ void tm_reduce_kernel(const TmParams p, int splits) {
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
   for (int64_t e = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; e < total;
        e += warps) {
-    float s = 0.f;
+    double s = 0.0;  // fp64 fold of the split partials (fixed order: deterministic)
     const int64_t r = e / p.n, c = e % p.n;
     for (int z = lane; z < splits; z += 32)
-      s += p.partial[(static_cast<int64_t>(z) * p.mpad + r) * p.pld + c];
+      s += static_cast<double>(p.partial[(static_cast<int64_t>(z) * p.mpad + r) * p.pld + c]);
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) {
-      p.C[r * p.ldc + c] = epilogue_value(p, r, c, s);
+      p.C[r * p.ldc + c] = epilogue_value(p, r, c, static_cast<float>(s));
     }
   }
 }
@@ -875,8 +875,18 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
                                 static_cast<uint64_t>(d.b_sk), static_cast<uint32_t>(bn), BK, false))
       return false;
     const int64_t kblocks = ceil_div64(d.k, BK);
-    // One tile per CTA, no second wave: floor(SMs / M tiles) splits.
+    // One tile per CTA, no second wave: floor(SMs / M tiles) splits — but no
+    // split longer than kMaxChunkRows: the tensor cores' fp32 accumulation
+    // over a long K loses accuracy (measured on Amazon-shaped H0ᵀ S, 96 K+ rows
+    // per split: 4.7e-4 relative to fp64), so long reductions take more,
+    // shorter splits (persistent CTAs walk several) folded in fp64.
+    static const int64_t kMaxChunkRows = [] {
+      const char* e = std::getenv("CAGNET_HTS_CHUNK_ROWS");
+      return e ? std::atoll(e) : 8192LL;
+    }();
     int64_t splits = sms / m_tiles;
+    const int64_t min_splits = ceil_div64(kblocks, std::max<int64_t>(kMaxChunkRows / BK, 1));
+    if (splits < min_splits) splits = min_splits;
     if (splits > kblocks) splits = kblocks;
     if (splits < 1) splits = 1;
     p.k_chunk = ceil_div64(kblocks, splits) * BK;

@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cerrno>
+#include <cstdio>
 #include <climits>
 #include <cstdint>
 #include <cstdlib>
@@ -494,6 +495,152 @@ DeviceCsr csr_from_pairs_device(const std::vector<uint64_t>& hu, const std::vect
 }
 
 }  // namespace
+
+DeviceCsr csr_from_edges_device(int64_t n, int64_t m, const int64_t* u, const int64_t* v, bool undirected,
+                                cudaStream_t s) {
+  // from_edge_list's validation (csr.cpp:79-92), same message.
+  std::vector<uint64_t> hu(static_cast<size_t>(m)), hv(static_cast<size_t>(m));
+  for (int64_t i = 0; i < m; ++i) {
+    if (u[i] < 0 || v[i] < 0 || u[i] >= n || v[i] >= n)
+      throw std::invalid_argument("from_edge_list: edge " + std::to_string(i) + " = (" + std::to_string(u[i]) +
+                                  ", " + std::to_string(v[i]) + ") outside vertex range [0, " + std::to_string(n) +
+                                  ")");
+    hu[static_cast<size_t>(i)] = static_cast<uint64_t>(u[i]);
+    hv[static_cast<size_t>(i)] = static_cast<uint64_t>(v[i]);
+  }
+  require(n >= 0 && n <= INT32_MAX, "from_edge_list: n outside the device's 32-bit column range");
+  return csr_from_pairs_device(hu, hv, static_cast<uint64_t>(n), undirected, s);
+}
+
+// ---- binary dataset cache ------------------------------------------------------------------
+// "CAGNETD1" | int64 {n, f, num_classes, train_count, nnz_adj, nnz_adj_t} |
+// adj {row_ptr int64[n+1], col int32[nnz], vals f32[nnz]} | adj_t likewise |
+// features f32[n x f] (dense) | labels int32[n] | mask uint8[n].  Host byte
+// order; a finished GraphDataset (normalised adjacency and its transpose), so
+// loading is a mapped read and the uploads — no generation, no sort.
+namespace {
+constexpr char kCacheMagic[8] = {'C', 'A', 'G', 'N', 'E', 'T', 'D', '1'};
+
+void write_all(FILE* fp, const void* p, size_t bytes, const std::string& path) {
+  if (bytes && std::fwrite(p, 1, bytes, fp) != bytes) throw std::runtime_error("save_dataset: write failed for " + path);
+}
+
+template <class T>
+std::vector<T> download(const T* dev, size_t count) {
+  std::vector<T> h(count);
+  if (count) CG_CUDA(cudaMemcpy(h.data(), dev, count * sizeof(T), cudaMemcpyDeviceToHost));
+  return h;
+}
+}  // namespace
+
+void dataset_save(const DeviceDataset& d, const std::string& path) {
+  CG_CUDA(cudaSetDevice(d.device));
+  FILE* fp = std::fopen(path.c_str(), "wb");
+  if (!fp) throw std::runtime_error("save_dataset: cannot open " + path);
+  try {
+    write_all(fp, kCacheMagic, sizeof(kCacheMagic), path);
+    const int64_t hdr[6] = {d.n, d.f, d.num_classes, d.train_count, d.adj.nnz, d.adj_t.nnz};
+    write_all(fp, hdr, sizeof(hdr), path);
+    for (const DeviceCsr* a : {&d.adj, &d.adj_t}) {
+      auto rp = download(a->row_ptr.get(), static_cast<size_t>(a->n_rows + 1));
+      auto ci = download(a->col_idx.get(), static_cast<size_t>(a->nnz));
+      auto va = download(a->vals.get(), static_cast<size_t>(a->nnz));
+      write_all(fp, rp.data(), rp.size() * 8, path);
+      write_all(fp, ci.data(), ci.size() * 4, path);
+      write_all(fp, va.data(), va.size() * 4, path);
+    }
+    std::vector<float> feats(static_cast<size_t>(d.n * d.f));
+    if (d.n && d.f)
+      CG_CUDA(cudaMemcpy2D(feats.data(), d.f * sizeof(float), d.features.get(), d.ldf * sizeof(float),
+                           d.f * sizeof(float), d.n, cudaMemcpyDeviceToHost));
+    write_all(fp, feats.data(), feats.size() * 4, path);
+    auto lab = download(d.labels.get(), static_cast<size_t>(d.n));
+    auto msk = download(d.mask.get(), static_cast<size_t>(d.n));
+    write_all(fp, lab.data(), lab.size() * 4, path);
+    write_all(fp, msk.data(), msk.size(), path);
+  } catch (...) {
+    std::fclose(fp);
+    throw;
+  }
+  if (std::fclose(fp) != 0) throw std::runtime_error("save_dataset: write failed for " + path);
+}
+
+std::unique_ptr<DeviceDataset> dataset_load_binary(const std::string& path, int device) {
+  MappedFile f(path, "load_dataset_binary");
+  const char* p = f.data();
+  size_t left = f.size();
+  auto take = [&](size_t bytes) {
+    if (bytes > left) throw std::runtime_error("load_dataset_binary: truncated file " + path);
+    const char* q = p;
+    p += bytes;
+    left -= bytes;
+    return q;
+  };
+  if (f.size() < sizeof(kCacheMagic) || std::memcmp(take(sizeof(kCacheMagic)), kCacheMagic, 8) != 0)
+    throw std::runtime_error("load_dataset_binary: " + path + " is not a CAGNETD1 dataset cache");
+  int64_t hdr[6];
+  std::memcpy(hdr, take(sizeof(hdr)), sizeof(hdr));
+  const int64_t n = hdr[0], fdim = hdr[1];
+  if (n < 0 || n > INT32_MAX || fdim < 0 || hdr[2] <= 0 || hdr[4] < 0 || hdr[5] < 0)
+    throw std::runtime_error("load_dataset_binary: corrupt header in " + path);
+  // The whole layout is checked against the file size before any device work.
+  const uint64_t need = 8 + sizeof(hdr) + 2ull * static_cast<uint64_t>(n + 1) * 8 +
+                        static_cast<uint64_t>(hdr[4] + hdr[5]) * 8 + static_cast<uint64_t>(n) * fdim * 4 +
+                        static_cast<uint64_t>(n) * 5;
+  if (f.size() < need) throw std::runtime_error("load_dataset_binary: truncated file " + path);
+  if (f.size() > need) throw std::runtime_error("load_dataset_binary: trailing bytes in " + path);
+  CG_CUDA(cudaSetDevice(device));
+  auto d = std::make_unique<DeviceDataset>();
+  d->device = device;
+  d->n = n;
+  d->f = fdim;
+  d->num_classes = hdr[2];
+  d->train_count = hdr[3];
+  d->ldf = padded_ld(fdim);
+  cudaStream_t s;
+  CG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  try {
+    for (int w = 0; w < 2; ++w) {
+      DeviceCsr& a = w == 0 ? d->adj : d->adj_t;
+      const int64_t nnz = hdr[4 + w];
+      a.device = device;
+      a.n_rows = a.n_cols = n;
+      a.nnz = nnz;
+      a.row_ptr.resize(static_cast<size_t>(n + 1));
+      a.col_idx.resize(static_cast<size_t>(nnz > 0 ? nnz : 1));
+      a.vals.resize(static_cast<size_t>(nnz > 0 ? nnz : 1));
+      const char* rp = take(static_cast<size_t>(n + 1) * 8);
+      const char* ci = take(static_cast<size_t>(nnz) * 4);
+      const char* va = take(static_cast<size_t>(nnz) * 4);
+      CG_CUDA(cudaMemcpy(a.row_ptr.get(), rp, static_cast<size_t>(n + 1) * 8, cudaMemcpyHostToDevice));
+      if (nnz) {
+        CG_CUDA(cudaMemcpy(a.col_idx.get(), ci, static_cast<size_t>(nnz) * 4, cudaMemcpyHostToDevice));
+        CG_CUDA(cudaMemcpy(a.vals.get(), va, static_cast<size_t>(nnz) * 4, cudaMemcpyHostToDevice));
+      }
+    }
+    d->features.resize(static_cast<size_t>(n * d->ldf > 0 ? n * d->ldf : 1));
+    kern::zero_bytes(d->features.get(), static_cast<size_t>(n * d->ldf) * sizeof(float), s);
+    CG_CUDA(cudaStreamSynchronize(s));
+    const char* fe = take(static_cast<size_t>(n * fdim) * 4);
+    if (n && fdim)
+      CG_CUDA(cudaMemcpy2D(d->features.get(), d->ldf * sizeof(float), fe, fdim * sizeof(float), fdim * sizeof(float),
+                           n, cudaMemcpyHostToDevice));
+    d->labels.resize(static_cast<size_t>(n > 0 ? n : 1));
+    d->mask.resize(static_cast<size_t>(n > 0 ? n : 1));
+    const char* la = take(static_cast<size_t>(n) * 4);
+    const char* ma = take(static_cast<size_t>(n));
+    if (n) {
+      CG_CUDA(cudaMemcpy(d->labels.get(), la, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice));
+      CG_CUDA(cudaMemcpy(d->mask.get(), ma, static_cast<size_t>(n), cudaMemcpyHostToDevice));
+    }
+    if (left != 0) throw std::runtime_error("load_dataset_binary: trailing bytes in " + path);
+  } catch (...) {
+    cudaStreamDestroy(s);
+    throw;
+  }
+  CG_CUDA(cudaStreamDestroy(s));
+  return d;
+}
 
 std::unique_ptr<DeviceDataset> dataset_load(const std::string& edges_path,
                                             const std::string& features_path,

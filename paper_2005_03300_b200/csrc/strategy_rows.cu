@@ -33,11 +33,11 @@ class TrainerRows final : public Trainer {
       a_parts_.push_back(extract_block_device(data_.adj, rows.begin, rows.end, cols.begin, cols.end, cs_));
       at_parts_.push_back(extract_block_device(data_.adj_t, rows.begin, rows.end, cols.begin, cols.end, cs_));
     }
-    int64_t maxf = 0;
-    for (int64_t d : dims_) maxf = d > maxf ? d : maxf;
-    const int64_t step = ceil_div64(data_.n, blocks());
-    acc_.alloc(rows.size(), maxf);
-    for (int i = 0; i < 2; ++i) panel_[i].alloc(step, maxf);
+    buf_w_ = 0;
+    size_buffers();
+    // Coalesced stage panels (and the peer-memory slots) up to 64 columns, or
+    // up to the narrow-first panel width when that is narrower.
+    coalesce_w_ = std::min<int64_t>(kCoalesceMaxF, padded_ld(big_width()));
     // Coalesced stages: this column's stage panels land side by side in one
     // buffer (one fused NCCL group) and a single SpMM runs over the block row
     // restricted to the stage columns [c_lo, c_hi).
@@ -49,10 +49,10 @@ class TrainerRows final : public Trainer {
       a_chunk_ = extract_block_device(data_.adj, rows.begin, rows.end, c_lo_, c_hi_, cs_);
       at_chunk_ = extract_block_device(data_.adj_t, rows.begin, rows.end, c_lo_, c_hi_, cs_);
       // Rows for whole padded slots (the 1D all-gather writes P equal slots).
-      gbuf_.alloc(std::max(c_hi_ - c_lo_, ceil_div64(data_.n, blocks()) * blocks()), kCoalesceMaxF);
+      gbuf_.alloc(std::max(c_hi_ - c_lo_, ceil_div64(data_.n, blocks()) * blocks()), coalesce_w_);
       if (one_d() && p2p_enabled_) {
         const size_t bytes = static_cast<size_t>(ceil_div64(data_.n, blocks()) * blocks()) *
-                             kCoalesceMaxF * sizeof(float);
+                             coalesce_w_ * sizeof(float);
         p2p_ok_ = p2p_.init(*comm_, rank_, grid_.ranks(), device_, bytes, cs_);
         overlap_ok_ = p2p_ok_ && overlap_enabled_;
         if (overlap_ok_) {
@@ -70,6 +70,7 @@ class TrainerRows final : public Trainer {
     if (l < 1 || l >= num_layers())
       throw std::invalid_argument("run_forward_layer: layer " + std::to_string(l) + " outside [1, " +
                                   std::to_string(num_layers()) + ")");
+    size_buffers();
     const int64_t fin = dims_[static_cast<size_t>(l - 1)];
     const int64_t fout = dims_[static_cast<size_t>(l)];
     const Mat& h = h_[static_cast<size_t>(l - 1)].m;
@@ -148,6 +149,7 @@ class TrainerRows final : public Trainer {
 
   void backward_and_step() override {
     const int L = num_layers();
+    size_buffers();
     // Only column 0 contributes the loss so replicated rows count once.
     if (grid_.col_of(rank_) != 0) kern::zero_bytes(loss_partial_.get(), sizeof(double), cs_);
     loss_all_reduce(loss_partial_.get());
@@ -294,7 +296,7 @@ class TrainerRows final : public Trainer {
     if (fuse_ < 1 || !one_d() || mine.cols > kern::kSpmmEpiMaxF) return false;
     if (stage_group().size() == 1 && chunk_end(0) - chunk_begin(0) == 1)
       return spmm_single_pass(parts[static_cast<size_t>(chunk_begin(0))], mine);
-    if (chunk_ok_ && mine.cols <= kCoalesceMaxF) {
+    if (chunk_ok_ && mine.ld <= coalesce_w_) {
       const DeviceCsr& blk = &parts == &a_parts_ ? a_chunk_ : at_chunk_;
       return spmm_single_pass(blk, Mat{nullptr, c_hi_ - c_lo_, mine.cols, mine.ld});
     }
@@ -307,7 +309,7 @@ class TrainerRows final : public Trainer {
     const int j = grid_.col_of(rank_);
     const Group& grp = stage_group();
     const bool comm = grp.size() > 1;
-    if (chunk_ok_ && mine.cols <= kCoalesceMaxF) {
+    if (chunk_ok_ && mine.ld <= coalesce_w_) {
       // Narrow panels: latency, not bandwidth, bounds each stage, so the
       // stage broadcasts go out as one NCCL group (same calls, same ledger)
       // into adjacent slots and one SpMM consumes them all.
@@ -485,6 +487,19 @@ class TrainerRows final : public Trainer {
   }
 
   static constexpr int64_t kCoalesceMaxF = 64;
+  int64_t coalesce_w_ = kCoalesceMaxF;  // widest coalesced panel (gbuf_ / peer slots), fixed at distribute
+  int64_t buf_w_ = 0;                   // width acc_ / panel_ are sized for
+
+  // acc_ / panel_ sized for big_width() (grown, eagerly, when a
+  // propagation-order switch widens them).
+  void size_buffers() {
+    const int64_t w = big_width();
+    if (w <= buf_w_) return;
+    acc_.alloc(tile_rows(rank_).size(), w);
+    for (int i = 0; i < 2; ++i) panel_[i].alloc(ceil_div64(data_.n, blocks()), w);
+    buf_w_ = w;
+    CG_CUDA(cudaStreamSynchronize(nullptr));  // the zeroing memsets ran on the legacy stream
+  }
 
   OwnedMat acc_;
   OwnedMat panel_[2];
@@ -529,7 +544,7 @@ class TrainerRows final : public Trainer {
   // an SpMM producer whose own exchange still publishes, else 0).
   bool arm(const Mat& panel, bool relu, int skip, kern::PushSpec* ps) {
     if (!(one_d() && p2p_ok_ && chunk_ok_ && !overlap_ok_ && !pipeline_enabled_ &&
-          panel.cols <= kCoalesceMaxF && !armed_.valid))
+          panel.ld <= coalesce_w_ && !armed_.valid))
       return false;
     const int b = static_cast<int>((p2p_stage_ + static_cast<uint64_t>(skip)) % PeerPanels::kBuffers);
     ps->bufs = p2p_.device_buffers(b);

@@ -100,9 +100,23 @@ class TrainerSumma final : public Trainer {
       comm_->restore(saved);
     }
 
+    int64_t maxall = 0;
+    for (int64_t d : dims_) maxall = std::max(maxall, d);
+    const int64_t fmax_cols = ceil_div64(maxall, side());
+    strip_.alloc(fmax_cols, fmax_cols, fmax_cols);  // Y strips: f_in / √P x f_out / √P
+    buf_w_ = 0;
+    size_buffers();
+    settle();
+  }
+
+  // The n-proportional panels sized for big_width() (grown, eagerly, when a
+  // propagation-order switch widens them).
+  void size_buffers() {
+    const int64_t w = big_width();
+    if (w <= buf_w_) return;
     const int64_t step_rows = ceil_div64(std::max<int64_t>(data_.n, 1), side());  // vertex block
     const int64_t sub_step = ceil_div64(std::max<int64_t>(step_rows, 1), layers());
-    const int64_t fcols = ceil_div64(maxf, side());
+    const int64_t fcols = ceil_div64(w, side());
     // Dense panels hold an H/G tile (sub_step rows) or a T/S tile, with room
     // for every column chunk of a chunked 2D panel at its own padded ld.
     const int64_t chunk_slack = 4 * (strat_.block > 0 ? ceil_div64(fcols, strat_.block) : 1);
@@ -110,17 +124,18 @@ class TrainerSumma final : public Trainer {
     partial_.alloc(step_rows, fcols, -1, layers() * sub_step);
     tslice_.alloc(sub_step, fcols);
     utile_.alloc(sub_step, fcols);
-    pfull_.alloc(sub_step, maxf);
+    pfull_.alloc(sub_step, w);
     redbuf_.alloc(static_cast<int64_t>(side()) * sub_step, fcols);
-    strip_.alloc(fcols, fcols, fcols);
     gather_.alloc(side() * sub_step, fcols, fcols);
-    settle();
+    buf_w_ = w;
+    CG_CUDA(cudaStreamSynchronize(nullptr));  // the zeroing memsets ran on the legacy stream
   }
 
   void forward_layer(int l) override {
     if (l < 1 || l >= num_layers())
       throw std::invalid_argument("run_forward_layer: layer " + std::to_string(l) + " outside [1, " +
                                   std::to_string(num_layers()) + ")");
+    size_buffers();
     const int i = grid_.row_of(rank_), j = grid_.col_of(rank_), k = grid_.layer_of(rank_);
     const int64_t wprev = dims_[static_cast<size_t>(l - 1)], wcur = dims_[static_cast<size_t>(l)];
     const BlockRange blockrow = block_range(data_.n, side(), i);
@@ -189,6 +204,7 @@ class TrainerSumma final : public Trainer {
 
   void backward_and_step() override {
     const int L = num_layers();
+    size_buffers();
     const int i = grid_.row_of(rank_), j = grid_.col_of(rank_), k = grid_.layer_of(rank_);
     loss_all_reduce(loss_partial_.get());
     for (int l = L - 1; l >= 1; --l) {
@@ -251,6 +267,7 @@ class TrainerSumma final : public Trainer {
 
  private:
   void begin_epoch() override { slot_ = 0; }
+  int64_t buf_w_ = 0;  // width the large panels are sized for
   int side() const { return grid_.rows(); }
   int layers() const { return grid_.layers(); }
 

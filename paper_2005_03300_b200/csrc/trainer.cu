@@ -738,6 +738,15 @@ double Trainer::last_loss() {
   return losses_host_.empty() ? 0.0 : losses_host_.back();
 }
 
+int64_t Trainer::big_width() const {
+  int64_t maxf = 0, rest = 0;
+  for (size_t i = 0; i < dims_.size(); ++i) {
+    maxf = std::max(maxf, dims_[i]);
+    if (i > 0) rest = std::max(rest, dims_[i]);
+  }
+  return (reassociate_ && dims_.size() >= 2 && dims_[0] > dims_[1]) ? rest : maxf;
+}
+
 void Trainer::settle() {
   CG_CUDA(cudaStreamSynchronize(nullptr));
   sync();

@@ -48,6 +48,13 @@ std::unique_ptr<DeviceDataset> dataset_permute(const DeviceDataset& d, uint64_t 
 std::unique_ptr<DeviceDataset> dataset_load(const std::string& edges_path,
                                             const std::string& features_path,
                                             const std::string& labels_path, bool undirected, int device);
+// from_edge_list (csr.cpp:79-92): sort + unique of the (u, v) pairs (and the
+// mirrored pairs when undirected) on the GPU; unit-valued raw CSR.
+DeviceCsr csr_from_edges_device(int64_t n, int64_t m, const int64_t* u, const int64_t* v, bool undirected,
+                                cudaStream_t s);
+// Binary dataset cache (io.cu): a finished dataset written / mapped back.
+void dataset_save(const DeviceDataset& d, const std::string& path);
+std::unique_ptr<DeviceDataset> dataset_load_binary(const std::string& path, int device);
 // make_dataset (dataset.cpp:76-90) from a raw unit-valued CSR already on the
 // current device (load_dataset's GPU-built from_edge_list).
 std::unique_ptr<DeviceDataset> dataset_make_device(DeviceCsr raw, const double* features, int64_t f,
@@ -213,6 +220,11 @@ class Trainer {
   // and both trainer streams complete.  Not a device-wide synchronisation:
   // ranks sharing one GPU must never wait for each other's streams.
   void settle();
+  // Width the strategies' large n-proportional scratch panels must hold: the
+  // widest layer, except under narrow-first propagation with a narrowing first
+  // layer, where nothing f0-wide is ever propagated or swept (the f0-wide H0
+  // tile is only read by the first GEMM) — Amazon {300,16,16,24}: 24, not 300.
+  int64_t big_width() const;
   void ms_after_cs();
   void cs_after_ms();
   // out (+)= a · h.  With epi (f <= 32, acc = false, one pass) the layer's

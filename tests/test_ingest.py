@@ -188,3 +188,62 @@ def test_ingest_large_graph_structure(cg, ref, need_gpus, tmp_path):
             assert np.array_equal(a[0], b.row_ptr) and np.array_equal(a[1], b.col_idx)
             assert np.array_equal(a[2], b.vals.astype(np.float32))
         assert np.array_equal(g.features(), feats.astype(np.float32))
+
+
+def test_binary_cache_rejects_bad_files(cg, tmp_path):
+    """Header checks happen on the host before any device work."""
+    bad = tmp_path / "not_a_cache.bin"
+    bad.write_bytes(b"hello world, not a dataset")
+    with pytest.raises(cg.CagnetError, match="not a CAGNETD1 dataset cache"):
+        cg.load_dataset_binary(str(bad))
+    trunc = tmp_path / "truncated.bin"
+    trunc.write_bytes(b"CAGNETD1" + np.array([10, 4, 3, 10, 5, 5], np.int64).tobytes() + b"\0" * 12)
+    with pytest.raises(cg.CagnetError, match="truncated"):
+        cg.load_dataset_binary(str(trunc))
+    with pytest.raises(cg.CagnetError, match="cannot open"):
+        cg.load_dataset_binary(str(tmp_path / "missing.bin"))
+
+
+@pytest.mark.gpu
+def test_binary_cache_roundtrip(cg, need_gpus, tmp_path):
+    """save -> load_dataset_binary gives the same dataset bit for bit, and the
+    same training trajectory."""
+    need_gpus(1)
+    d = cg.generate_dataset(3000, 20.0, 24, 6, 1, 2, 3)
+    path = tmp_path / "d.cagnet"
+    d.save(path)
+    e = cg.load_dataset_binary(path)
+    assert (e.n, e.nnz, e.num_features, e.num_classes, e.train_count()) == \
+        (d.n, d.nnz, d.num_features, d.num_classes, d.train_count())
+    for which in (0, 1):
+        a, b = d.csr(which).download(), e.csr(which).download()
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    assert np.array_equal(d.features(), e.features())
+    assert np.array_equal(d.labels(), e.labels())
+    model = cg.init_glorot([24, 8, 6], 4, 0.5)
+    losses = []
+    for data in (d, e):
+        t = cg.make_trainer(data, model, cg.Strategy("1d", 1))
+        t.distribute()
+        losses.append(t.run_epochs(3))
+    assert np.array_equal(losses[0], losses[1])
+
+
+@pytest.mark.gpu
+def test_from_edge_list_on_gpu(cg, orc, need_gpus):
+    """from_edge_list golden arrays (test_sparse_core.cpp:39-55) and random
+    edge lists against the C restatement, directed and undirected."""
+    need_gpus(1)
+    rp, ci, v = cg.from_edge_list(3, [0, 0, 2], [1, 1, 0], undirected=False).download()
+    assert list(rp) == [0, 1, 1, 2] and list(ci) == [1, 0] and list(v) == [1.0, 1.0]
+    rp, ci, _ = cg.from_edge_list(3, [0, 0, 2], [1, 1, 0], undirected=True).download()
+    assert list(rp) == [0, 2, 3, 4] and list(ci) == [1, 2, 0, 0]
+    rng = np.random.default_rng(9)
+    u, w = rng.integers(0, 5000, 60000), rng.integers(0, 5000, 60000)
+    for und in (False, True):
+        a = cg.from_edge_list(5000, u, w, undirected=und).download()
+        b = orc.from_edge_list(5000, u, w, und)
+        assert np.array_equal(a[0], b.row_ptr) and np.array_equal(a[1], b.col_idx)
+    with pytest.raises(cg.InvalidArgument, match=r"edge 1 = \(3, 0\) outside vertex range \[0, 3\)"):
+        cg.from_edge_list(3, [0, 3], [1, 0])
