@@ -418,8 +418,23 @@ __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArg
   auto ld_c = [&](const int32_t* p) { return HINT ? __ldcs(p) : __ldg(p); };
   auto ld_v = [&](const float* p) { return HINT ? __ldcs(p) : __ldg(p); };
   if constexpr (CV) {
-    const int2* __restrict__ p = a.colval + nz_b + q;
+    // The QPR sub-teams read QPR consecutive {col, val} entries per step; the
+    // row's segment is walked from the QPR-aligned entry at or below nz_b, so
+    // every step's entries sit in one 64 B-aligned chunk (one L1 wavefront,
+    // never two) — the head group is peeled with a range predicate.
     const int2* pe = a.colval + nz_e;
+    const int2* __restrict__ p = a.colval + nz_b + q;
+    if constexpr (QPR > 1) {
+      const int64_t head = nz_b & ~static_cast<int64_t>(QPR - 1);
+      if (head != nz_b) {
+        const int2* hp = a.colval + head + q;
+        if (hp >= a.colval + nz_b && hp < pe) {
+          const int2 x = __ldg(hp);
+          fma_vec(acc, __int_as_float(x.y), gather(x.x));
+        }
+        p = hp + QPR;
+      }
+    }
     for (; p + (U - 1) * QPR < pe; p += U * QPR) {
       float4 h[U];
       float w[U];

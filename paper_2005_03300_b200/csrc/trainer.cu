@@ -560,9 +560,12 @@ void Trainer::gemm_aw(const Mat& a, int l, int64_t r0, int64_t c0, Mat c, bool a
   run_gemm(d, "gemm_tw");
 }
 
-void Trainer::run_gemm(const kern::GemmDesc& d, const char* kind) {
+void Trainer::run_gemm(const kern::GemmDesc& d, const char* kind, cudaStream_t st) {
+  // Profiled (timing) epochs keep every GEMM on the compute stream, where the
+  // per-launch events are recorded.
+  if (timing_ || st == nullptr) st = cs_;
   const int slot = prof_begin();
-  kern::gemm_tf32x3(d, cs_);
+  kern::gemm_tf32x3(d, st);
   if (slot >= 0) {
     // 4 (m k + k n + m n) algorithmic bytes, 2 m n k flops.
     const double m = static_cast<double>(d.m), n = static_cast<double>(d.n), k = static_cast<double>(d.k);
@@ -576,7 +579,7 @@ void Trainer::run_gemm(const kern::GemmDesc& d, const char* kind) {
   }
 }
 
-void Trainer::gemm_hts(const Mat& h, const Mat& s, Mat c, bool acc) {
+void Trainer::gemm_hts(const Mat& h, const Mat& s, Mat c, bool acc, cudaStream_t st) {
   kern::GemmDesc d;
   d.m = h.cols;
   d.n = s.cols;
@@ -590,7 +593,7 @@ void Trainer::gemm_hts(const Mat& h, const Mat& s, Mat c, bool acc) {
   d.C = c.p;
   d.ldc = c.ld;
   d.accumulate = acc;
-  run_gemm(d, "gemm_hts");
+  run_gemm(d, "gemm_hts", st);
 }
 
 void Trainer::gemm_swt(const Mat& s, int l, int64_t r0, int64_t c0, Mat c, bool acc, int epi,

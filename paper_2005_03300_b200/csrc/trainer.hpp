@@ -247,11 +247,12 @@ class Trainer {
   void gemm_aw(const Mat& a, int l, int64_t r0, int64_t c0, Mat c, bool acc, int epi,
                Mat aux_out);
   // C (+)= H^T · S
-  void gemm_hts(const Mat& h, const Mat& s, Mat c, bool acc);
+  // st = nullptr: the compute stream.
+  void gemm_hts(const Mat& h, const Mat& s, Mat c, bool acc, cudaStream_t st = nullptr);
   // C (+)= S · W[r0:r0+n, c0:c0+k]^T, optional relu' epilogue with aux
   void gemm_swt(const Mat& s, int l, int64_t r0, int64_t c0, Mat c, bool acc, int epi,
                 const Mat* aux);
-  void run_gemm(const kern::GemmDesc& d, const char* kind);
+  void run_gemm(const kern::GemmDesc& d, const char* kind, cudaStream_t st = nullptr);
   void bcast_mat(const Group& g, int root, Mat m, Category cat);
   void sgd_all();
   void note_prereduction(uint64_t words) { prered_.push_back(words); }
