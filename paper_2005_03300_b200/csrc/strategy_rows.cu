@@ -18,12 +18,6 @@ namespace {
 class TrainerRows final : public Trainer {
  public:
   using Trainer::Trainer;
-  ~TrainerRows() override {
-    if (cs_) cudaStreamSynchronize(cs_);
-    if (ms_) cudaStreamSynchronize(ms_);
-    for (cudaEvent_t e : ev_s_)
-      if (e) cudaEventDestroy(e);
-  }
 
   BlockRange tile_rows(int r) const override { return tile_rows_of(grid_, data_.n, r); }
   BlockRange tile_cols(int r, int64_t width) const override { return tile_cols_of(grid_, r, width); }
@@ -166,19 +160,18 @@ class TrainerRows final : public Trainer {
         //   Y = Hᵀ (A G) = (Aᵀ H)ᵀ G = Tᵀ G with T kept from the forward pass;
         //   G_prev = (A (G Wᵀ)) ⊙ relu′(Z_prev): the SpMM runs f_in wide.
         Mat y = Y_[static_cast<size_t>(l - 1)].m;
-        // Y is only read by the SGD step: its GEMM and all-reduce run on the
-        // comm stream behind the remaining backward compute (joined before
-        // SGD), so the next SpMM does not wait for them.
-        ms_after_cs();
         if (grid_.col_of(rank_) == 0)
-          gemm_hts(saved_t_[static_cast<size_t>(l)].m, g, y, false, ms_);
+          gemm_hts(saved_t_[static_cast<size_t>(l)].m, g, y, false);
         else
-          kern::zero_bytes(y.p, y.rows * y.ld * sizeof(float), ms_);
+          kern::zero_bytes(y.p, y.rows * y.ld * sizeof(float), cs_);
+        // Y is only read by the SGD step: its all-reduce runs on the comm
+        // stream behind the remaining backward compute (joined before SGD).
+        ms_after_cs();
         comm_->all_reduce(grid_.world(), y.p, static_cast<size_t>(y.rows * y.cols), ncclFloat32,
                           Category::Reduce, words(y), ms_);
         if (l >= 2) {
           Mat gp = g_[static_cast<size_t>(l - 2)].m;
-          Mat u = sbuf(0, g.rows, dims_[static_cast<size_t>(l - 1)]);
+          Mat u = view(acc_, g.rows, dims_[static_cast<size_t>(l - 1)]);
           gemm_swt(g, l - 1, 0, 0, u, false, kern::EPI_NONE, nullptr);
           const Mat& zp = z_[static_cast<size_t>(l - 2)].m;
           if (fusable(a_parts_, u)) {
@@ -199,11 +192,7 @@ class TrainerRows final : public Trainer {
         }
         continue;
       }
-      // S alternates between two buffers by layer, so Y = Hᵀ S can still read
-      // this layer's S on the comm stream while the next layer's SpMM writes
-      // the other one.
-      const int sb = l & 1;
-      Mat s = sbuf(sb, g.rows, dims_[static_cast<size_t>(l)]);
+      Mat s = view(acc_, g.rows, dims_[static_cast<size_t>(l)]);
       const int64_t fprev = dims_[static_cast<size_t>(l - 1)];
       bool fused = false;
       if (fuse_ >= 2 && l >= 2 && fprev <= kern::kSpmmEpiMaxFo && fusable(a_parts_, g)) {
@@ -228,12 +217,11 @@ class TrainerRows final : public Trainer {
         if (!one_d()) row_reduce(s);
       }
       Mat y = Y_[static_cast<size_t>(l - 1)].m;
-      ms_after_cs();
       if (grid_.col_of(rank_) == 0)
-        gemm_hts(h_[static_cast<size_t>(l - 1)].m, s, y, false, ms_);
+        gemm_hts(h_[static_cast<size_t>(l - 1)].m, s, y, false);
       else
-        kern::zero_bytes(y.p, y.rows * y.ld * sizeof(float), ms_);
-      s_reader(sb);
+        kern::zero_bytes(y.p, y.rows * y.ld * sizeof(float), cs_);
+      ms_after_cs();
       comm_->all_reduce(grid_.world(), y.p, static_cast<size_t>(y.rows * y.cols), ncclFloat32,
                         Category::Reduce, words(y), ms_);
       if (l >= 2 && !fused) {
@@ -256,10 +244,7 @@ class TrainerRows final : public Trainer {
     sgd_all();
   }
 
-  void begin_epoch() override {
-    epoch_exchanges_ = 0;
-    s_pending_[0] = s_pending_[1] = false;  // the previous epoch joined the comm stream
-  }
+  void begin_epoch() override { epoch_exchanges_ = 0; }
 
   void finish_external_layer() override {
     // A push the layer committed for an exchange that will not come is
@@ -505,31 +490,12 @@ class TrainerRows final : public Trainer {
   int64_t coalesce_w_ = kCoalesceMaxF;  // widest coalesced panel (gbuf_ / peer slots), fixed at distribute
   int64_t buf_w_ = 0;                   // width acc_ / panel_ are sized for
 
-  // Backward S buffers (0 = acc_, 1 = acc2_): a write on the compute stream
-  // first waits for a comm-stream Y GEMM still reading the buffer.
-  OwnedMat acc2_;
-  bool s_pending_[2] = {false, false};
-  cudaEvent_t ev_s_[2] = {nullptr, nullptr};
-  Mat sbuf(int which, int64_t rows, int64_t cols) {
-    if (s_pending_[which]) {
-      CG_CUDA(cudaStreamWaitEvent(cs_, ev_s_[which], 0));
-      s_pending_[which] = false;
-    }
-    return view(which ? acc2_ : acc_, rows, cols);
-  }
-  void s_reader(int which) {  // a comm-stream kernel reading S was just issued
-    if (!ev_s_[which]) CG_CUDA(cudaEventCreateWithFlags(&ev_s_[which], cudaEventDisableTiming));
-    CG_CUDA(cudaEventRecord(ev_s_[which], ms_));
-    s_pending_[which] = true;
-  }
-
-  // acc_ / acc2_ / panel_ sized for big_width() (grown, eagerly, when a
+  // acc_ / panel_ sized for big_width() (grown, eagerly, when a
   // propagation-order switch widens them).
   void size_buffers() {
     const int64_t w = big_width();
     if (w <= buf_w_) return;
     acc_.alloc(tile_rows(rank_).size(), w);
-    acc2_.alloc(tile_rows(rank_).size(), w);
     for (int i = 0; i < 2; ++i) panel_[i].alloc(ceil_div64(data_.n, blocks()), w);
     buf_w_ = w;
     CG_CUDA(cudaStreamSynchronize(nullptr));  // the zeroing memsets ran on the legacy stream
