@@ -1,12 +1,19 @@
+# 2- and 4-GPU pass (gpurun --gpus 4): the multi-rank tests on NCCL (one GPU per rank) beside
+# the in-process world, and the multi-GPU bench lines (max over ranks, cost-model reconciliation).
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out/m4
-timeout 1200 python -m pytest tests -m "gpu" -q --timeout 300 -p no:cacheprovider -rf > gpurun_out/m4/pytest_multi4.log 2>&1; echo "pytest rc=$?" >> gpurun_out/m4/pytest_multi4.log
+O=gpurun_out/${ROUND_TAG:-r02}_m4
+mkdir -p $O
+nvidia-smi topo -m > $O/topo.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider -rs -k "nccl or comm or adapter" > $O/pytest_multi4.log 2>&1; echo "pytest rc=$?" >> $O/pytest_multi4.log
 run() { # name nproc args...
   name=$1; np=$2; shift 2
-  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $np --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 400)) bench.py --gpus $np "$@" > gpurun_out/m4/$name.log 2>&1; echo "rc=$?" >> gpurun_out/m4/$name.log
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $np --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 400)) bench.py --gpus $np "$@" > $O/$name.log 2>&1; echo "rc=$?" >> $O/$name.log
 }
-run 1d_n2 2 --steps 10 --warmup 3 --no-alt
-run 1d_n4 4 --steps 10 --warmup 3 --no-alt
-run 15d_n4 4 --strategy 1.5d --steps 10 --warmup 3 --no-alt
-run 2d_n4 4 --strategy 2d --steps 10 --warmup 3 --no-alt
-run 15d_n2 2 --strategy 1.5d --steps 10 --warmup 3 --no-alt
+run reddit_1d_n2 2 --steps 20 --warmup 5 --no-alt
+run reddit_1d_n4 4 --steps 20 --warmup 5 --no-alt
+run reddit_15d_n4 4 --strategy 1.5d --steps 20 --warmup 5 --no-alt
+run reddit_2d_n4 4 --strategy 2d --steps 20 --warmup 5 --no-alt
+run reddit_15d_n2 2 --strategy 1.5d --steps 20 --warmup 5 --no-alt
+run amazon_2d_n4 4 --config amazon --strategy 2d --steps 3 --warmup 3 --no-alt
+run amazon_1d_n4 4 --config amazon --steps 3 --warmup 3 --no-alt
+grep -h '^{' $O/*.log > $O/bench_multi.jsonl
