@@ -1,11 +1,15 @@
 // K1 — CSR SpMM for the GCN propagation Aᵀ·H (forward) and A·G (backward).
 //
 // Reference: spmm_add, csr.cpp:164-179 — acc(i,:) += v_k * H(c_k,:) for the
-// nonzeros of row i in ascending order.  This kernel keeps that order per
-// output element (one fp32 FMA per nonzero, sequential per lane), so the only
-// difference to the fp64 reference is fp32 rounding.
+// nonzeros of row i in ascending order.  The wide-row kernel keeps that order
+// per output element (one fp32 FMA per nonzero, sequential per lane).  The
+// narrow-row kernel (spmm_nzpar_kernel, every f <= 32 SpMM) splits a row's
+// nonzeros over QPR sub-teams — sub-team q takes the entries at positions
+// q, q + QPR, ... from the QPR-aligned start, each in ascending order — and
+// folds the QPR partial sums in a fixed xor-shuffle tree: deterministic, but
+// a different fp32 summation order than the reference's, within the 1e-4 bar.
 //
-// Mapping: a row group of LPR lanes owns one output row; each lane holds VPL
+// Wide-row mapping: a row group of LPR lanes owns one output row; each lane holds VPL
 // 128-bit column vectors of the row in registers.  Column indices and values
 // are loaded once, coalesced, by the LPR lanes of the group and broadcast to
 // the group with warp shuffles; every gathered H row is read as LPR*16 B
