@@ -400,6 +400,15 @@ void launch_tn_mi(int mi, const GemmDesc& d, int blocks, int64_t rpw, float* par
 
 bool aligned16(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; }
 
+// Rows from which the quad kernel beats the tcgen05 path (CAGNET_GEMM_QUAD_MIN).
+int64_t quad_min_rows() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("CAGNET_GEMM_QUAD_MIN");
+    return e ? std::atoll(e) : 1000000LL;
+  }();
+  return v;
+}
+
 // CAGNET_GEMM_QUAD=0 keeps the row-team kernel for k, n <= 16 (comparison).
 bool quad_enabled() {
   const char* e = std::getenv("CAGNET_GEMM_QUAD");
@@ -432,12 +441,13 @@ bool gemm_small_try(const GemmDesc& d, cudaStream_t s) {
   const int64_t kMinRows = min_rows();
   if (!small_enabled() || d.k <= 0) return false;
   const int sms = num_sms(current_device());
-  if (d.k <= 32 && d.n <= 256 && d.m >= kMinRows) {
-    const bool vec = d.a_sk == 1 && d.a_sm % 4 == 0 && aligned16(d.A) && d.a_sm >= ((d.k + 3) / 4) * 4;
-    const bool cvec = d.ldc % 4 == 0 && aligned16(d.C) &&
-                      (d.epilogue != EPI_RELU || !d.aux_out || (d.ldao % 4 == 0 && aligned16(d.aux_out))) &&
-                      (d.epilogue != EPI_RELU_PRIME || (d.ldaux % 4 == 0 && aligned16(d.aux)));
-    if (vec && cvec && d.k <= 16 && d.n <= 16 && quad_enabled()) {
+  const bool vec = d.a_sk == 1 && d.a_sm % 4 == 0 && aligned16(d.A) && d.a_sm >= ((d.k + 3) / 4) * 4;
+  const bool cvec = d.ldc % 4 == 0 && aligned16(d.C) &&
+                    (d.epilogue != EPI_RELU || !d.aux_out || (d.ldao % 4 == 0 && aligned16(d.aux_out))) &&
+                    (d.epilogue != EPI_RELU_PRIME || (d.ldaux % 4 == 0 && aligned16(d.aux)));
+  const bool quad = vec && cvec && d.k <= 16 && d.n <= 16 && quad_enabled();
+  if (d.k <= 32 && d.n <= 256 && (d.m >= kMinRows || (quad && d.m >= quad_min_rows()))) {
+    if (quad) {
       static const int R = [] {
         const char* e = std::getenv("CAGNET_GEMM_QUAD_R");  // rows in flight per lane (measured: 4 best)
         return e ? std::atoi(e) : 4;
