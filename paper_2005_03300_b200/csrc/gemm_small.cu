@@ -403,8 +403,8 @@ bool aligned16(const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0;
 // Rows from which the quad kernel beats the tcgen05 path (CAGNET_GEMM_QUAD_MIN).
 int64_t quad_min_rows() {
   static const int64_t v = [] {
-    const char* e = std::getenv("CAGNET_GEMM_QUAD_MIN");
-    return e ? std::atoll(e) : 1000000LL;
+    const char* e = std::getenv("CAGNET_GEMM_QUAD_MIN");  // Reddit (233 K rows): S·Wᵀ 30 -> 22 us
+    return e ? std::atoll(e) : 100000LL;
   }();
   return v;
 }
