@@ -389,20 +389,31 @@ def run_ours(args, cfg):
     for _ in range(2):  # warm: eager epoch, then the graph capture
         trainer.step_host(x_pin.numpy(), lab_pin.numpy())
     barrier()
-    # Per-step wall time (each step_host returns after the loss D2H); the
-    # median keeps one host hiccup out of the figure, the mean is reported too.
+    # Synchronous steps: per-step wall time of step_host (copy -> epoch -> loss
+    # D2H, nothing overlapped); the median keeps one host hiccup out.
     e2e_steps = []
     for _ in range(args.steps):
         t1 = time.perf_counter()
         trainer.step_host(x_pin.numpy(), lab_pin.numpy())
         e2e_steps.append((time.perf_counter() - t1) * 1e3)
     barrier()
-    e2e_ms = statistics.median(e2e_steps)
-    e2e_mean = statistics.mean(e2e_steps)
-    e2e_t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    sync_ms = statistics.median(e2e_steps)
+    sync_mean = statistics.mean(e2e_steps)
+    # Pipelined steps (the headline e2e): prefetch_host queues step k+1's H2D
+    # on a copy stream while step k's epoch runs; every step's copy and loss
+    # D2H are inside the timed region, which spans all K steps.
+    t1 = time.perf_counter()
+    trainer.prefetch_host(x_pin.numpy(), lab_pin.numpy())
+    for k in range(args.steps):
+        if k + 1 < args.steps:
+            trainer.prefetch_host(x_pin.numpy(), lab_pin.numpy())
+        trainer.step_prefetched()
+    pipe_ms = (time.perf_counter() - t1) * 1e3 / args.steps
+    barrier()
+    e2e_t = torch.tensor([pipe_ms, sync_ms], dtype=torch.float64, device="cuda")
     if pg:
         pg.all_reduce(e2e_t, op=pg.ReduceOp.MAX)
-    e2e_ms = float(e2e_t.item())
+    e2e_ms, sync_ms = float(e2e_t[0].item()), float(e2e_t[1].item())
     h2d = feats.size * 4 + (r1 - r0) * 4
 
     # ---- roofline of the dominant kernel (per-launch CUDA events) ------------
@@ -500,8 +511,14 @@ def run_ours(args, cfg):
                    "generator": cfg["generator"],
                    "l2": "inputs larger than L2 (CSR A+A^T and H0 > 126 MB)"},
         "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": 8, "stat": "median of per-step wall times, max over ranks",
-                "mean_ms": round(e2e_mean, 4)},
+                "d2h_bytes_per_step": 8,
+                "stat": "K pipelined steps through the public host-buffer API (prefetch_host + "
+                        "step_prefetched: each step's H2D from pinned memory overlaps the previous "
+                        "step's epoch, each step's loss read back), wall time / K, max over ranks",
+                "sync_ms": round(sync_ms, 4),
+                "sync_stat": "median per-step wall time of step_host (copy, epoch, loss D2H in "
+                             "sequence), max over ranks",
+                "sync_mean_ms": round(sync_mean, 4)},
         "gpu_launches": int(launches),
         "eager_ms_per_step": round(eager_ms_step, 4),
         "roofline": roof,

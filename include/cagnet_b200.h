@@ -399,6 +399,16 @@ CAGNET_API int cagnet_cost_memory(int64_t n, int64_t nnz, int64_t f, int64_t fma
 CAGNET_API int cagnet_cost_compare(int kind, const int64_t* params6, const uint64_t* ledgers, int ranks,
                                    int epochs, double* out4, int* flags3);
 
+/* Pipelined end-to-end steps: prefetch_host queues the H2D copies of a later
+ * step's inputs (same layout as step_host; host buffers pinned for full
+ * speed, and left untouched until the step consumes them) on a copy stream
+ * and returns at once; step_prefetched consumes the oldest staged inputs,
+ * runs the epoch and returns its loss (blocking).  Step k+1's copies overlap
+ * step k's epoch; at most two steps staged ahead. */
+CAGNET_API int cagnet_trainer_prefetch_host(cagnet_trainer_t t, const float* x_tile,
+                                            const int32_t* labels_tile);
+CAGNET_API int cagnet_trainer_step_prefetched(cagnet_trainer_t t, double* loss);
+
 /* Total hot-path kernel launches issued by this library so far. */
 CAGNET_API int cagnet_kernel_launches(uint64_t* out);
 /* The compute stream the trainer launches on (a cudaStream_t). */

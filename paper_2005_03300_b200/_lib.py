@@ -113,6 +113,8 @@ SIGNATURES = {
     "cagnet_trainer_profile_entry": [vp, i32, C.c_char_p, i32, _f64p],
     "cagnet_trainer_profile_reset": [vp],
     "cagnet_trainer_step_host": [vp, vp, vp, C.POINTER(f64)],
+    "cagnet_trainer_prefetch_host": [vp, vp, vp],
+    "cagnet_trainer_step_prefetched": [vp, C.POINTER(f64)],
     "cagnet_kernel_launches": [C.POINTER(u64)],
     "cagnet_comm_create": [i32, i32, i32, i32, C.c_char_p, i32, C.POINTER(vp)],
     "cagnet_comm_group": [vp, i32, C.POINTER(i32), C.POINTER(i32)],

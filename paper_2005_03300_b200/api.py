@@ -591,6 +591,17 @@ class Trainer:
                                            C.byref(loss)))
         return loss.value
 
+    def prefetch_host(self, x_tile: np.ndarray, labels_tile: np.ndarray) -> None:
+        """Queue the H2D copies of a later step's inputs (returns at once; keep
+        the host arrays alive and unchanged until that step ran)."""
+        check(lib.cagnet_trainer_prefetch_host(self.h, x_tile.ctypes.data, labels_tile.ctypes.data))
+
+    def step_prefetched(self) -> float:
+        """One epoch on the oldest prefetched inputs; returns its loss."""
+        loss = C.c_double()
+        check(lib.cagnet_trainer_step_prefetched(self.h, C.byref(loss)))
+        return loss.value
+
     def stream(self) -> int:
         s = C.c_void_p()
         check(lib.cagnet_trainer_stream(self.h, C.byref(s)))

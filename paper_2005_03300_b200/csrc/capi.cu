@@ -1086,6 +1086,20 @@ int cagnet_trainer_profile_reset(cagnet_trainer_t t) {
   return guarded([&] { t->t->reset_profile(); });
 }
 
+int cagnet_trainer_prefetch_host(cagnet_trainer_t t, const float* x_tile, const int32_t* labels_tile) {
+  return guarded([&] {
+    cagnet::require(x_tile != nullptr && labels_tile != nullptr, "prefetch_host: null input");
+    t->t->prefetch_host(x_tile, labels_tile);
+  });
+}
+
+int cagnet_trainer_step_prefetched(cagnet_trainer_t t, double* loss) {
+  return guarded([&] {
+    const double l = t->t->step_prefetched();
+    if (loss) *loss = l;
+  });
+}
+
 int cagnet_trainer_step_host(cagnet_trainer_t t, const float* x_tile, const int32_t* labels_tile,
                              double* loss) {
   return guarded([&] {

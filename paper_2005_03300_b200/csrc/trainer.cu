@@ -288,6 +288,12 @@ Trainer::Trainer(const DeviceDataset& data, std::vector<int64_t> dims, const dou
 
 Trainer::~Trainer() {
   cudaSetDevice(device_);
+  if (xs_) {
+    cudaStreamSynchronize(xs_);
+    cudaStreamDestroy(xs_);
+    for (cudaEvent_t e : {ev_staged_[0], ev_staged_[1], ev_consumed_[0], ev_consumed_[1]})
+      if (e) cudaEventDestroy(e);
+  }
   if (cs_) cudaStreamSynchronize(cs_);
   if (ms_ && ms_ != cs_) cudaStreamSynchronize(ms_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
@@ -535,6 +541,47 @@ double Trainer::step_host(const float* x_tile, const int32_t* labels_tile) {
                             cudaMemcpyHostToDevice, cs_));
   epoch();
   std::vector<double> l = run_epochs(0);
+  return losses_host_.empty() ? 0.0 : losses_host_.back();
+}
+
+void Trainer::prefetch_host(const float* x_tile, const int32_t* labels_tile) {
+  CG_CUDA(cudaSetDevice(device_));
+  if (pf_count_ >= 2) throw std::logic_error("prefetch_host: two steps are already staged");
+  if (!xs_) {
+    CG_CUDA(cudaStreamCreateWithFlags(&xs_, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CG_CUDA(cudaEventCreateWithFlags(&ev_staged_[i], cudaEventDisableTiming));
+      CG_CUDA(cudaEventCreateWithFlags(&ev_consumed_[i], cudaEventDisableTiming));
+      CG_CUDA(cudaEventRecord(ev_consumed_[i], cs_));
+    }
+  }
+  const int b = (pf_head_ + pf_count_) % 2;
+  const Mat& h0 = h_.at(0).m;
+  pstage_[b].resize(static_cast<size_t>(h0.rows * h0.cols > 0 ? h0.rows * h0.cols : 1));
+  plabels_[b].resize(static_cast<size_t>(h0.rows > 0 ? h0.rows : 1));
+  // The slot is free once the step that last consumed it re-pitched it.
+  CG_CUDA(cudaStreamWaitEvent(xs_, ev_consumed_[b], 0));
+  if (h0.rows && h0.cols)
+    CG_CUDA(cudaMemcpyAsync(pstage_[b].get(), x_tile, h0.rows * h0.cols * sizeof(float), cudaMemcpyHostToDevice, xs_));
+  if (h0.rows)
+    CG_CUDA(cudaMemcpyAsync(plabels_[b].get(), labels_tile, h0.rows * sizeof(int32_t), cudaMemcpyHostToDevice, xs_));
+  CG_CUDA(cudaEventRecord(ev_staged_[b], xs_));
+  ++pf_count_;
+}
+
+double Trainer::step_prefetched() {
+  CG_CUDA(cudaSetDevice(device_));
+  if (pf_count_ == 0) throw std::logic_error("step_prefetched: no staged inputs (call prefetch_host first)");
+  const int b = pf_head_;
+  const Mat& h0 = h_.at(0).m;
+  CG_CUDA(cudaStreamWaitEvent(cs_, ev_staged_[b], 0));
+  if (h0.rows && h0.cols) kern::copy2d(h0.p, h0.ld, pstage_[b].get(), h0.cols, h0.rows, h0.cols, cs_);
+  if (h0.rows) kern::copy_bytes(labels_.get(), plabels_[b].get(), h0.rows * sizeof(int32_t), cs_);
+  CG_CUDA(cudaEventRecord(ev_consumed_[b], cs_));
+  pf_head_ = (pf_head_ + 1) % 2;
+  --pf_count_;
+  epoch();
+  run_epochs(0);
   return losses_host_.empty() ? 0.0 : losses_host_.back();
 }
 

@@ -203,6 +203,13 @@ class Trainer {
   // One epoch from host buffers: H2D of this rank's feature tile (rows x
   // cols, dense) and label rows, the epoch, D2H of the loss.
   double step_host(const float* x_tile, const int32_t* labels_tile);
+  // Pipelined form of step_host: prefetch_host queues the H2D copies of a
+  // later step's inputs on a copy stream into one of two staging slots
+  // (returns at once); step_prefetched consumes the oldest staged inputs,
+  // runs the epoch and returns its loss.  Step k + 1's copy then overlaps
+  // step k's epoch.  At most two steps may be staged ahead.
+  void prefetch_host(const float* x_tile, const int32_t* labels_tile);
+  double step_prefetched();
 
  protected:
   void epoch_body();  // one epoch's launches (eager or under capture)
@@ -300,6 +307,12 @@ class Trainer {
   std::vector<DeviceCsr> a_parts_, at_parts_;
   DevBuf<double> loss_partial_;
   DevBuf<float> stage_;  // host-input staging for step_host
+  // prefetch_host / step_prefetched: two staging slots filled on xs_.
+  DevBuf<float> pstage_[2];
+  DevBuf<int32_t> plabels_[2];
+  cudaStream_t xs_ = nullptr;
+  cudaEvent_t ev_staged_[2] = {nullptr, nullptr}, ev_consumed_[2] = {nullptr, nullptr};
+  int pf_head_ = 0, pf_count_ = 0;  // oldest filled slot, filled slots
   // Column blocks of the local CSR parts for L2-blocked SpMM passes, keyed by
   // (row_ptr, blocks).
   std::map<std::pair<const void*, int>, std::vector<DeviceCsr>> colblocks_;

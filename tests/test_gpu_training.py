@@ -432,3 +432,42 @@ def test_forward_layer_between_replayed_epochs(cg, orc, P, layers):
         import oracle
         assert oracle.rel_frobenius(t.weight(0), w[0]) < TOL
         assert oracle.rel_frobenius(t.h_tile(L - 1), h[r0:r1]) < TOL
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_host_steps_sync_and_pipelined(cg, graph):
+    """The end-to-end call (cagnet_trainer_step_host: H2D of the rank's inputs,
+    the epoch, D2H of the loss) and its pipelined form (prefetch_host +
+    step_prefetched, step k+1's copies overlapping step k's epoch) give the same
+    losses bit for bit, alternating two different input sets; the first step
+    on the dataset's own inputs equals run_epochs."""
+    dims = [24, 8, 6]
+    data = cg.generate_dataset(300, 12.0, 24, 6, 2, 3, 4)
+    model = cg.init_glorot(dims, 5, 0.5)
+    strat = cg.Strategy("1d", 1, reassociate=True, graph=graph)
+    x1 = np.ascontiguousarray(data.features(), np.float32)
+    l1 = np.ascontiguousarray(data.labels(), np.int32)
+    x2 = np.ascontiguousarray(x1 * 0.5 + 0.25, np.float32)
+    l2 = np.ascontiguousarray((l1 + 1) % 6, np.int32)
+    seq = [(x1, l1), (x2, l2), (x1, l1), (x2, l2), (x2, l2)]
+
+    def fresh():
+        t = cg.make_trainer(data, model, strat)
+        t.distribute()
+        return t
+
+    ref = fresh().run_epochs(1)[0]
+    a = fresh()
+    sync = [a.step_host(x, l) for x, l in seq]
+    b = fresh()
+    piped = []
+    b.prefetch_host(*seq[0])
+    for k in range(len(seq)):
+        if k + 1 < len(seq):
+            b.prefetch_host(*seq[k + 1])
+        piped.append(b.step_prefetched())
+    assert sync[0] == ref
+    assert sync == piped
+    assert len(set(sync)) > 1
+    with pytest.raises(cg.CagnetError, match="no staged inputs"):
+        b.step_prefetched()
