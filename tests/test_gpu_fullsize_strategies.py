@@ -50,3 +50,4 @@ def test_amazon_strategies_agree(cg, amazon, single, kind, P, repl):
     print(kind, P, {k: f"{v:.2e}" for k, v in errs.items()})
     assert max(v for k, v in errs.items() if not k.startswith("g")) < 1e-4, errs
     assert max(v for k, v in errs.items() if k.startswith("g")) < 1e-3, errs
+
