@@ -1002,6 +1002,7 @@ int cagnet_trainer_part(cagnet_trainer_t t, int which, int part, cagnet_csr_t* o
                          cudaMemcpyDeviceToDevice));
       CG_CUDA(cudaMemcpy(h->csr.vals.get(), src.vals.get(), src.nnz * sizeof(float), cudaMemcpyDeviceToDevice));
     }
+    CG_CUDA(cudaStreamSynchronize(nullptr));  // D2D cudaMemcpy returns before it completes
     *out = h.release();
   });
 }

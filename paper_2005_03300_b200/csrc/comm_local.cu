@@ -290,19 +290,30 @@ std::vector<std::vector<char>> LocalCollectives::arrive(const Group& g, std::vec
 }
 
 std::vector<std::pair<const void*, void*>> LocalCollectives::enter(const Group& g, const void* a, void* b,
-                                                                   cudaStream_t s) {
+                                                                   cudaStream_t s, uint64_t sig) {
   const int S = static_cast<int>(g.size());
-  std::vector<char> mine(2 * sizeof(void*));
+  std::vector<char> mine(2 * sizeof(void*) + sizeof(uint64_t));
   std::memcpy(mine.data(), &a, sizeof(void*));
   std::memcpy(mine.data() + sizeof(void*), &b, sizeof(void*));
+  std::memcpy(mine.data() + 2 * sizeof(void*), &sig, sizeof(uint64_t));
   auto all = arrive(g, std::move(mine), s);
   std::vector<std::pair<const void*, void*>> out(static_cast<size_t>(S));
   for (int q = 0; q < S; ++q) {
     std::memcpy(&out[q].first, all[q].data(), sizeof(void*));
     std::memcpy(&out[q].second, all[q].data() + sizeof(void*), sizeof(void*));
+    uint64_t other = 0;
+    std::memcpy(&other, all[q].data() + 2 * sizeof(void*), sizeof(uint64_t));
+    if (other != sig)
+      throw std::logic_error("local collective mismatch in group " + std::to_string(g.id) + ": rank " +
+                             std::to_string(rank_) + " call signature " + std::to_string(sig) +
+                             ", member " + std::to_string(q) + " " + std::to_string(other));
   }
   return out;
 }
+
+namespace {
+uint64_t call_sig(uint64_t op, uint64_t root, uint64_t size) { return (op << 56) ^ (root << 48) ^ size; }
+}  // namespace
 
 void LocalCollectives::leave(const Group& g, cudaStream_t s) {
   const int S = static_cast<int>(g.size());
@@ -333,7 +344,7 @@ char* LocalCollectives::scratch(size_t bytes, cudaStream_t s) {
 }
 
 void LocalCollectives::bcast(const Group& g, int root_member, void* buf, size_t bytes, cudaStream_t s) {
-  auto p = enter(g, buf, buf, s);
+  auto p = enter(g, buf, buf, s, call_sig(1, static_cast<uint64_t>(root_member), bytes));
   if (g.index_of(rank_) != root_member && bytes)
     kern::copy_bytes(buf, p[static_cast<size_t>(root_member)].first, bytes, s);
   leave(g, s);
@@ -342,11 +353,17 @@ void LocalCollectives::bcast(const Group& g, int root_member, void* buf, size_t 
 void LocalCollectives::bcast3(const Group& g, int root_member, void* a, size_t na, void* b, size_t nb,
                               void* c, size_t nc, cudaStream_t s) {
   const int m = g.index_of(rank_);
-  std::vector<char> mine(3 * sizeof(void*));
+  std::vector<char> mine(3 * sizeof(void*) + 3 * sizeof(size_t));
   std::memcpy(mine.data(), &a, sizeof(void*));
   std::memcpy(mine.data() + sizeof(void*), &b, sizeof(void*));
   std::memcpy(mine.data() + 2 * sizeof(void*), &c, sizeof(void*));
+  const size_t sizes[3] = {na, nb, nc};
+  std::memcpy(mine.data() + 3 * sizeof(void*), sizes, sizeof(sizes));
   auto all = arrive(g, std::move(mine), s);
+  for (size_t q = 0; q < all.size(); ++q)
+    if (std::memcmp(all[q].data() + 3 * sizeof(void*), sizes, sizeof(sizes)) != 0)
+      throw std::logic_error("local bcast3 size mismatch in group " + std::to_string(g.id) + ": rank " +
+                             std::to_string(rank_) + " vs member " + std::to_string(q));
   if (m != root_member) {
     const std::vector<char>& r = all[static_cast<size_t>(root_member)];
     void* src[3];
@@ -361,7 +378,7 @@ void LocalCollectives::bcast3(const Group& g, int root_member, void* a, size_t n
 void LocalCollectives::all_reduce(const Group& g, void* buf, size_t count, int dtype, cudaStream_t s) {
   const size_t es = dtype == 1 ? 8 : 4;
   char* tmp = scratch(count * es, s);
-  auto p = enter(g, buf, buf, s);
+  auto p = enter(g, buf, buf, s, call_sig(2, static_cast<uint64_t>(dtype), count));
   std::vector<const void*> src;
   for (auto& e : p) src.push_back(e.first);
   if (dtype == 1)
@@ -374,7 +391,7 @@ void LocalCollectives::all_reduce(const Group& g, void* buf, size_t count, int d
 
 void LocalCollectives::reduce_scatter(const Group& g, const void* send, void* recv, size_t slice, int dtype,
                                       cudaStream_t s) {
-  auto p = enter(g, send, recv, s);
+  auto p = enter(g, send, recv, s, call_sig(3, static_cast<uint64_t>(dtype), slice));
   const int m = g.index_of(rank_);
   std::vector<const void*> src;
   for (auto& e : p) src.push_back(e.first);
@@ -387,7 +404,7 @@ void LocalCollectives::reduce_scatter(const Group& g, const void* send, void* re
 
 void LocalCollectives::all_gather(const Group& g, const void* send, void* recv, size_t slice_bytes,
                                   cudaStream_t s) {
-  auto p = enter(g, send, recv, s);
+  auto p = enter(g, send, recv, s, call_sig(4, 0, slice_bytes));
   for (size_t q = 0; q < p.size(); ++q) {
     char* dst = static_cast<char*>(recv) + q * slice_bytes;
     if (dst != p[q].first) kern::copy_bytes(dst, p[q].first, slice_bytes, s);

@@ -139,8 +139,10 @@ class LocalCollectives {
   // Raise + rendezvous (payload exchange) + arrive wait.
   std::vector<std::vector<char>> arrive(const Group& g, std::vector<char> mine, cudaStream_t s);
   // Rendezvous + arrive barrier; returns the members' (a, b) pointers.
+  // sig: the call's shape (operation, root, sizes); every member must pass
+  // the same one — a mismatch is a host-side bug and throws.
   std::vector<std::pair<const void*, void*>> enter(const Group& g, const void* a, void* b,
-                                                   cudaStream_t s);
+                                                   cudaStream_t s, uint64_t sig);
   void leave(const Group& g, cudaStream_t s);
   char* scratch(size_t bytes, cudaStream_t s);
 

@@ -559,6 +559,8 @@ DeviceCsr extract_block_device(const DeviceCsr& a, int64_t r0, int64_t r1, int64
   b.device = current_device();
   b.n_rows = r1 - r0;
   b.n_cols = c1 - c0;
+  b.row_off = a.row_off + r0;
+  b.col_off = a.col_off + c0;
   b.row_ptr.resize(static_cast<size_t>(b.n_rows + 1));
   if (b.n_rows == 0) {
     CG_CUDA(cudaMemsetAsync(b.row_ptr.get(), 0, sizeof(int64_t), s));

@@ -16,6 +16,9 @@ struct DeviceCsr {
   DevBuf<int64_t> row_ptr;  // n_rows + 1
   DevBuf<int32_t> col_idx;  // nnz
   DevBuf<float> vals;       // nnz
+  // Global row / column of local (0, 0) when this is a block of a dataset matrix
+  // (extract_block); the packed SpMM stream checks its values against them.
+  int64_t row_off = 0, col_off = 0;
 };
 
 // csr.cpp:195-218 — every ordered pair (u, v != u) consumes one draw of the

@@ -633,6 +633,9 @@ std::unique_ptr<DeviceDataset> dataset_load_binary(const std::string& path, int 
       CG_CUDA(cudaMemcpy(d->labels.get(), la, static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice));
       CG_CUDA(cudaMemcpy(d->mask.get(), ma, static_cast<size_t>(n), cudaMemcpyHostToDevice));
     }
+    // Pageable H2D copies may return before their DMA lands; the dataset's
+    // users run on non-blocking streams.
+    CG_CUDA(cudaStreamSynchronize(nullptr));
     if (left != 0) throw std::runtime_error("load_dataset_binary: trailing bytes in " + path);
   } catch (...) {
     cudaStreamDestroy(s);

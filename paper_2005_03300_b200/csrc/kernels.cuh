@@ -40,6 +40,17 @@ struct SpmmEpi {
 constexpr int kSpmmEpiMaxF = 32;
 constexpr int kSpmmEpiMaxFo = 64;
 
+// Packed nonzero stream of a block of the normalized adjacency (pack_normalized):
+// entry k = (d << bits) | col, d the column vertex's degree in A + I; the value
+// 1/sqrt(d_row d_col) (csr.cpp:94-116) is rebuilt as row_scale[row] * rsqrt(d), so
+// the narrow-row kernel streams 4 B per nonzero — one L1 wavefront per 8 entries —
+// instead of 8 B in two (values agree to ~5e-7 relative, inside the 1e-4 bar).
+struct SpmmPacked {
+  const uint32_t* e = nullptr;
+  const float* row_scale = nullptr;
+  int bits = 0;
+};
+
 // T[i, 0:f] = (accumulate ? T[i, 0:f] : 0) + sum_k vals[k] * H[col[k], 0:f]
 // with the nonzeros of each row folded in ascending order (the reference's
 // accumulation order), one fp32 FMA per term.
@@ -49,16 +60,28 @@ constexpr int kSpmmEpiMaxFo = 64;
 void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
               const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
               cudaStream_t stream, int64_t nnz = -1, const SpmmEpi* epi = nullptr,
-              const int2* colval = nullptr);
+              const int2* colval = nullptr, const SpmmPacked* packed = nullptr);
 
 // Same, with row i's nonzeros given as [seg_begin[i], seg_end[i]).
 void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_end,
                    const int32_t* col_idx, const float* vals, const float* H, int64_t ldh, int f,
                    float* T, int64_t ldt, bool accumulate, cudaStream_t stream, int64_t nnz = -1,
-                   const SpmmEpi* epi = nullptr, const int2* colval = nullptr);
+                   const SpmmEpi* epi = nullptr, const int2* colval = nullptr,
+                   const SpmmPacked* packed = nullptr);
 // out[k] = {col_idx[k], bits of vals[k]} for the interleaved nonzero stream.
 void interleave_colval(int64_t nnz, const int32_t* col_idx, const float* vals, int2* out,
                        cudaStream_t stream);
+// The packed stream of a block whose local (0, 0) is (row_off, col_off) of a
+// normalized dataset matrix; deg = degrees of A + I of every vertex.  Adds to
+// *bad (device counter) every nonzero whose value is not bitwise
+// (float)(1/sqrt(d_r d_c)) or whose degree needs more than 32 - bits bits; the
+// stream is only usable when *bad stays 0.
+// deg[i] = row_ptr[i + 1] - row_ptr[i].
+void row_degrees(int64_t n, const int64_t* row_ptr, int32_t* deg, cudaStream_t stream);
+void pack_normalized(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
+                     const float* vals, const int32_t* deg, int64_t row_off, int64_t col_off,
+                     int bits, uint32_t* out, float* row_scale, unsigned long long* bad,
+                     cudaStream_t stream);
 // split[b * rows + r] (b = 0..nb) = first nonzero of row r in column block b
 // of the ceiling-rule split of n_cols into nb blocks; split[nb * rows + r] = row end.
 void column_splits(int64_t rows, int64_t n_cols, int nb, const int64_t* row_ptr,

@@ -159,6 +159,8 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
   }
   CG_CUDA(cudaMalloc(reinterpret_cast<void**>(&flags_), (P + 3) * sizeof(uint64_t)));
   CG_CUDA(cudaMemset(flags_, 0, (P + 3) * sizeof(uint64_t)));
+  // Legacy-stream zeroing: finished before any peer (non-blocking streams) can write.
+  CG_CUDA(cudaStreamSynchronize(nullptr));
 
   PeerInfo mine{};
   void* ptrs[kAllocs];
@@ -179,6 +181,7 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
   std::vector<uint64_t> hsend(words, 0), hrecv(words * P, 0);
   std::memcpy(hsend.data(), &mine, sizeof(PeerInfo));
   CG_CUDA(cudaMemcpy(dsend.get(), hsend.data(), words * 8, cudaMemcpyHostToDevice));
+  CG_CUDA(cudaStreamSynchronize(nullptr));  // legacy-stream copy done before the non-blocking streams read it
   comm.setup_all_gather(dsend.get(), drecv.get(), words, ncclUint64, s);
   CG_CUDA(cudaStreamSynchronize(s));
   CG_CUDA(cudaMemcpy(hrecv.data(), drecv.get(), words * P * 8, cudaMemcpyDeviceToHost));
@@ -238,6 +241,7 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
   DevBuf<int32_t> vs(1), va(static_cast<size_t>(P));
   const int32_t v = ok ? 1 : 0;
   CG_CUDA(cudaMemcpy(vs.get(), &v, sizeof(v), cudaMemcpyHostToDevice));
+  CG_CUDA(cudaStreamSynchronize(nullptr));  // legacy-stream copy done before the non-blocking streams read it
   comm.setup_all_gather(vs.get(), va.get(), 1, ncclInt32, s);
   CG_CUDA(cudaStreamSynchronize(s));
   std::vector<int32_t> verdicts(static_cast<size_t>(P));
@@ -260,6 +264,7 @@ bool PeerPanels::init(Comm& comm, int rank, int ranks, int device, size_t bytes,
   }
   d_flags_.resize(static_cast<size_t>(P));
   CG_CUDA(cudaMemcpy(d_flags_.get(), peer_flags_.data(), P * sizeof(uint64_t*), cudaMemcpyHostToDevice));
+  CG_CUDA(cudaStreamSynchronize(nullptr));  // legacy-stream copy done before the non-blocking streams read it
   return true;
 }
 

@@ -106,6 +106,7 @@ struct SpmmArgs {
   // Optional interleaved copy of (col_idx, vals) as int2 {col, float bits}:
   // one 8 B load per nonzero instead of two 4 B loads (narrow-row kernel).
   const int2* colval = nullptr;
+  SpmmPacked packed;  // packed.e != nullptr: the packed stream (narrow-row kernel, LV = 4)
 };
 
 // VEC = 4: 16-byte vectors (requires 16 B aligned rows, ld a multiple of 4); VEC = 1: scalars.
@@ -377,11 +378,13 @@ __device__ __forceinline__ void spmm_row_epilogue(const SpmmArgs& a, int64_t row
 // row's nonzeros (sub-team q takes q, q+QPR, ...), so every lane streams
 // independent gathers with no shuffles in the loop (U in flight); the QPR
 // partial sums are folded with xor shuffles at the end (deterministic order).
-// CV: the nonzeros come from the interleaved (col, value) stream a.colval —
-// per warp instruction the 8 sub-teams then read 8 consecutive 8 B entries (one
-// L1 wavefront) instead of 8 columns and 8 values (two), which matters because
-// the kernel is bound by L1 LSU wavefronts (one per gathered row).
-template <int LV, int QPR, int U, bool ACC, bool CV, int NT = kThreads, int HINT = 0,
+// CV = 1: the nonzeros come from the interleaved (col, value) stream a.colval
+// (one 8 B load per step instead of a column and a value load).  CV = 2: the
+// packed stream a.packed — 4 B per nonzero, 8 sub-teams' entries in 32 B: one L1
+// wavefront per step, where 8 B loads take about two (half-warp passes); the
+// kernel is bound by L1 LSU wavefronts (one per gathered 64 B row), so this is
+// ~10 % of its time (profiles/r02_micro_packed_stream.txt).
+template <int LV, int QPR, int U, bool ACC, int CV, int NT = kThreads, int HINT = 0,
           bool FULLV = false, bool EPI = false>
 __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArgs a) {
   constexpr int TEAM = LV * QPR;
@@ -421,7 +424,43 @@ __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArg
   // gathered H rows out of L2.
   auto ld_c = [&](const int32_t* p) { return HINT ? __ldcs(p) : __ldg(p); };
   auto ld_v = [&](const float* p) { return HINT ? __ldcs(p) : __ldg(p); };
-  if constexpr (CV) {
+  if constexpr (CV == 2) {
+    // Same walk over the packed stream; w = rsqrt(d_col), the row scale is
+    // applied once after the fold.
+    const uint32_t* __restrict__ pk = a.packed.e;
+    const int bits = a.packed.bits;
+    const uint32_t cmask = (1u << bits) - 1u;
+    auto weight = [&](uint32_t x) { return rsqrtf(static_cast<float>(x >> bits)); };
+    const uint32_t* pe = pk + nz_e;
+    const uint32_t* p = pk + nz_b + q;
+    if constexpr (QPR > 1) {
+      const int64_t head = nz_b & ~static_cast<int64_t>(QPR - 1);
+      if (head != nz_b) {
+        const uint32_t* hp = pk + head + q;
+        if (hp >= pk + nz_b && hp < pe) {
+          const uint32_t x = __ldg(hp);
+          fma_vec(acc, weight(x), gather(static_cast<int>(x & cmask)));
+        }
+        p = hp + QPR;
+      }
+    }
+    for (; p + (U - 1) * QPR < pe; p += U * QPR) {
+      float4 h[U];
+      float w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t x = __ldg(p + u * QPR);
+        w[u] = weight(x);
+        h[u] = gather(static_cast<int>(x & cmask));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) fma_vec(acc, w[u], h[u]);
+    }
+    for (; p < pe; p += QPR) {
+      const uint32_t x = __ldg(p);
+      fma_vec(acc, weight(x), gather(static_cast<int>(x & cmask)));
+    }
+  } else if constexpr (CV) {
     // The QPR sub-teams read QPR consecutive {col, val} entries per step; the
     // row's segment is walked from the QPR-aligned entry at or below nz_b, so
     // every step's entries sit in one 64 B-aligned chunk (one L1 wavefront,
@@ -477,6 +516,15 @@ __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArg
     acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
     acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
   }
+  if constexpr (CV == 2) {
+    if (row < a.n_rows) {
+      const float s = __ldg(a.packed.row_scale + row);
+      acc.x *= s;
+      acc.y *= s;
+      acc.z *= s;
+      acc.w *= s;
+    }
+  }
   if constexpr (EPI) {
     if (ACC && row < a.n_rows && vec_ok) {
       // Final pass of a split propagation: fold in the earlier passes' partial.
@@ -504,7 +552,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArg
   }
 }
 
-template <int LV, int QPR, int U, int NT, int HINT, bool CV>
+template <int LV, int QPR, int U, int NT, int HINT, int CV>
 void launch_nzpar_cv(const SpmmArgs& a, bool acc, bool epi, unsigned g, bool full, cudaStream_t s) {
   if (epi && acc) {
     if (full)
@@ -535,10 +583,17 @@ void launch_nzpar_v(const SpmmArgs& a, bool acc, bool epi, cudaStream_t s) {
   const unsigned g = static_cast<unsigned>(ceil_div64(a.n_rows, rows_per_block));
   // Full vectors: every lane of the LV-wide row team owns a live float4.
   const bool full = (a.f + 3) / 4 == LV;
+  if constexpr (LV == 4) {
+    if (a.packed.e) {
+      launch_nzpar_cv<LV, QPR, U, NT, HINT, 2>(a, acc, epi, g, full, s);
+      CG_LAUNCH_CHECK();
+      return;
+    }
+  }
   if (a.colval)
-    launch_nzpar_cv<LV, QPR, U, NT, HINT, true>(a, acc, epi, g, full, s);
+    launch_nzpar_cv<LV, QPR, U, NT, HINT, 1>(a, acc, epi, g, full, s);
   else
-    launch_nzpar_cv<LV, QPR, U, NT, HINT, false>(a, acc, epi, g, full, s);
+    launch_nzpar_cv<LV, QPR, U, NT, HINT, 0>(a, acc, epi, g, full, s);
   CG_LAUNCH_CHECK();
 }
 
@@ -633,7 +688,7 @@ __global__ void column_splits_kernel(int64_t rows, int nb, int64_t step,
 void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_end,
                    const int32_t* col_idx, const float* vals, const float* H, int64_t ldh, int f,
                    float* T, int64_t ldt, bool accumulate, cudaStream_t stream, int64_t nnz,
-                   const SpmmEpi* epi, const int2* colval) {
+                   const SpmmEpi* epi, const int2* colval, const SpmmPacked* packed) {
   if (n_rows <= 0 || f <= 0) return;
   const double mean = nnz >= 0 ? static_cast<double>(nnz) / static_cast<double>(n_rows) : 64.0;
   const bool aligned = (ldh % 4 == 0) && (ldt % 4 == 0) &&
@@ -644,7 +699,8 @@ void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_
             "spmm: fused epilogue needs a final f <= 32 SpMM on 16 B-aligned rows");
     require(!accumulate || epi->W == nullptr,
             "spmm: an accumulating fused epilogue cannot change the row width");
-    SpmmArgs a{n_rows, seg_begin, seg_end, col_idx, vals, H, ldh, f, T, ldt, mean, *epi, colval};
+    SpmmArgs a{n_rows, seg_begin, seg_end, col_idx, vals, H, ldh, f, T, ldt, mean, *epi, colval,
+               packed ? *packed : SpmmPacked{}};
     dispatch<4>(a, accumulate, true, stream);
     return;
   }
@@ -652,7 +708,7 @@ void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_
   const int chunk = aligned ? 32 * 8 * 4 : 32 * 8;
   for (int c0 = 0; c0 < f; c0 += chunk) {
     SpmmArgs a{n_rows, seg_begin, seg_end, col_idx, vals, H + c0, ldh, f - c0 < chunk ? f - c0 : chunk,
-               T + c0, ldt, mean, SpmmEpi{}, colval};
+               T + c0, ldt, mean, SpmmEpi{}, colval, packed ? *packed : SpmmPacked{}};
     if (aligned)
       dispatch<4>(a, accumulate, false, stream);
     else
@@ -662,9 +718,10 @@ void spmm_segments(int64_t n_rows, const int64_t* seg_begin, const int64_t* seg_
 
 void spmm_csr(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx, const float* vals,
               const float* H, int64_t ldh, int f, float* T, int64_t ldt, bool accumulate,
-              cudaStream_t stream, int64_t nnz, const SpmmEpi* epi, const int2* colval) {
+              cudaStream_t stream, int64_t nnz, const SpmmEpi* epi, const int2* colval,
+              const SpmmPacked* packed) {
   spmm_segments(n_rows, row_ptr, row_ptr + 1, col_idx, vals, H, ldh, f, T, ldt, accumulate, stream,
-                nnz, epi, colval);
+                nnz, epi, colval, packed);
 }
 
 namespace {
@@ -674,7 +731,59 @@ __global__ void interleave_kernel(int64_t nnz, const int32_t* __restrict__ ci, c
        k += static_cast<int64_t>(gridDim.x) * blockDim.x)
     out[k] = make_int2(ci[k], __float_as_int(v[k]));
 }
+
+// Warp per row: the row scale, then the row's entries (lanes over nonzeros).
+__global__ void pack_normalized_kernel(int64_t n_rows, const int64_t* __restrict__ row_ptr,
+                                       const int32_t* __restrict__ col_idx,
+                                       const float* __restrict__ vals, const int32_t* __restrict__ deg,
+                                       int64_t row_off, int64_t col_off, int bits,
+                                       uint32_t* __restrict__ out, float* __restrict__ row_scale,
+                                       unsigned long long* bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const uint32_t dmax = bits >= 32 ? 0u : (0xffffffffu >> bits);
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n_rows; r += warps) {
+    const double dr = static_cast<double>(deg[row_off + r]);
+    if (lane == 0) row_scale[r] = static_cast<float>(1.0 / sqrt(dr));
+    unsigned long long nbad = 0;
+    for (int64_t k = row_ptr[r] + lane; k < row_ptr[r + 1]; k += 32) {
+      const int32_t c = col_idx[k];
+      const int32_t dc = deg[col_off + c];
+      // dataset normalization (graph.cu normalize_device, csr.cpp:94-116), bitwise
+      const float want = static_cast<float>(1.0 / sqrt(dr * static_cast<double>(dc)));
+      const bool ok = __float_as_uint(want) == __float_as_uint(vals[k]) && dc > 0 &&
+                      static_cast<uint32_t>(dc) <= dmax && (static_cast<uint32_t>(c) >> bits) == 0;
+      nbad += ok ? 0 : 1;
+      out[k] = (static_cast<uint32_t>(dc) << bits) | static_cast<uint32_t>(c);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nbad += __shfl_xor_sync(0xffffffffu, nbad, o);
+    if (lane == 0 && nbad) atomicAdd(bad, nbad);
+  }
+}
+__global__ void row_degrees_kernel(int64_t n, const int64_t* __restrict__ rp, int32_t* __restrict__ deg) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) deg[i] = static_cast<int32_t>(rp[i + 1] - rp[i]);
+}
 }  // namespace
+
+void row_degrees(int64_t n, const int64_t* row_ptr, int32_t* deg, cudaStream_t s) {
+  if (n <= 0) return;
+  row_degrees_kernel<<<static_cast<unsigned>(ceil_div64(n, 256)), 256, 0, s>>>(n, row_ptr, deg);
+  CG_LAUNCH_CHECK();
+}
+
+void pack_normalized(int64_t n_rows, const int64_t* row_ptr, const int32_t* col_idx,
+                     const float* vals, const int32_t* deg, int64_t row_off, int64_t col_off,
+                     int bits, uint32_t* out, float* row_scale, unsigned long long* bad,
+                     cudaStream_t s) {
+  if (n_rows <= 0) return;
+  const int64_t want = ceil_div64(n_rows, 8);
+  const unsigned g = static_cast<unsigned>(want < 16LL * 1024 ? want : 16LL * 1024);
+  pack_normalized_kernel<<<g, 256, 0, s>>>(n_rows, row_ptr, col_idx, vals, deg, row_off, col_off, bits,
+                                           out, row_scale, bad);
+  CG_LAUNCH_CHECK();
+}
 
 void interleave_colval(int64_t nnz, const int32_t* col_idx, const float* vals, int2* out, cudaStream_t s) {
   if (nnz <= 0) return;

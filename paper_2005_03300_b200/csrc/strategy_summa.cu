@@ -47,6 +47,7 @@ class TrainerSumma final : public Trainer {
     DevBuf<int64_t> mine(4), all(static_cast<size_t>(4 * P));
     const int64_t m4[4] = {a_parts_[0].n_rows, a_parts_[0].n_cols, a_parts_[0].nnz, at_parts_[0].nnz};
     CG_CUDA(cudaMemcpy(mine.get(), m4, sizeof(m4), cudaMemcpyHostToDevice));
+    CG_CUDA(cudaStreamSynchronize(nullptr));  // pageable H2D: DMA done before cs_ reads it
     comm_->setup_all_gather(mine.get(), all.get(), 4, ncclInt64, cs_);
     shapes_.assign(static_cast<size_t>(4 * P), 0);
     CG_CUDA(cudaStreamSynchronize(cs_));

@@ -210,7 +210,11 @@ void OwnedMat::alloc(int64_t rows, int64_t cols, int64_t ld, int64_t capacity_ro
   const int64_t cap = capacity_rows > rows ? capacity_rows : rows;
   const size_t count = static_cast<size_t>((cap > 0 ? cap : 1) * (ld > 0 ? ld : 1));
   buf.resize(count);
+  // The zeroing runs on the legacy stream, which does not order against the
+  // trainers' non-blocking streams: wait for it, or a lazily allocated tile
+  // (the kept T of a widening layer) could be zeroed after its first writes.
   CG_CUDA(cudaMemset(buf.get(), 0, count * sizeof(float)));
+  CG_CUDA(cudaStreamSynchronize(nullptr));
   m.p = buf.get();
   m.rows = rows;
   m.cols = cols;
@@ -284,6 +288,7 @@ Trainer::Trainer(const DeviceDataset& data, std::vector<int64_t> dims, const dou
   losses_dev_.resize(4096);
   loss_slot_.resize(1);
   CG_CUDA(cudaMemset(loss_slot_.get(), 0, sizeof(int)));
+  CG_CUDA(cudaStreamSynchronize(nullptr));  // legacy-stream zeroing before the trainer's streams run
 }
 
 Trainer::~Trainer() {
@@ -321,8 +326,50 @@ const int2* Trainer::colval(const int32_t* ci, const float* v, int64_t nnz) {
   return colval_.emplace(key, std::move(buf)).first->second.get();
 }
 
+const kern::SpmmPacked* Trainer::packed(const DeviceCsr& a) {
+  static const bool on = [] {
+    const char* e = std::getenv("CAGNET_SPMM_PACK");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || a.nnz <= 0 || a.n_rows <= 0) return nullptr;
+  const auto key = std::make_pair(static_cast<const void*>(a.col_idx.get()),
+                                  static_cast<const void*>(a.vals.get()));
+  auto it = packed_.find(key);
+  if (it != packed_.end()) return it->second.view.e ? &it->second.view : nullptr;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  CG_CUDA(cudaStreamIsCapturing(cs_, &st));
+  if (st != cudaStreamCaptureStatusNone) return nullptr;  // no allocation inside a capture
+  const int64_t n = data_.adj.n_rows;
+  PackedCsr pc;
+  // Column bits for the block's local columns; the degree takes the rest.
+  int bits = 1;
+  while (bits < 31 && (int64_t{1} << bits) < a.n_cols) ++bits;
+  const bool fits = a.row_off >= 0 && a.col_off >= 0 && a.row_off + a.n_rows <= n &&
+                    a.col_off + a.n_cols <= n && bits <= 28;
+  if (fits) {
+    if (!deg_.get()) {
+      deg_.resize(static_cast<size_t>(n));
+      kern::row_degrees(n, data_.adj.row_ptr.get(), deg_.get(), cs_);
+    }
+    pc.e.resize(static_cast<size_t>(a.nnz));
+    pc.row_scale.resize(static_cast<size_t>(a.n_rows));
+    DevBuf<unsigned long long> bad(1);
+    CG_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned long long), cs_));
+    kern::pack_normalized(a.n_rows, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), deg_.get(), a.row_off,
+                          a.col_off, bits, pc.e.get(), pc.row_scale.get(), bad.get(), cs_);
+    unsigned long long nbad = 0;
+    CG_CUDA(cudaMemcpyAsync(&nbad, bad.get(), sizeof(nbad), cudaMemcpyDeviceToHost, cs_));
+    CG_CUDA(cudaStreamSynchronize(cs_));
+    if (nbad == 0) pc.view = kern::SpmmPacked{pc.e.get(), pc.row_scale.get(), bits};
+  }
+  if (!pc.view.e) pc = PackedCsr{};  // not a normalized block: keep the int2 stream
+  auto ins = packed_.emplace(key, std::move(pc)).first;
+  return ins->second.view.e ? &ins->second.view : nullptr;
+}
+
 void Trainer::init_tiles() {
   colval_.clear();
+  packed_.clear();
   colblocks_.clear();  // keyed by row_ptr addresses, which a new distribute() may reuse
   const int L = num_layers();
   const BlockRange rows = tile_rows(rank_);
@@ -396,11 +443,11 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const ke
   const int nb = spmm_passes(a, h);
   if (epi) {
     if (nb > 1) throw std::logic_error("spmm: fused epilogue needs one pass");
-    spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, acc, epi);
+    spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, acc, epi, true, &a);
     return;
   }
   if (nb <= 1 || a.nnz == 0 || out.rows != a.n_rows || out.cols != h.cols) {
-    spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, acc);
+    spmm_raw(a.n_rows, a.nnz, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), h, out, acc, nullptr, true, &a);
     return;
   }
   // Column blocks materialised once per (matrix, pass count) as contiguous
@@ -417,9 +464,11 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const ke
     it = colblocks_.emplace(key, std::move(blocks)).first;
   }
   std::vector<const int2*> cvs;
+  std::vector<const kern::SpmmPacked*> pks;
   for (int b = 0; b < nb; ++b) {
     const DeviceCsr& blk = it->second[static_cast<size_t>(b)];
-    cvs.push_back(colval(blk.col_idx.get(), blk.vals.get(), blk.nnz));
+    pks.push_back(packed(blk));
+    cvs.push_back(pks.back() ? nullptr : colval(blk.col_idx.get(), blk.vals.get(), blk.nnz));
   }
   const int slot = prof_begin();
   for (int b = 0; b < nb; ++b) {
@@ -427,7 +476,7 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const ke
     const BlockRange cr = block_range(a.n_cols, nb, b);
     kern::spmm_csr(blk.n_rows, blk.row_ptr.get(), blk.col_idx.get(), blk.vals.get(), h.p + cr.begin * h.ld,
                    h.ld, static_cast<int>(h.cols), out.p, out.ld, acc || b > 0, cs_, blk.nnz, nullptr,
-                   cvs[static_cast<size_t>(b)]);
+                   cvs[static_cast<size_t>(b)], pks[static_cast<size_t>(b)]);
   }
   if (slot >= 0) {
     const double f = static_cast<double>(h.cols), r = static_cast<double>(a.n_rows);
@@ -445,15 +494,16 @@ double Trainer::l2_panel_bytes() {
 
 void Trainer::spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32_t* ci,
                        const float* v, const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi,
-                       bool stable) {
+                       bool stable, const DeviceCsr* src) {
   const int64_t width = epi && epi->W ? epi->fo : h.cols;
   if (out.rows != rows || out.cols != width)
     throw std::invalid_argument("spmm: accumulator shape mismatch");
   // nnz here is the length of the (0-based) arrays, so the interleaved copy covers every row.
-  const int2* cv = stable ? colval(ci, v, nnz) : nullptr;
+  const kern::SpmmPacked* pk = stable && src && src->col_idx.get() == ci ? packed(*src) : nullptr;
+  const int2* cv = stable && !pk ? colval(ci, v, nnz) : nullptr;
   const int slot = prof_begin();
   kern::spmm_csr(rows, rp, ci, v, h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld, acc, cs_, nnz,
-                 epi, cv);
+                 epi, cv, pk);
   if (slot >= 0) {
     // B = 8(r+1) + 8 nnz + 4 f c + 4 f r (1 + acc); F = 2 nnz f;
     // plus the fused epilogue's extra row traffic (raw copy, relu′ mask, relu).
@@ -764,7 +814,9 @@ void Trainer::flush_losses() {
   std::vector<double> tot(static_cast<size_t>(pending));
   if (pending) {
     CG_CUDA(cudaMemcpy(tot.data(), losses_dev_.get(), pending * sizeof(double), cudaMemcpyDeviceToHost));
-    CG_CUDA(cudaMemset(loss_slot_.get(), 0, sizeof(int)));
+    // On the compute stream: later pushes (comm stream, behind an event on
+    // it) must see the reset.
+    CG_CUDA(cudaMemsetAsync(loss_slot_.get(), 0, sizeof(int), cs_));
   }
   for (double t : tot) losses_host_.push_back(t / static_cast<double>(train_total_));
   epochs_read_ = epochs_done_;

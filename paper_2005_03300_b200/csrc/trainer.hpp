@@ -245,8 +245,10 @@ class Trainer {
                 const float* v, const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi, const char* kind);
   // stable = false: the CSR arrays are a scratch buffer whose contents change
   // between calls (no interleaved copy is cached for them).
+  // src (optional): the block these arrays belong to, for the packed stream.
   void spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32_t* ci, const float* v,
-                const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi = nullptr, bool stable = true);
+                const Mat& h, Mat out, bool acc, const kern::SpmmEpi* epi = nullptr, bool stable = true,
+                const DeviceCsr* src = nullptr);
   // True when spmm(a, h, ...) is a single kernel pass (no L2 column blocking).
   bool spmm_single_pass(const DeviceCsr& a, const Mat& h) const;
   int spmm_passes(const DeviceCsr& a, const Mat& h) const;
@@ -321,6 +323,17 @@ class Trainer {
   // (CAGNET_SPMM_CV=0 disables them).
   std::map<std::pair<const void*, const void*>, DevBuf<int2>> colval_;
   const int2* colval(const int32_t* ci, const float* v, int64_t nnz);
+  // Packed streams (kern::SpmmPacked) of blocks of the normalized adjacency,
+  // keyed like colval_; a block whose values fail the check maps to an empty
+  // entry (CAGNET_SPMM_PACK=0 disables them).  deg_: degrees of A + I.
+  struct PackedCsr {
+    DevBuf<uint32_t> e;
+    DevBuf<float> row_scale;
+    kern::SpmmPacked view;
+  };
+  std::map<std::pair<const void*, const void*>, PackedCsr> packed_;
+  DevBuf<int32_t> deg_;
+  const kern::SpmmPacked* packed(const DeviceCsr& a);
   static double l2_panel_bytes();
   DevBuf<double> losses_dev_;
   DevBuf<int> loss_slot_;  // device-side write index into losses_dev_
