@@ -463,21 +463,34 @@ void* stream_scratch(cudaStream_t s, size_t bytes) {
   };
   static std::mutex mu;
   static std::map<cudaStream_t, Entry> cache;
-  std::lock_guard<std::mutex> lk(mu);
-  Entry& e = cache[s];
-  if (e.bytes >= bytes && e.p) return e.p;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    const Entry& e = cache[s];
+    if (e.bytes >= bytes && e.p) return e.p;
+  }
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
   CG_CUDA(cudaStreamIsCapturing(s, &st));
   if (st != cudaStreamCaptureStatusNone)
     throw std::logic_error("stream_scratch: workspace growth inside a graph capture");
-  if (e.p) {
-    CG_CUDA(cudaStreamSynchronize(s));
-    CG_CUDA(cudaFree(e.p));
-  }
+  // Stream-ordered growth: the old workspace is released behind the work
+  // already queued on s, and nothing here blocks the host.  (The previous
+  // form synchronised s and cudaFree'd under the lock: with one host thread
+  // per rank, a rank whose stream held a collective waiting for a peer kept
+  // the lock while the peer's thread blocked on it before launching its side
+  // of that collective — a deadlock on the first growth of an NCCL run.)
   const size_t want = bytes + bytes / 4 + 256;
-  CG_CUDA(cudaMalloc(&e.p, want));
-  e.bytes = want;
-  return e.p;
+  void* p = nullptr;
+  CG_CUDA(cudaMallocAsync(&p, want, s));
+  void* old = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    Entry& e = cache[s];
+    old = e.p;
+    e.p = p;
+    e.bytes = want;
+  }
+  if (old) CG_CUDA(cudaFreeAsync(old, s));
+  return p;
 }
 
 }  // namespace cagnet

@@ -63,6 +63,7 @@ class TrainerRows final : public Trainer {
         }
       }
     }
+    prepare_streams();
     settle();
   }
 
@@ -584,6 +585,14 @@ class TrainerRows final : public Trainer {
 
   // A pushed exchange that no stage consumed still has to be waited for, so
   // the device-side wait count stays in step with the publish count.
+  std::vector<const DeviceCsr*> stream_csrs() const override {
+    std::vector<const DeviceCsr*> v = Trainer::stream_csrs();
+    if (chunk_ok_) {
+      v.push_back(&a_chunk_);
+      v.push_back(&at_chunk_);
+    }
+    return v;
+  }
   void settle_pending() {
     if (!pending_.valid) return;
     pending_.valid = false;

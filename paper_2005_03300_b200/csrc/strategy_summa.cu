@@ -107,6 +107,7 @@ class TrainerSumma final : public Trainer {
     strip_.alloc(fmax_cols, fmax_cols, fmax_cols);  // Y strips: f_in / √P x f_out / √P
     buf_w_ = 0;
     size_buffers();
+    prepare_streams();
     settle();
   }
 
@@ -268,6 +269,9 @@ class TrainerSumma final : public Trainer {
 
  private:
   void begin_epoch() override { slot_ = 0; }
+  // The SUMMA SpMMs stream the resident / broadcast tiles (spmm_raw without a
+  // block), never a_parts_ directly: no packed copies.
+  std::vector<const DeviceCsr*> stream_csrs() const override { return {}; }
   int64_t buf_w_ = 0;  // width the large panels are sized for
   int side() const { return grid_.rows(); }
   int layers() const { return grid_.layers(); }

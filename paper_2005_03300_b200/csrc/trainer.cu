@@ -326,7 +326,18 @@ const int2* Trainer::colval(const int32_t* ci, const float* v, int64_t nnz) {
   return colval_.emplace(key, std::move(buf)).first->second.get();
 }
 
-const kern::SpmmPacked* Trainer::packed(const DeviceCsr& a) {
+std::vector<const DeviceCsr*> Trainer::stream_csrs() const {
+  std::vector<const DeviceCsr*> v;
+  for (const DeviceCsr& c : a_parts_) v.push_back(&c);
+  for (const DeviceCsr& c : at_parts_) v.push_back(&c);
+  return v;
+}
+
+void Trainer::prepare_streams() {
+  for (const DeviceCsr* c : stream_csrs()) packed(*c, true);
+}
+
+const kern::SpmmPacked* Trainer::packed(const DeviceCsr& a, bool build) {
   static const bool on = [] {
     const char* e = std::getenv("CAGNET_SPMM_PACK");
     return !(e && e[0] == '0');
@@ -336,9 +347,7 @@ const kern::SpmmPacked* Trainer::packed(const DeviceCsr& a) {
                                   static_cast<const void*>(a.vals.get()));
   auto it = packed_.find(key);
   if (it != packed_.end()) return it->second.view.e ? &it->second.view : nullptr;
-  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-  CG_CUDA(cudaStreamIsCapturing(cs_, &st));
-  if (st != cudaStreamCaptureStatusNone) return nullptr;  // no allocation inside a capture
+  if (!build) return nullptr;
   const int64_t n = data_.adj.n_rows;
   PackedCsr pc;
   // Column bits for the block's local columns; the degree takes the rest.

@@ -333,7 +333,13 @@ class Trainer {
   };
   std::map<std::pair<const void*, const void*>, PackedCsr> packed_;
   DevBuf<int32_t> deg_;
-  const kern::SpmmPacked* packed(const DeviceCsr& a);
+  // build = false (every call inside an epoch): only a stream prepared at
+  // distribute() — building one needs a host read of the check, and a host
+  // sync mid-epoch can deadlock ranks whose streams wait on each other.
+  const kern::SpmmPacked* packed(const DeviceCsr& a, bool build = false);
+  // Builds the packed streams of stream_csrs() (end of distribute()).
+  void prepare_streams();
+  virtual std::vector<const DeviceCsr*> stream_csrs() const;
   static double l2_panel_bytes();
   DevBuf<double> losses_dev_;
   DevBuf<int> loss_slot_;  // device-side write index into losses_dev_
