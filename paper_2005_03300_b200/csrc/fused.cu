@@ -462,10 +462,15 @@ void* stream_scratch(cudaStream_t s, size_t bytes) {
     size_t bytes = 0;
   };
   static std::mutex mu;
-  static std::map<cudaStream_t, Entry> cache;
+  // Keyed by device too: a destroyed stream's handle can come back for a
+  // stream of another device, and pool memory is not accessible across devices.
+  static std::map<std::pair<int, cudaStream_t>, Entry> cache;
+  int dev = 0;
+  CG_CUDA(cudaGetDevice(&dev));
+  const auto key = std::make_pair(dev, s);
   {
     std::lock_guard<std::mutex> lk(mu);
-    const Entry& e = cache[s];
+    const Entry& e = cache[key];
     if (e.bytes >= bytes && e.p) return e.p;
   }
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
@@ -484,7 +489,7 @@ void* stream_scratch(cudaStream_t s, size_t bytes) {
   void* old = nullptr;
   {
     std::lock_guard<std::mutex> lk(mu);
-    Entry& e = cache[s];
+    Entry& e = cache[key];
     old = e.p;
     e.p = p;
     e.bytes = want;
