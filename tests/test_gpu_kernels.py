@@ -198,6 +198,7 @@ TM_CASES = [
     (40000, 16, 16, 0, 0),     # H·W (16 -> 16)
     (30000, 24, 16, 0, 1),     # S·Wᵀ (16 -> 24)
     (16, 16, 70000, 1, 0),     # Hᵀ·S, the 16-wide weight gradient
+    (16, 16, 232965, 1, 0),    # Hᵀ·S at Reddit's K (8 K-row splits folded in fp64)
     # >= 1 M rows: the CUDA-core narrow x narrow kernels (gemm_small.cu)
     (1000003, 16, 16, 0, 0),   # H·W (16 -> 16), Amazon / Protein hidden layers (quad kernel)
     (1000003, 16, 16, 0, 1),   # S·Wᵀ (16 -> 16), quad kernel with a transposed B
