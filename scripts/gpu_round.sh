@@ -8,6 +8,7 @@ nvidia-smi > $O/nvsmi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q --timeout 900 -p no:cacheprovider -rf > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "rc=$?" >> $O/smoke.log
 timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench.log 2>&1; echo "rc=$?" >> $O/bench.log
+timeout 900 python bench.py --config amazon --steps 3 --warmup 3 --no-cpu-baseline --no-alt > $O/bench_amazon.log 2>&1; echo "rc=$?" >> $O/bench_amazon.log
 [ -n "$SKIP_NCU" ] && exit 0
 CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-alt"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file $O/launches.csv $CMD > $O/ncu_launch.log 2>&1
