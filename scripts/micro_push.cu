@@ -132,7 +132,8 @@ bool setup_mc(size_t bytes, float4** mc_ptr, float4** uc) {
 int main(int argc, char** argv) {
   CK(cudaGetDeviceCount(&G));
   if (G > MAXG) G = MAXG;
-  const int64_t n = 232965;
+  // argv[1]: graph rows multiplier (1 = Reddit: a 16-float panel of 232,965 rows).
+  const int64_t n = 232965LL * (argc > 1 ? atoi(argv[1]) : 1);
   rows = (n + G - 1) / G;
   const int64_t n4 = rows * 4;  // 16 floats per row
   printf("GPUs %d, rows per slot %lld (%.2f MB)\n", G, (long long)rows, rows * 64 / 1e6);
