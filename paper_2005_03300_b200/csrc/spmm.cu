@@ -106,7 +106,7 @@ struct SpmmArgs {
   // Optional interleaved copy of (col_idx, vals) as int2 {col, float bits}:
   // one 8 B load per nonzero instead of two 4 B loads (narrow-row kernel).
   const int2* colval = nullptr;
-  SpmmPacked packed;  // packed.e != nullptr: the packed stream (narrow-row kernel, LV = 4)
+  SpmmPacked packed;  // packed.e != nullptr: the packed stream (narrow-row kernel, LV = 2 / 4)
 };
 
 // VEC = 4: 16-byte vectors (requires 16 B aligned rows, ld a multiple of 4); VEC = 1: scalars.
@@ -386,6 +386,10 @@ __device__ __forceinline__ void spmm_row_epilogue(const SpmmArgs& a, int64_t row
 // ~10 % of its time (profiles/r02_micro_packed_stream.txt).
 template <int LV, int QPR, int U, bool ACC, int CV, int NT = kThreads, int HINT = 0,
           bool FULLV = false, bool EPI = false>
+// Full occupancy (32 registers): the gathers need every warp in flight.  The
+// fused-epilogue variants of short rows (teams of < 16 lanes) spill in their
+// epilogue at 32, and are still faster than at 64 registers and half the
+// warps (Amazon-shaped SpMM 5.14 -> 5.34 ms with 64).
 __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArgs a) {
   constexpr int TEAM = LV * QPR;
   constexpr int RPW = 32 / TEAM;
@@ -456,6 +460,7 @@ __global__ void __launch_bounds__(NT, 2048 / NT) spmm_nzpar_kernel(const SpmmArg
 #pragma unroll
       for (int u = 0; u < U; ++u) fma_vec(acc, w[u], h[u]);
     }
+#pragma unroll 1
     for (; p < pe; p += QPR) {
       const uint32_t x = __ldg(p);
       fma_vec(acc, weight(x), gather(static_cast<int>(x & cmask)));
@@ -583,7 +588,7 @@ void launch_nzpar_v(const SpmmArgs& a, bool acc, bool epi, cudaStream_t s) {
   const unsigned g = static_cast<unsigned>(ceil_div64(a.n_rows, rows_per_block));
   // Full vectors: every lane of the LV-wide row team owns a live float4.
   const bool full = (a.f + 3) / 4 == LV;
-  if constexpr (LV == 4) {
+  if constexpr (LV == 2 || LV == 4) {
     if (a.packed.e) {
       launch_nzpar_cv<LV, QPR, U, NT, HINT, 2>(a, acc, epi, g, full, s);
       CG_LAUNCH_CHECK();

@@ -99,6 +99,14 @@ class TrainerSumma final : public Trainer {
       }
       CG_CUDA(cudaStreamSynchronize(ms_));
       comm_->restore(saved);
+      // Packed streams of the resident tiles: tile q is block (i, (q, k)) of
+      // A / Aᵀ, the rows of block row i and the columns subrows(q, k).
+      for (int o = 0; o < 2; ++o)
+        for (int q = 0; q < side(); ++q) {
+          const SparsePanel& sp = resident_[o][static_cast<size_t>(q)];
+          build_packed(sp.rows, sp.cols, sp.nnz, sp.row_ptr.get(), sp.col.get(), sp.vals.get(), arows.begin,
+                       subrows(q, k).begin);
+        }
     }
 
     int64_t maxall = 0;

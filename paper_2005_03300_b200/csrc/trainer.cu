@@ -334,46 +334,49 @@ std::vector<const DeviceCsr*> Trainer::stream_csrs() const {
 }
 
 void Trainer::prepare_streams() {
-  for (const DeviceCsr* c : stream_csrs()) packed(*c, true);
+  for (const DeviceCsr* c : stream_csrs())
+    build_packed(c->n_rows, c->n_cols, c->nnz, c->row_ptr.get(), c->col_idx.get(), c->vals.get(), c->row_off,
+                 c->col_off);
 }
 
-const kern::SpmmPacked* Trainer::packed(const DeviceCsr& a, bool build) {
+const kern::SpmmPacked* Trainer::packed(const int32_t* ci, const float* v) const {
+  auto it = packed_.find(std::make_pair(static_cast<const void*>(ci), static_cast<const void*>(v)));
+  return it != packed_.end() && it->second.view.e ? &it->second.view : nullptr;
+}
+
+void Trainer::build_packed(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rp, const int32_t* ci,
+                           const float* v, int64_t row_off, int64_t col_off) {
   static const bool on = [] {
     const char* e = std::getenv("CAGNET_SPMM_PACK");
     return !(e && e[0] == '0');
   }();
-  if (!on || a.nnz <= 0 || a.n_rows <= 0) return nullptr;
-  const auto key = std::make_pair(static_cast<const void*>(a.col_idx.get()),
-                                  static_cast<const void*>(a.vals.get()));
-  auto it = packed_.find(key);
-  if (it != packed_.end()) return it->second.view.e ? &it->second.view : nullptr;
-  if (!build) return nullptr;
+  if (!on || nnz <= 0 || rows <= 0) return;
+  const auto key = std::make_pair(static_cast<const void*>(ci), static_cast<const void*>(v));
+  if (packed_.count(key)) return;
   const int64_t n = data_.adj.n_rows;
   PackedCsr pc;
   // Column bits for the block's local columns; the degree takes the rest.
   int bits = 1;
-  while (bits < 31 && (int64_t{1} << bits) < a.n_cols) ++bits;
-  const bool fits = a.row_off >= 0 && a.col_off >= 0 && a.row_off + a.n_rows <= n &&
-                    a.col_off + a.n_cols <= n && bits <= 28;
+  while (bits < 31 && (int64_t{1} << bits) < cols) ++bits;
+  const bool fits = row_off >= 0 && col_off >= 0 && row_off + rows <= n && col_off + cols <= n && bits <= 28;
   if (fits) {
     if (!deg_.get()) {
       deg_.resize(static_cast<size_t>(n));
       kern::row_degrees(n, data_.adj.row_ptr.get(), deg_.get(), cs_);
     }
-    pc.e.resize(static_cast<size_t>(a.nnz));
-    pc.row_scale.resize(static_cast<size_t>(a.n_rows));
+    pc.e.resize(static_cast<size_t>(nnz));
+    pc.row_scale.resize(static_cast<size_t>(rows));
     DevBuf<unsigned long long> bad(1);
     CG_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(unsigned long long), cs_));
-    kern::pack_normalized(a.n_rows, a.row_ptr.get(), a.col_idx.get(), a.vals.get(), deg_.get(), a.row_off,
-                          a.col_off, bits, pc.e.get(), pc.row_scale.get(), bad.get(), cs_);
+    kern::pack_normalized(rows, rp, ci, v, deg_.get(), row_off, col_off, bits, pc.e.get(), pc.row_scale.get(),
+                          bad.get(), cs_);
     unsigned long long nbad = 0;
     CG_CUDA(cudaMemcpyAsync(&nbad, bad.get(), sizeof(nbad), cudaMemcpyDeviceToHost, cs_));
     CG_CUDA(cudaStreamSynchronize(cs_));
     if (nbad == 0) pc.view = kern::SpmmPacked{pc.e.get(), pc.row_scale.get(), bits};
   }
   if (!pc.view.e) pc = PackedCsr{};  // not a normalized block: keep the int2 stream
-  auto ins = packed_.emplace(key, std::move(pc)).first;
-  return ins->second.view.e ? &ins->second.view : nullptr;
+  packed_.emplace(key, std::move(pc));
 }
 
 void Trainer::init_tiles() {
@@ -476,7 +479,7 @@ void Trainer::spmm(const DeviceCsr& a, const Mat& h, Mat out, bool acc, const ke
   std::vector<const kern::SpmmPacked*> pks;
   for (int b = 0; b < nb; ++b) {
     const DeviceCsr& blk = it->second[static_cast<size_t>(b)];
-    pks.push_back(packed(blk));
+    pks.push_back(packed(blk.col_idx.get(), blk.vals.get()));
     cvs.push_back(pks.back() ? nullptr : colval(blk.col_idx.get(), blk.vals.get(), blk.nnz));
   }
   const int slot = prof_begin();
@@ -508,7 +511,8 @@ void Trainer::spmm_raw(int64_t rows, int64_t nnz, const int64_t* rp, const int32
   if (out.rows != rows || out.cols != width)
     throw std::invalid_argument("spmm: accumulator shape mismatch");
   // nnz here is the length of the (0-based) arrays, so the interleaved copy covers every row.
-  const kern::SpmmPacked* pk = stable && src && src->col_idx.get() == ci ? packed(*src) : nullptr;
+  (void)src;
+  const kern::SpmmPacked* pk = stable ? packed(ci, v) : nullptr;
   const int2* cv = stable && !pk ? colval(ci, v, nnz) : nullptr;
   const int slot = prof_begin();
   kern::spmm_csr(rows, rp, ci, v, h.p, h.ld, static_cast<int>(h.cols), out.p, out.ld, acc, cs_, nnz,

@@ -333,10 +333,13 @@ class Trainer {
   };
   std::map<std::pair<const void*, const void*>, PackedCsr> packed_;
   DevBuf<int32_t> deg_;
-  // build = false (every call inside an epoch): only a stream prepared at
-  // distribute() — building one needs a host read of the check, and a host
-  // sync mid-epoch can deadlock ranks whose streams wait on each other.
-  const kern::SpmmPacked* packed(const DeviceCsr& a, bool build = false);
+  // The packed stream built for these arrays, if any.  Built only in
+  // distribute() (build_packed / prepare_streams): the check needs a host
+  // read, and a host sync mid-epoch can deadlock ranks whose streams wait on
+  // each other.
+  const kern::SpmmPacked* packed(const int32_t* ci, const float* v) const;
+  void build_packed(int64_t rows, int64_t cols, int64_t nnz, const int64_t* rp, const int32_t* ci,
+                    const float* v, int64_t row_off, int64_t col_off);
   // Builds the packed streams of stream_csrs() (end of distribute()).
   void prepare_streams();
   virtual std::vector<const DeviceCsr*> stream_csrs() const;
