@@ -87,3 +87,52 @@ def test_packed_stream_matches_interleaved(tmp_path, need_gpus):
     errs = {k: rel(res["1"][k], res["0"][k]) for k in res["0"].files}
     assert max(errs.values()) < 1e-5, errs
     assert any(v > 0 for v in errs.values()), "the packed stream did not engage"
+
+
+TAMPER_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[3])
+import paper_2005_03300_b200 as cg
+d = cg.load_dataset_binary(sys.argv[1], device=0)
+dims = [16, 16, 16, 4]
+out = cg.run_distributed(d, cg.init_glorot(dims, 4, 0.5), cg.Strategy("1d", 1, reassociate=True), 3)
+np.savez(sys.argv[2], h=out.h_final, y0=out.y_final[0], y1=out.y_final[1], losses=np.asarray(out.losses))
+"""
+
+
+def test_packed_stream_falls_back_off_normalized_values(cg, tmp_path, need_gpus):
+    """A dataset whose adjacency values are not 1/sqrt(d_r d_c) (a binary cache
+    with every value scaled by 1.01, A and Aᵀ alike) fails the packed stream's
+    check at distribute(): the SpMMs keep the interleaved stream, so the run
+    is bitwise the CAGNET_SPMM_PACK=0 run — while on the untampered cache the
+    packed stream engages (results differ in the last bits)."""
+    need_gpus(1)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    d = cg.generate_dataset(3000, 24.0, 16, 4, 1, 2, 3, device=0)
+    clean = str(tmp_path / "clean.bin")
+    d.save(clean)
+    n, nnz, nnz_t = d.n, None, None
+    raw = bytearray(open(clean, "rb").read())
+    hdr = np.frombuffer(bytes(raw[8:8 + 48]), dtype=np.int64)
+    assert hdr[0] == n
+    nnz, nnz_t = int(hdr[4]), int(hdr[5])
+    off = 8 + 48
+    for m in (nnz, nnz_t):
+        off += (n + 1) * 8 + m * 4
+        vals = np.frombuffer(bytes(raw[off:off + m * 4]), dtype=np.float32) * np.float32(1.01)
+        raw[off:off + m * 4] = vals.astype(np.float32).tobytes()
+        off += m * 4
+    tampered = str(tmp_path / "tampered.bin")
+    open(tampered, "wb").write(bytes(raw))
+    res = {}
+    for name, path in (("clean", clean), ("tampered", tampered)):
+        for pack in ("1", "0"):
+            outp = str(tmp_path / f"{name}{pack}.npz")
+            subprocess.run([sys.executable, "-c", TAMPER_SCRIPT, path, outp, root], check=True,
+                           env=dict(os.environ, CAGNET_SPMM_PACK=pack), timeout=300)
+            res[name + pack] = np.load(outp)
+    for k in res["tampered0"].files:
+        assert np.array_equal(res["tampered1"][k], res["tampered0"][k]), k
+    assert any(not np.array_equal(res["clean1"][k], res["clean0"][k]) for k in res["clean0"].files)
+    errs = {k: rel(res["clean1"][k], res["clean0"][k]) for k in res["clean0"].files}
+    assert max(errs.values()) < 1e-5, errs
