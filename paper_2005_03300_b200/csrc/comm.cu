@@ -2,6 +2,8 @@
 
 #include "comm.hpp"
 
+#include "nvtx.hpp"
+
 namespace cagnet {
 
 namespace {
@@ -97,6 +99,7 @@ ncclComm_t Comm::comm_for(const Group& g) const {
 
 void Comm::bcast(const Group& g, int root_rank, void* buf, size_t count, ncclDataType_t t,
                  Category cat, uint64_t words, cudaStream_t s) {
+  NvtxRange nvtx_range("comm bcast");
   (void)g.index_of(rank_);
   const int root = g.index_of(root_rank);
   if (g.size() == 1) return;
@@ -117,6 +120,7 @@ void Comm::bcast(const Group& g, int root_rank, void* buf, size_t count, ncclDat
 
 void Comm::bcast_csr(const Group& g, int root_rank, int64_t* row_ptr, int64_t n_rows,
                      int32_t* col, float* vals, int64_t nnz, Category cat, cudaStream_t s) {
+  NvtxRange nvtx_range("comm bcast_csr");
   (void)g.index_of(rank_);
   const int root = g.index_of(root_rank);
   if (g.size() == 1) return;
@@ -147,6 +151,7 @@ void Comm::bcast_csr(const Group& g, int root_rank, int64_t* row_ptr, int64_t n_
 
 void Comm::all_reduce(const Group& g, void* buf, size_t count, ncclDataType_t t, Category cat,
                       uint64_t words, cudaStream_t s) {
+  NvtxRange nvtx_range("comm all_reduce");
   const int member = g.index_of(rank_);
   if (g.size() == 1) return;
   if (local_)
@@ -166,6 +171,7 @@ void Comm::all_reduce(const Group& g, void* buf, size_t count, ncclDataType_t t,
 void Comm::reduce_scatter(const Group& g, const void* send, void* recv, size_t slice_count,
                           ncclDataType_t t, Category cat, const std::vector<uint64_t>& slot_words,
                           cudaStream_t s) {
+  NvtxRange nvtx_range("comm reduce_scatter");
   const int member = g.index_of(rank_);
   if (g.size() == 1) return;
   if (local_)
@@ -186,6 +192,7 @@ void Comm::reduce_scatter(const Group& g, const void* send, void* recv, size_t s
 void Comm::all_gather(const Group& g, const void* send, void* recv, size_t slice_count,
                       ncclDataType_t t, Category cat, const std::vector<uint64_t>& slot_words,
                       cudaStream_t s) {
+  NvtxRange nvtx_range("comm all_gather");
   const int member = g.index_of(rank_);
   if (g.size() == 1) return;
   if (local_)

@@ -10,6 +10,7 @@
 #include "kernels.cuh"
 #include "rng.hpp"
 
+#include "nvtx.hpp"
 #include "trainer.hpp"
 
 namespace cagnet {
@@ -757,8 +758,16 @@ void Trainer::run_forward_layer(int l) {
 
 void Trainer::epoch_body() {
   begin_epoch();
-  for (int l = 1; l < num_layers(); ++l) forward_layer(l);
-  backward_and_step();
+  static const char* const kLayerNames[] = {"forward_layer 1", "forward_layer 2", "forward_layer 3",
+                                            "forward_layer 4", "forward_layer 5", "forward_layer"};
+  for (int l = 1; l < num_layers(); ++l) {
+    NvtxRange r(kLayerNames[l <= 5 ? l - 1 : 5]);
+    forward_layer(l);
+  }
+  {
+    NvtxRange r("backward_and_step");
+    backward_and_step();
+  }
   cs_after_ms();  // join the comm stream (graph capture needs every fork joined)
 }
 
@@ -777,6 +786,7 @@ void Trainer::epoch() {
   if (epochs_done_ - epochs_read_ >= static_cast<int>(losses_dev_.count)) flush_losses();
   // Per-kernel timing events stay eager (collect_profile reads every launch).
   if (!use_graph_ || timing_ || !graph_warm_) {
+    NvtxRange r("epoch (eager)");
     // Eager.  The first graph-mode epoch is eager too: lazy allocations
     // (split tables, workspaces) and kernel attributes happen outside capture.
     CG_CUDA(cudaEventRecord(ev_t0_, cs_));
@@ -785,6 +795,7 @@ void Trainer::epoch() {
     if (use_graph_ && !timing_) graph_warm_ = true;
     return;
   }
+  NvtxRange r(graph_exec_ ? "epoch (graph replay)" : "epoch (capture + replay)");
   if (!graph_exec_) {
     const size_t notes0 = prered_.size();
     comm_->snapshot(ledger_before_);
