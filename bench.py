@@ -541,9 +541,34 @@ def run_ours(args, cfg):
         "loss_last": float(losses[-1]) if len(losses) else None,
         "setup_s": {"dataset_gen": round(gen_s, 2)},
     }
+    if world > 1:
+        line["parity"] = serial_parity(cg, data, cfg, strat, losses) if rank == 0 else None
     print(json.dumps(line))
     if pg:
         pg.destroy_process_group()
+
+
+def serial_parity(cg, data, cfg, strat, losses, tol=1e-4):
+    """Every multi-GPU bench run checks its own numbers: rank 0 trains a P = 1 trainer (the
+    serial step, gnn.cpp:68-132) on its copy of the same graph, same initial weights, and
+    compares the first epochs' losses with the distributed run's (the tolerance of the
+    strategy-vs-serial tests, tests/test_gpu_training.py)."""
+    k = int(min(len(losses), 4))
+    if k == 0:
+        return None
+    serial = cg.make_trainer(data, cg.init_glorot(cfg["dims"], SEED_W, LR),
+                             cg.Strategy("1d", 1, 1, reassociate=strat.reassociate, fuse=strat.fuse),
+                             0, None)
+    try:
+        serial.distribute()
+        serial.run_epochs(k)
+        ref = np.asarray(serial.losses()[:k], dtype=np.float64)
+    finally:
+        serial.free()
+    got = np.asarray(losses[:k], dtype=np.float64)
+    rel = float(np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-30)))
+    return {"vs": "P=1 trainer on rank 0, same graph and initial weights", "epochs": k,
+            "max_rel": rel, "tol": tol, "ok": bool(rel <= tol)}
 
 
 def main():
