@@ -56,6 +56,14 @@ constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr int kMaxStages = 8;
 constexpr int kMaxTmemStages = 8;         // A (hi + lo) stages in TMEM (upper bound)
 constexpr int kMaxResidentB = 96 * 1024;  // bytes of resident [B_hi; B_lo]
+// BN <= 16: accumulator chains and sets (build-time A/B knobs; TMEM left over
+// after the accumulators holds the A stages).
+#ifndef CAGNET_TM_CH16
+#define CAGNET_TM_CH16 4
+#endif
+#ifndef CAGNET_TM_SETS16
+#define CAGNET_TM_SETS16 2
+#endif
 
 // TMEM budget (512 columns): accumulator sets x chains x 2 BN, the rest holds
 // A stages of 64 columns (hi + lo).  The split-K Hᵀ·S kernel has one tile per
@@ -63,8 +71,8 @@ constexpr int kMaxResidentB = 96 * 1024;  // bytes of resident [B_hi; B_lo]
 // trip, not bandwidth, bounds a shallow ring).
 template <int BN, bool BSTREAM>
 struct Cfg {
-  static constexpr int CH = BN <= 16 ? 4 : BN <= 48 ? 2 : 1;       // accumulator chains
-  static constexpr int SETS = (BSTREAM || BN == 48) ? 1 : 2;       // accumulator sets
+  static constexpr int CH = BN <= 16 ? CAGNET_TM_CH16 : BN <= 48 ? 2 : 1;  // accumulator chains
+  static constexpr int SETS = (BSTREAM || BN == 48) ? 1 : BN <= 16 ? CAGNET_TM_SETS16 : 2;  // sets
   static constexpr uint32_t SET_COLS = CH * 2 * BN;
   static constexpr int TS_FIT = (512 - SETS * SET_COLS) / (2 * BK);
   static constexpr int TSTAGES = TS_FIT > kMaxTmemStages ? kMaxTmemStages : TS_FIT;
@@ -852,7 +860,7 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
       return false;
     p.nkb_res = nkb;
     p.k_chunk = static_cast<int64_t>(nkb) * BK;
-    p.chains = nkb >= 2 ? (bn <= 16 ? 4 : bn <= 48 ? 2 : 1) : 1;
+    p.chains = nkb >= 2 ? (bn <= 16 ? CAGNET_TM_CH16 : bn <= 48 ? 2 : 1) : 1;
     p.tstore = epi_maps(false) ? 1 : 0;
     const int grid = static_cast<int>(m_tiles < sms ? m_tiles : sms);
     launch_bn<0, false>(bn, maps, p, grid, stream);
@@ -891,7 +899,7 @@ bool gemm_tm_try(const GemmDesc& d, cudaStream_t stream) {
     if (splits < 1) splits = 1;
     p.k_chunk = ceil_div64(kblocks, splits) * BK;
     splits = ceil_div64(d.k, p.k_chunk);
-    p.chains = p.k_chunk / BK >= 2 ? (bn <= 16 ? 4 : bn <= 48 ? 2 : 1) : 1;
+    p.chains = p.k_chunk / BK >= 2 ? (bn <= 16 ? CAGNET_TM_CH16 : bn <= 48 ? 2 : 1) : 1;
     float* work = nullptr;
     if (splits > 1) {
       work = static_cast<float*>(
