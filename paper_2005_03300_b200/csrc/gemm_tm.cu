@@ -48,10 +48,7 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 32;
 constexpr int kConv = 128;                // converter threads per group
-#ifndef CAGNET_TM_CONV_GROUPS
-#define CAGNET_TM_CONV_GROUPS 2
-#endif
-constexpr int kConvGroups = CAGNET_TM_CONV_GROUPS;  // groups take alternate k-blocks (warps 2-5, 6-9)
+constexpr int kConvGroups = 2;            // groups take alternate k-blocks (warps 2-5, 6-9)
 constexpr int kEpi = 128;                 // epilogue threads (warps 10-13)
 constexpr int kEpiWarp0 = 2 + kConvGroups * kConv / 32;
 constexpr int kThreads = 64 + kConvGroups * kConv + kEpi;
